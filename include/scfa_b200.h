@@ -1,0 +1,204 @@
+/* scfa_b200.h — C ABI of the B200 Sparse Causal Flash Attention engine.
+ *
+ * Drop-in boundary for the QK-sparse and hash-sparse attention path of the
+ * reference `scfa` package (a NumPy package; its "FFI" is the Python API it
+ * exports from pkg/src/scfa/__init__.py:10-90).  Every entry point below
+ * replaces one reference function, cited as file:line under /root/reference.
+ *
+ * Conventions
+ *   - All pointers are DEVICE pointers; every call is stream-ordered on the
+ *     caller's `stream` (cudaStream_t passed as void*) and never synchronises.
+ *   - Caller owns every buffer (including workspace); the library allocates
+ *     nothing persistent.  Buffer sizes are stated per function.
+ *   - Return value: SCFA_OK or one of the SCFA_ERR_* codes, which map 1:1 to
+ *     the reference exception taxonomy (pkg/src/scfa/errors.py:4-29).
+ *     scfa_last_error() returns a thread-local message for the last failure.
+ *   - Data-dependent contract violations found on the device (keep values
+ *     outside {0,1}, negative bucket ids, unsorted batches ...) are reported
+ *     through an int32 `err_flag` in device memory (0 = ok, else SCFA_ERR_*),
+ *     so that the host decides when to synchronise.
+ *   - Layouts: boundary (B, T, H, D) and engine (B, H, T, D) are both
+ *     accepted through explicit element strides; attention operands are
+ *     engine-layout, contiguous, bf16.  Index/bucket vectors consumed by the
+ *     attention kernels are int32, one row of T_pad entries per (b, h)
+ *     (T_pad = round_up(T, 128)), produced by scfa_build_aux / scfa_pack_index.
+ */
+#ifndef SCFA_B200_H
+#define SCFA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SCFA_OK 0
+#define SCFA_ERR_SHAPE 1     /* ShapeError     (errors.py:8-9)   */
+#define SCFA_ERR_FORMAT 2    /* FormatError    (errors.py:12-17) */
+#define SCFA_ERR_PARAM 3     /* ParameterError (errors.py:20-21) */
+#define SCFA_ERR_NUMERIC 4   /* NumericError   (errors.py:24-25) */
+#define SCFA_ERR_CONTRACT 5  /* ContractError  (errors.py:28-29) */
+#define SCFA_ERR_CUDA 6      /* launch / driver failure (no reference analogue) */
+
+/* dtype codes for index-like inputs */
+#define SCFA_DT_F32 0
+#define SCFA_DT_F64 1
+#define SCFA_DT_U8 2
+#define SCFA_DT_I32 3
+#define SCFA_DT_I64 4
+
+/* attention flags */
+#define SCFA_FLAG_EXCLUDE_SELF 1 /* strict causality q_idx > k_idx (_kernel.py:83-84) */
+#define SCFA_FLAG_HASH 2         /* also require q_hash == k_hash (_kernel.py:87-88)  */
+
+int scfa_abi_version(void);
+const char* scfa_last_error(void);
+
+/* ---------------------------------------------------------------- QK prep
+ * Replaces compact()'s stable argsort of ~keep (pkg/src/scfa/qk_sparse.py:41-71).
+ * keep: (B,T,H) with element strides (sb, st, sh), dtype code `keep_dtype`,
+ *       entries must be 0 or 1 (else *err_flag = SCFA_ERR_SHAPE, qk_sparse.py:54-55).
+ * perm   (B*H, T) int32: slot -> position; kept positions ascending, then
+ *        dropped positions ascending == argsort(~kept, stable).
+ * rank   (B*H, T) int32: position -> slot (inverse of perm).
+ * counts (B*H)    int32: kept count per head (indices_per_head).            */
+int scfa_qk_compact(const void* keep, int keep_dtype, int64_t B, int64_t T, int64_t H, int64_t sb,
+                    int64_t st, int64_t sh, int32_t* perm, int32_t* rank, int32_t* counts,
+                    int32_t* err_flag, void* stream);
+
+/* ---------------------------------------------------------------- hash prep
+ * Replaces _bucket_order / sort_by_bucket's stable argsort
+ * (pkg/src/scfa/hash_sparse.py:89-133).  Stable LSD radix sort per (b,h) by
+ * bucket id; with `pos` given (element strides ps_bh, ps_t; dtype pos_dtype),
+ * the order is lexicographic (bucket, position) as the reference's
+ * hash*span+idx key.  Bucket ids must be in [0, 2^31) (negative -> ShapeError,
+ * hash_sparse.py:112-113).
+ * hash: element (b,h,t) at b*sb + h*sh + t*st.   perm/rank: (B*H, T) int32.
+ * scratch: (B*H, T) int32 workspace.                                          */
+int scfa_hash_sort(const void* hash, int hash_dtype, int64_t B, int64_t T, int64_t H, int64_t sb,
+                   int64_t st, int64_t sh, const void* pos, int pos_dtype, int64_t ps_bh,
+                   int64_t ps_t, int32_t* perm, int32_t* rank, int32_t* scratch, int32_t* err_flag,
+                   void* stream);
+
+/* ---------------------------------------------------------------- gather / scatter
+ * Row gather into engine layout (compact(...) take_along_axis, qk_sparse.py:68-70;
+ * sort_by_bucket gather_rows, hash_sparse.py:122-125) fused with the
+ * (B,T,H,D)->(B,H,T,D) transpose (to_heads, tensors.py:157-159).
+ * src row (b, t, h) at b*sb + t*st + h*sh elements, D contiguous elements.
+ * dst (B*H, n_slots, D) contiguous; dst[bh, s] = src[b, perm[bh, s], h].
+ * elem_bytes: 2 (bf16/f16) or 4 (f32).                                        */
+int scfa_gather_rows(const void* src, int elem_bytes, int64_t B, int64_t H, int64_t D, int64_t sb,
+                     int64_t st, int64_t sh, const int32_t* perm, int64_t T_perm, int64_t n_slots,
+                     void* dst, void* stream);
+
+/* Inverse: dst row (b,t,h) = src[bh, rank[bh,t]] if rank < n_slots else 0.
+ * Replaces qk_postprocess (qk_sparse.py:214-225) and hash_scatter +
+ * from_heads (hash_sparse.py:216-220,238).  src (B*H, n_slots, D) contiguous
+ * with element size src_bytes (2 = bf16, 4 = f32); dst strides (db, dt, dh)
+ * elements of size dst_bytes (2 or 4).                                        */
+int scfa_scatter_rows(const void* src, int src_bytes, int64_t B, int64_t H, int64_t T, int64_t D,
+                      const int32_t* rank, int64_t n_slots, void* dst, int dst_bytes, int64_t db,
+                      int64_t dt, int64_t dh, void* stream);
+
+/* Per-slot index / bucket vectors for the kernels (pad_index, qk_sparse.py:74-83).
+ * idx_out[bh, s] = pos[bh, perm[bh, s]] (pos NULL: perm[bh, s]) for s < counts[bh]
+ *                  (counts NULL = all valid),
+ *                  pad_value for counts[bh] <= s < n_slots, oob_value beyond.
+ * hash_out (optional): bucket of perm[bh, s] read from `hash` (strides as in
+ * scfa_hash_sort), hash_oob beyond n_slots.  Both (B*H, T_pad) int32.        */
+int scfa_build_aux(const int32_t* perm, const int32_t* counts, int64_t B, int64_t H,
+                   int64_t T_perm, int64_t n_slots, int64_t T_pad, int32_t pad_value,
+                   int32_t oob_value, const void* hash, int hash_dtype, int64_t sb, int64_t st,
+                   int64_t sh, int32_t hash_oob, const void* pos, int pos_dtype, int64_t ps_bh,
+                   int64_t ps_t, int32_t* idx_out, int32_t* hash_out, void* stream);
+
+/* rank[bh, idx[b, s, h]] = s for s < n_slots, n_slots elsewhere: the inverse
+ * routing table behind qk_postprocess's put_along_axis (qk_sparse.py:218-224)
+ * and hash_scatter (hash_sparse.py:216-220).  idx element (b,s,h) at
+ * b*sb + s*ss + h*sh; out-of-range entries set *err_flag = SCFA_ERR_SHAPE.
+ * rank (B*H, T) int32.                                                        */
+int scfa_invert_index(const void* idx, int dtype, int64_t B, int64_t n_slots, int64_t H, int64_t sb,
+                      int64_t ss, int64_t sh, int64_t T, int32_t* rank, int32_t* err_flag, void* stream);
+
+/* Copy a caller index vector (element (bh,t) at bh*s_bh + t*s_t) into the
+ * padded int32 kernel layout (B*H, T_pad), oob_value past T.                 */
+int scfa_pack_index(const void* src, int dtype, int64_t BH, int64_t T, int64_t s_bh, int64_t s_t,
+                    int64_t T_pad, int32_t oob_value, int32_t* dst, void* stream);
+
+/* Contract checks (ContractError) on packed vectors.
+ * qk: _check_padded/_check_indices (qk_sparse.py:95-117).
+ * sorted: _check_sorted (hash_sparse.py:136-142).                           */
+int scfa_validate_qk(const int32_t* q_idx, const int32_t* k_idx, int64_t BH, int64_t T_q,
+                     int64_t T_kv, int64_t Tq_pad, int64_t Tkv_pad, int32_t* err_flag, void* stream);
+int scfa_validate_sorted(const int32_t* idx, const int32_t* hash, int64_t BH, int64_t T,
+                         int64_t T_pad, int32_t* err_flag, void* stream);
+
+/* ---------------------------------------------------------------- schedules
+ * Exact tile lists for the kernels.  Replaces the per-head schedule of
+ * causal_j_stops (_kernel.py:45-53) and hash_tile_ranges (_kernel.py:56-79),
+ * tightened: only tiles with >= 1 visible pair are listed, and tiles whose
+ * pairs are all visible carry bit 15 ("no mask needed").
+ * rows_are_queries = 1: stationary side = queries (fwd, dQ); 0: keys (dK/dV).
+ * Block sizes: row_block 128; col_block 128 (fwd) or 64 (bwd).
+ * list (B*H, n_row_blocks, list_stride) uint16 with list_stride >= n_col_blocks;
+ * list_count (B*H, n_row_blocks) int32; tiles_total (1 int64, accumulated).  */
+int scfa_build_tile_lists(const int32_t* q_idx, const int32_t* q_hash, const int32_t* k_idx,
+                          const int32_t* k_hash, int64_t BH, int64_t T_q, int64_t T_kv,
+                          int64_t Tq_pad, int64_t Tkv_pad, int rows_are_queries, int row_block,
+                          int col_block, int flags, uint16_t* list, int32_t* list_count,
+                          int64_t list_stride, unsigned long long* tiles_total, void* stream);
+
+/* Reference schedule at arbitrary BlockSpec(B_m, B_n) (tensors.py:63-78):
+ * j_start/j_stop per query block exactly as causal_j_stops (flags without
+ * SCFA_FLAG_HASH) or hash_tile_ranges (with it); tiles[bh] = sum(j_stop - j_start)
+ * (FlashOutputs.tiles_computed, _kernel.py:28-29).  j_* (B*H, ceil(T_q/B_m)).  */
+int scfa_ref_schedule(const int32_t* q_idx, const int32_t* q_hash, const int32_t* k_idx,
+                      const int32_t* k_hash, int64_t BH, int64_t T_q, int64_t T_kv, int64_t Tq_pad,
+                      int64_t Tkv_pad, int64_t B_m, int64_t B_n, int flags, int32_t* j_start,
+                      int32_t* j_stop, int64_t* tiles, void* stream);
+
+/* ---------------------------------------------------------------- attention
+ * Forward: forward_head over the tile list (_kernel.py:92-123) via
+ * qk_forward_kernel (qk_sparse.py:120-148) / hash_forward_kernel
+ * (hash_sparse.py:145-179) / flash_forward (dense.py:33-63).
+ * q (B*H, T_q, D), k/v (B*H, T_kv, D) bf16 contiguous, D in {64, 128}.
+ * o (B*H, T_q, D) bf16 (normalised output), m/l (B*H, T_q) f32 = FlashOutputs.M/L
+ * (M = -inf, L = 0 for stranded rows), lse2 (B*H, Tq_pad) f32 log2-domain
+ * logsumexp (+inf for stranded rows) consumed by the backward.
+ * list/list_count: from scfa_build_tile_lists(rows_are_queries=1, 128, 128).  */
+int scfa_attn_fwd(const void* q, const void* k, const void* v, int64_t BH, int64_t T_q,
+                  int64_t T_kv, int64_t D, const int32_t* q_idx, const int32_t* q_hash,
+                  const int32_t* k_idx, const int32_t* k_hash, int64_t Tq_pad, int64_t Tkv_pad,
+                  const uint16_t* list, const int32_t* list_count, int64_t list_stride,
+                  float scale, int flags, void* o, float* m, float* l, float* lse2, void* stream);
+
+/* delta = rowsum(dO * O) (qk_sparse.py:168, hash_sparse.py:194, dense.py:81);
+ * lse2 rebuilt from (M, L) when lse2_in is NULL (m_hat/inv_l, _kernel.py:152-154).
+ * delta, lse2_out: (B*H, Tq_pad) f32 (pads: delta 0, lse2 +inf).              */
+int scfa_bwd_prep(const void* o, const void* d_out, const float* lse2_in, const float* m,
+                  const float* l, int64_t BH, int64_t T_q, int64_t D, int64_t Tq_pad, float scale,
+                  float* delta, float* lse2_out, void* stream);
+
+/* Backward pass 1 (dQ, query-block owner, _kernel.py:173-179).
+ * list: scfa_build_tile_lists(rows_are_queries=1, 128, 64).  dq (B*H,T_q,D) f32. */
+int scfa_attn_bwd_dq(const void* q, const void* k, const void* v, const void* d_out, int64_t BH,
+                     int64_t T_q, int64_t T_kv, int64_t D, const int32_t* q_idx,
+                     const int32_t* q_hash, const int32_t* k_idx, const int32_t* k_hash,
+                     int64_t Tq_pad, int64_t Tkv_pad, const float* lse2, const float* delta,
+                     const uint16_t* list, const int32_t* list_count, int64_t list_stride,
+                     float scale, int flags, float* dq, void* stream);
+
+/* Backward pass 2 (dK/dV, key-block owner over the transposed schedule,
+ * _kernel.py:181-192).  list: scfa_build_tile_lists(rows_are_queries=0, 128, 64).
+ * dk, dv (B*H, T_kv, D) f32.                                                    */
+int scfa_attn_bwd_dkdv(const void* q, const void* k, const void* v, const void* d_out, int64_t BH,
+                       int64_t T_q, int64_t T_kv, int64_t D, const int32_t* q_idx,
+                       const int32_t* q_hash, const int32_t* k_idx, const int32_t* k_hash,
+                       int64_t Tq_pad, int64_t Tkv_pad, const float* lse2, const float* delta,
+                       const uint16_t* list, const int32_t* list_count, int64_t list_stride,
+                       float scale, int flags, float* dk, float* dv, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SCFA_B200_H */

@@ -1,0 +1,290 @@
+"""The shared tile engine: problem description, schedules, fwd/bwd launches.
+
+Counterpart of pkg/src/scfa/_kernel.py.  The reference runs one NumPy tile
+loop per (b, h) (``forward_head`` :92-123, ``backward_head`` :139-193) over a
+contiguous key-block range per query block (``causal_j_stops`` :45-53,
+``hash_tile_ranges`` :56-79).  Here a :class:`Problem` carries the padded
+int32 index / bucket vectors of every (b, h) slice, builds exact tile lists
+on the device, and launches the tcgen05 kernels of
+``csrc/scfa_attn.cu`` through the C ABI.
+"""
+
+import ctypes
+
+import torch
+
+from . import _lib
+from .errors import ShapeError
+from .tensors import BlockSpec, default_scale, pad128
+
+
+class FlashOutputs:
+    """Forward results (``_kernel.py:18-30``).
+
+    O (B, H, T_Q, D) bf16, normalised output; M (B, H, T_Q) f32 running max of
+    the scaled logits (-inf for stranded queries); L (B, H, T_Q) f32 softmax
+    denominator relative to M (0 for stranded queries).  ``tiles_computed``
+    is the reference schedule's tile count at the caller's BlockSpec,
+    computed on first access; ``tiles_executed`` counts the 128x128 tiles the
+    kernel actually ran.
+    """
+
+    def __init__(self, O, M, L, tiles_computed=None, *, problem=None, blocks=None, lse2=None):
+        self.O = O
+        self.M = M
+        self.L = L
+        self._tiles = tiles_computed
+        self._problem = problem
+        self._blocks = blocks if blocks is not None else BlockSpec()
+        self._lse2 = lse2
+
+    @property
+    def tiles_computed(self):
+        if self._tiles is None:
+            self._tiles = self._problem.ref_tiles(self._blocks) if self._problem is not None else 0
+        return self._tiles
+
+    @tiles_computed.setter
+    def tiles_computed(self, v):
+        self._tiles = v
+
+    @property
+    def tiles_executed(self):
+        return self._problem.executed_tiles() if self._problem is not None else 0
+
+    def __repr__(self):
+        return f"FlashOutputs(O={tuple(self.O.shape)}, tiles_computed={self.tiles_computed})"
+
+
+class Problem:
+    """Index/bucket vectors of all (b, h) slices, padded to 128 per slice.
+
+    q_idx (B*H, Tq_pad) / k_idx (B*H, Tkv_pad) int32 carry original positions
+    (QUERY_PAD/KEY_PAD in pad slots, sentinels past the end); q_hash/k_hash
+    carry bucket ids when ``flags`` has FLAG_HASH.
+    """
+
+    def __init__(self, B, H, T_q, T_kv, D, q_idx, k_idx, q_hash=None, k_hash=None, flags=0):
+        self.B, self.H, self.T_q, self.T_kv, self.D = int(B), int(H), int(T_q), int(T_kv), int(D)
+        self.q_idx, self.k_idx, self.q_hash, self.k_hash = q_idx, k_idx, q_hash, k_hash
+        self.flags = int(flags)
+        self._lists = {}
+        self._tiles_total = None
+
+    @property
+    def BH(self):
+        return self.B * self.H
+
+    @property
+    def Tq_pad(self):
+        return pad128(self.T_q)
+
+    @property
+    def Tkv_pad(self):
+        return pad128(self.T_kv)
+
+    def _hash_ptrs(self):
+        if self.flags & _lib.FLAG_HASH:
+            return _lib.ptr(self.q_hash), _lib.ptr(self.k_hash)
+        return _lib.ptr(self.q_idx), _lib.ptr(self.k_idx)
+
+    def tile_list(self, rows_are_queries, col_block):
+        key = (bool(rows_are_queries), int(col_block))
+        if key in self._lists:
+            return self._lists[key]
+        T_rows = self.T_q if rows_are_queries else self.T_kv
+        T_cols = self.T_kv if rows_are_queries else self.T_q
+        n_rb = -(-T_rows // 128)
+        n_cb = -(-T_cols // col_block)
+        stride = max(n_cb, 1)
+        dev = self.q_idx.device
+        lst = torch.empty((self.BH, max(n_rb, 1), stride), dtype=torch.int16, device=dev)
+        cnt = torch.zeros((self.BH, max(n_rb, 1)), dtype=torch.int32, device=dev)
+        if self._tiles_total is None:
+            self._tiles_total = torch.zeros(3, dtype=torch.int64, device=dev)
+        slot = {(True, 128): 0, (True, 64): 1, (False, 64): 2}.get(key, None)
+        total_ptr = None if slot is None else ctypes.c_void_p(self._tiles_total.data_ptr() + 8 * slot)
+        qh, kh = self._hash_ptrs()
+        _lib.call(
+            "scfa_build_tile_lists",
+            _lib.ptr(self.q_idx), qh, _lib.ptr(self.k_idx), kh,
+            self.BH, self.T_q, self.T_kv, self.Tq_pad, self.Tkv_pad,
+            1 if rows_are_queries else 0, 128, int(col_block), self.flags,
+            _lib.ptr(lst), _lib.ptr(cnt), stride, total_ptr, _lib.stream_ptr(),
+        )
+        self._lists[key] = (lst, cnt, stride)
+        return self._lists[key]
+
+    def executed_tiles(self):
+        """128x128 tiles run by the forward kernel (non-empty tiles only)."""
+        self.tile_list(True, 128)
+        return int(self._tiles_total[0].item())
+
+    def ref_schedule(self, blocks=BlockSpec()):
+        """Reference per-query-block ranges at BlockSpec granularity (all heads)."""
+        nQ = blocks.query_blocks(self.T_q) if self.T_q else 0
+        dev = self.q_idx.device
+        js = torch.zeros((self.BH, nQ), dtype=torch.int32, device=dev)
+        je = torch.zeros((self.BH, nQ), dtype=torch.int32, device=dev)
+        tiles = torch.zeros(self.BH, dtype=torch.int64, device=dev)
+        qh, kh = self._hash_ptrs()
+        _lib.call(
+            "scfa_ref_schedule",
+            _lib.ptr(self.q_idx), qh, _lib.ptr(self.k_idx), kh,
+            self.BH, self.T_q, self.T_kv, self.Tq_pad, self.Tkv_pad,
+            int(blocks.B_m), int(blocks.B_n), self.flags,
+            _lib.ptr(js), _lib.ptr(je), _lib.ptr(tiles), _lib.stream_ptr(),
+        )
+        return js, je, tiles
+
+    def ref_tiles(self, blocks=BlockSpec()):
+        if self.BH == 0 or self.T_q == 0:
+            return 0
+        return int(self.ref_schedule(blocks)[2].sum().item())
+
+    def validate(self, kind):
+        err = torch.zeros(1, dtype=torch.int32, device=self.q_idx.device)
+        if kind == "qk":
+            _lib.call("scfa_validate_qk", _lib.ptr(self.q_idx), _lib.ptr(self.k_idx), self.BH,
+                      self.T_q, self.T_kv, self.Tq_pad, self.Tkv_pad, _lib.ptr(err), _lib.stream_ptr())
+        else:
+            for idx, hsh, T, Tp in ((self.q_idx, self.q_hash, self.T_q, self.Tq_pad),
+                                    (self.k_idx, self.k_hash, self.T_kv, self.Tkv_pad)):
+                _lib.call("scfa_validate_sorted", _lib.ptr(idx), _lib.ptr(hsh), self.BH, T, Tp,
+                          _lib.ptr(err), _lib.stream_ptr())
+        code = int(err.item())
+        if code:
+            what = ("indices must be strictly increasing with pads forming the tail"
+                    if kind == "qk" else "bucket ids must be non-decreasing and positions increase within a bucket")
+            _lib.raise_for(code, what)
+
+
+def pack_index(x, BH, T, oob, device):
+    """Caller index tensor (B, H, T) of any int dtype -> padded int32 (BH, T_pad)."""
+    x = torch.as_tensor(x, device=device)
+    if x.dim() != 3 or x.shape[0] * x.shape[1] != BH or x.shape[2] != T:
+        raise ShapeError(f"index tensor of shape {tuple(x.shape)} does not match ({BH} heads, T={T})")
+    x2 = x.reshape(BH, T)
+    out = torch.empty((BH, pad128(T)), dtype=torch.int32, device=device)
+    _lib.call("scfa_pack_index", _lib.ptr(x2), _lib.dtype_code(x2), BH, T, x2.stride(0), x2.stride(1),
+              pad128(T), int(oob), _lib.ptr(out), _lib.stream_ptr())
+    return out
+
+
+def as_operand(x, device=None):
+    """Engine operand: CUDA bf16, contiguous (numpy arrays are uploaded)."""
+    if not isinstance(x, torch.Tensor):
+        x = torch.as_tensor(x)
+    if device is None:
+        device = x.device if x.is_cuda else torch.device("cuda")
+    if x.device != torch.device(device) or x.dtype != torch.bfloat16:
+        x = x.to(device=device, dtype=torch.bfloat16)
+    return x.contiguous()
+
+
+def check_forward_operands(q, k, v):
+    if q.dim() != 4 or k.dim() != 4 or v.dim() != 4:
+        raise ShapeError("attention operands must be 4-D (B, H, T, D)")
+    if q.shape[:2] != k.shape[:2] or k.shape != v.shape or q.shape[3] != k.shape[3]:
+        raise ShapeError(f"operand shapes disagree: {tuple(q.shape)}, {tuple(k.shape)}, {tuple(v.shape)}")
+
+
+def _scale(scale, D):
+    return float(default_scale(D) if scale is None else scale)
+
+
+def attention_forward(problem, q, k, v, scale=None, blocks=None):
+    """Launch the forward kernel over the exact tile list; returns FlashOutputs."""
+    B, H, T_q, D = q.shape
+    T_kv = k.shape[2]
+    dev = q.device
+    O = torch.empty((B, H, T_q, D), dtype=torch.bfloat16, device=dev)
+    M = torch.empty((B, H, T_q), dtype=torch.float32, device=dev)
+    L = torch.empty((B, H, T_q), dtype=torch.float32, device=dev)
+    lse2 = torch.empty((B * H, pad128(T_q)), dtype=torch.float32, device=dev)
+    if B * H > 0 and T_q > 0:
+        lst, cnt, stride = problem.tile_list(True, 128)
+        qh, kh = problem._hash_ptrs()
+        _lib.call(
+            "scfa_attn_fwd",
+            _lib.ptr(q), _lib.ptr(k), _lib.ptr(v), B * H, T_q, T_kv, D,
+            _lib.ptr(problem.q_idx), qh, _lib.ptr(problem.k_idx), kh,
+            problem.Tq_pad, problem.Tkv_pad, _lib.ptr(lst), _lib.ptr(cnt), stride,
+            _scale(scale, D), problem.flags,
+            _lib.ptr(O), _lib.ptr(M), _lib.ptr(L), _lib.ptr(lse2), _lib.stream_ptr(),
+        )
+    return FlashOutputs(O, M, L, problem=problem, blocks=blocks, lse2=lse2)
+
+
+def attention_backward(problem, q, k, v, outputs, d_out, scale=None):
+    """dQ, dK, dV (fp32, engine layout) recomputing P from the saved statistics."""
+    B, H, T_q, D = q.shape
+    T_kv = k.shape[2]
+    dev = q.device
+    if d_out.shape != q.shape:
+        raise ShapeError(f"dO shape {tuple(d_out.shape)} != {tuple(q.shape)}")
+    d_out = as_operand(d_out, dev)
+    O = as_operand(outputs.O, dev)
+    dq = torch.empty((B, H, T_q, D), dtype=torch.float32, device=dev)
+    dk = torch.empty((B, H, T_kv, D), dtype=torch.float32, device=dev)
+    dv = torch.empty((B, H, T_kv, D), dtype=torch.float32, device=dev)
+    BH = B * H
+    if BH == 0:
+        return dq, dk, dv
+    Tq_pad = pad128(T_q)
+    delta = torch.empty((BH, Tq_pad), dtype=torch.float32, device=dev)
+    lse2 = torch.empty((BH, Tq_pad), dtype=torch.float32, device=dev)
+    lse_in = getattr(outputs, "_lse2", None)
+    M = outputs.M if lse_in is None else None
+    Lv = outputs.L if lse_in is None else None
+    if M is not None:
+        M = torch.as_tensor(M, device=dev).to(torch.float32).contiguous()
+        Lv = torch.as_tensor(Lv, device=dev).to(torch.float32).contiguous()
+    _lib.call("scfa_bwd_prep", _lib.ptr(O), _lib.ptr(d_out), _lib.ptr(lse_in), _lib.ptr(M), _lib.ptr(Lv),
+              BH, T_q, D, Tq_pad, _scale(scale, D), _lib.ptr(delta), _lib.ptr(lse2), _lib.stream_ptr())
+    qh, kh = problem._hash_ptrs()
+    if T_q > 0:
+        lst, cnt, stride = problem.tile_list(True, 64)
+        _lib.call(
+            "scfa_attn_bwd_dq",
+            _lib.ptr(q), _lib.ptr(k), _lib.ptr(v), _lib.ptr(d_out), BH, T_q, T_kv, D,
+            _lib.ptr(problem.q_idx), qh, _lib.ptr(problem.k_idx), kh, problem.Tq_pad, problem.Tkv_pad,
+            _lib.ptr(lse2), _lib.ptr(delta), _lib.ptr(lst), _lib.ptr(cnt), stride,
+            _scale(scale, D), problem.flags, _lib.ptr(dq), _lib.stream_ptr(),
+        )
+    if T_kv > 0:
+        lst, cnt, stride = problem.tile_list(False, 64)
+        _lib.call(
+            "scfa_attn_bwd_dkdv",
+            _lib.ptr(q), _lib.ptr(k), _lib.ptr(v), _lib.ptr(d_out), BH, T_q, T_kv, D,
+            _lib.ptr(problem.q_idx), qh, _lib.ptr(problem.k_idx), kh, problem.Tq_pad, problem.Tkv_pad,
+            _lib.ptr(lse2), _lib.ptr(delta), _lib.ptr(lst), _lib.ptr(cnt), stride,
+            _scale(scale, D), problem.flags, _lib.ptr(dk), _lib.ptr(dv), _lib.stream_ptr(),
+        )
+    return dq, dk, dv
+
+
+def causal_j_stops(q_idx, k_idx, blocks=BlockSpec()):
+    """Reference ``causal_j_stops`` for one head's 1-D index vectors (computed on the GPU)."""
+    q = torch.as_tensor(q_idx)
+    k = torch.as_tensor(k_idx)
+    dev = q.device if q.is_cuda else torch.device("cuda")
+    Tq, Tk = int(q.numel()), int(k.numel())
+    pq = pack_index(q.reshape(1, 1, Tq), 1, Tq, -1, dev)
+    pk = pack_index(k.reshape(1, 1, Tk), 1, Tk, 0x7FFFFFFF, dev)
+    prob = Problem(1, 1, Tq, Tk, 64, pq, pk)
+    return prob.ref_schedule(blocks)[1][0]
+
+
+def hash_tile_ranges(q_hash, q_idx, k_hash, k_idx, blocks=BlockSpec()):
+    """Reference ``hash_tile_ranges`` (_kernel.py:56-79) for one head, on the GPU."""
+    tens = [torch.as_tensor(x) for x in (q_hash, q_idx, k_hash, k_idx)]
+    dev = next((t.device for t in tens if t.is_cuda), torch.device("cuda"))
+    Tq, Tk = int(tens[1].numel()), int(tens[3].numel())
+    qh = pack_index(tens[0].reshape(1, 1, Tq), 1, Tq, -3, dev)
+    qi = pack_index(tens[1].reshape(1, 1, Tq), 1, Tq, -1, dev)
+    kh = pack_index(tens[2].reshape(1, 1, Tk), 1, Tk, -2, dev)
+    ki = pack_index(tens[3].reshape(1, 1, Tk), 1, Tk, 0x7FFFFFFF, dev)
+    prob = Problem(1, 1, Tq, Tk, 64, qi, ki, qh, kh, flags=_lib.FLAG_HASH)
+    js, je, _ = prob.ref_schedule(blocks)
+    return js[0], je[0]

@@ -1,0 +1,542 @@
+// scfa_attn.cu — tcgen05/TMEM/TMA tile engine for Sparse Causal Flash Attention.
+//
+// One kernel template runs all three passes of the reference tile loop
+// (pkg/src/scfa/_kernel.py:92-193):
+//
+//   FWD      rows = queries, streamed cols = keys.   S = Q K^T ; P = softmax ; O += P V
+//   BWD_DQ   rows = queries, streamed cols = keys.   S, dP = dO V^T ; dS ; dQ += dS K
+//   BWD_DKDV rows = keys,    streamed cols = queries. S^T, dP^T ; dV += P^T dO ; dK += dS^T Q
+//
+// Each CTA owns one 128-row stationary block of one (b, h) slice and walks a
+// per-block tile list built by scfa_sched.cu.  The list holds only tiles
+// that contain at least one visible (query, key) pair — fully masked tiles
+// are skipped, not masked — and flags the tiles whose pairs are all visible
+// so that the per-element causal/bucket mask runs only in boundary tiles.
+//
+// Roles (192 threads):
+//   warps 0-3  : one thread per stationary row == TMEM lane.  Online softmax
+//                (fwd) or P / dS recompute (bwd), epilogue.
+//   warp 4     : TMA producer (stationary tiles once, streamed tiles in an
+//                NS-stage mbarrier ring, plus the per-column index/bucket
+//                (and lse/delta) vectors via cp.async.bulk).
+//   warp 5     : TMEM allocator + single-thread tcgen05.mma issuer.
+//
+// TMEM (per CTA, 256 columns for D=64 so that two CTAs share an SM):
+//   FWD      S fp32 [0,128) (P bf16 aliases [0,64)), O fp32 [128,128+D)
+//   BWD_DQ   S [0,64) (dS bf16 aliases [0,32)), dP [64,128), dQ [128,128+D)
+//   BWD_DKDV S^T [0,64) (P^T aliases [0,32)), dP^T [64,128) (dS^T aliases
+//            [64,96)), dV [128,128+D), dK [128+D,128+2D)
+#include "scfa_common.cuh"
+#include "scfa_internal.h"
+
+namespace scfa {
+
+enum Mode : int { MODE_FWD = 0, MODE_DQ = 1, MODE_DKDV = 2 };
+
+template <int kMode, int kD>
+struct Cfg {
+  static constexpr int BM = 128;                          // stationary rows
+  static constexpr int BN = (kMode == MODE_FWD) ? 128 : 64;  // streamed rows per tile
+  static constexpr int NS = (kMode == MODE_FWD) ? 2 : 3;     // pipeline stages
+  static constexpr int DCH = kD / 64;                     // 128-byte column chunks
+  static constexpr int NX = (kMode == MODE_FWD) ? 1 : 2;  // stationary tensors
+  static constexpr int NAUX = (kMode == MODE_DKDV) ? 4 : 2;  // per-column vectors
+  static constexpr int X_BYTES = BM * kD * 2;
+  static constexpr int Y_BYTES = BN * kD * 2;
+  static constexpr int AUX_BYTES = BN * 4;
+  static constexpr int STAGE_BYTES = 2 * Y_BYTES + NAUX * AUX_BYTES;
+  static constexpr int TM_S = 0;
+  static constexpr int TM_DP = (kMode == MODE_FWD) ? 0 : BN;
+  static constexpr int TM_ACC0 = 128;
+  static constexpr int TM_ACC1 = 128 + kD;
+  static constexpr int TM_USED = (kMode == MODE_DKDV) ? 128 + 2 * kD : 128 + kD;
+  static constexpr uint32_t TM_COLS = TM_USED <= 256 ? 256 : 512;
+  static constexpr int MAX_LIST = 1024;
+  // shared memory carve-up (offsets from a 1024-aligned base)
+  static constexpr int OFF_X = 0;
+  static constexpr int OFF_STAGE = OFF_X + NX * X_BYTES;
+  static constexpr int OFF_BAR = OFF_STAGE + NS * STAGE_BYTES;
+  static constexpr int N_BARS = 4 + 2 * NS;
+  static constexpr int OFF_LIST = OFF_BAR + 8 * N_BARS + 16;
+  static constexpr int SMEM_BYTES = OFF_LIST + 2 * MAX_LIST + 1024 /*align slack*/;
+};
+
+struct AttnArgs {
+  int BH;
+  int T_rows, T_cols;          // true lengths of the stationary / streamed side
+  int T_rows_pad, T_cols_pad;  // padded lengths of the aux vectors
+  const int* row_idx;
+  const int* row_hash;
+  const int* col_idx;
+  const int* col_hash;
+  const float* lse2;   // (BH, Tq_pad), log2-domain; +inf where no key is visible
+  const float* delta;  // (BH, Tq_pad)
+  const uint16_t* list;
+  const int* list_count;
+  int list_stride;
+  int n_row_blocks;
+  __nv_bfloat16* out_o;  // FWD
+  float* out0;           // FWD: M      DQ: dQ   DKDV: dK
+  float* out1;           // FWD: L      DKDV: dV
+  float* out_lse2;       // FWD
+  float scale_log2;
+  float scale;
+  int exclude_self;
+  int use_hash;
+};
+
+SCFA_DEVICE bool visible(int qi, int ki, int qh, int kh, int excl, int use_hash) {
+  bool ok = excl ? (qi > ki) : (qi >= ki);
+  return ok && (!use_hash || qh == kh);
+}
+
+template <int kMode, int kD>
+__global__ void __launch_bounds__(192, 2)
+    scfa_attn_kernel(const __grid_constant__ CUtensorMap tm_x0, const __grid_constant__ CUtensorMap tm_x1,
+                     const __grid_constant__ CUtensorMap tm_y0, const __grid_constant__ CUtensorMap tm_y1,
+                     const AttnArgs args) {
+  using C = Cfg<kMode, kD>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  // Heaviest stationary blocks (largest causal reach) are launched first.
+  const int rb = args.n_row_blocks - 1 - blockIdx.x;
+  const int bh = blockIdx.y;
+  const int row0 = rb * C::BM;
+
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* bar_x_full = bars + 0;
+  uint64_t* bar_s_full = bars + 1;
+  uint64_t* bar_p_full = bars + 2;
+  uint64_t* bar_acc = bars + 3;
+  uint64_t* bar_y_full = bars + 4;
+  uint64_t* bar_y_empty = bars + 4 + C::NS;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_BAR + 8 * C::N_BARS);
+  uint16_t* list_s = reinterpret_cast<uint16_t*>(smem + C::OFF_LIST);
+
+  const int list_base = bh * args.n_row_blocks + rb;
+  int n_tiles = args.list_count[list_base];
+  if (n_tiles > C::MAX_LIST) n_tiles = C::MAX_LIST;  // host guarantees this never clips
+  const uint16_t* list_g = args.list + static_cast<size_t>(list_base) * args.list_stride;
+  for (int i = threadIdx.x; i < n_tiles; i += blockDim.x) list_s[i] = list_g[i];
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar_x_full, 1);
+    mbar_init(bar_s_full, 1);
+    mbar_init(bar_p_full, 128);
+    mbar_init(bar_acc, 1);
+    for (int s = 0; s < C::NS; ++s) {
+      mbar_init(bar_y_full + s, 1);
+      mbar_init(bar_y_empty + s, 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 5) tmem_alloc<C::TM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 4) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0 && n_tiles > 0) {
+      tma_prefetch_desc(&tm_x0);
+      tma_prefetch_desc(&tm_y0);
+      tma_prefetch_desc(&tm_y1);
+      if (C::NX == 2) tma_prefetch_desc(&tm_x1);
+      mbar_arrive_expect_tx(bar_x_full, C::NX * C::X_BYTES);
+      for (int c = 0; c < C::DCH; ++c) {
+        tma_load_3d(smem + C::OFF_X + c * C::BM * 128, &tm_x0, bar_x_full, c * 64, row0, bh);
+        if (C::NX == 2)
+          tma_load_3d(smem + C::OFF_X + C::X_BYTES + c * C::BM * 128, &tm_x1, bar_x_full, c * 64, row0, bh);
+      }
+      for (int t = 0; t < n_tiles; ++t) {
+        const int st = t % C::NS;
+        if (t >= C::NS) mbar_wait(bar_y_empty + st, ((t / C::NS) - 1) & 1);
+        const int cb = list_s[t] & 0x7fff;
+        const int col0 = cb * C::BN;
+        uint8_t* stage = smem + C::OFF_STAGE + st * C::STAGE_BYTES;
+        mbar_arrive_expect_tx(bar_y_full + st, 2 * C::Y_BYTES + C::NAUX * C::AUX_BYTES);
+        for (int c = 0; c < C::DCH; ++c) {
+          tma_load_3d(stage + c * C::BN * 128, &tm_y0, bar_y_full + st, c * 64, col0, bh);
+          tma_load_3d(stage + C::Y_BYTES + c * C::BN * 128, &tm_y1, bar_y_full + st, c * 64, col0, bh);
+        }
+        uint8_t* aux = stage + 2 * C::Y_BYTES;
+        const size_t coff = static_cast<size_t>(bh) * args.T_cols_pad + col0;
+        bulk_load(aux, args.col_idx + coff, C::AUX_BYTES, bar_y_full + st);
+        bulk_load(aux + C::AUX_BYTES, args.col_hash + coff, C::AUX_BYTES, bar_y_full + st);
+        if (kMode == MODE_DKDV) {
+          bulk_load(aux + 2 * C::AUX_BYTES, args.lse2 + coff, C::AUX_BYTES, bar_y_full + st);
+          bulk_load(aux + 3 * C::AUX_BYTES, args.delta + coff, C::AUX_BYTES, bar_y_full + st);
+        }
+      }
+    }
+  } else if (warp == 5) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0 && n_tiles > 0) {
+      constexpr uint32_t idesc_s = make_idesc_bf16(128, C::BN, false, false);
+      constexpr uint32_t idesc_acc = make_idesc_bf16(128, kD, false, true);
+      const uint32_t x0_addr = smem_u32(smem + C::OFF_X);
+      const uint32_t x1_addr = x0_addr + C::X_BYTES;
+      mbar_wait(bar_x_full, 0);
+      tc_fence_after();
+      for (int t = 0; t < n_tiles; ++t) {
+        const int st = t % C::NS;
+        mbar_wait(bar_y_full + st, (t / C::NS) & 1);
+        tc_fence_after();
+        const uint32_t y0_addr = smem_u32(smem + C::OFF_STAGE + st * C::STAGE_BYTES);
+        const uint32_t y1_addr = y0_addr + C::Y_BYTES;
+        // S = X0 . Y0^T  (and dP = X1 . Y1^T), K = head dim, both operands K-major.
+#pragma unroll
+        for (int k = 0; k < kD / 16; ++k) {
+          const uint32_t koff = (k & 3) * 32;
+          const uint32_t a = x0_addr + (k >> 2) * (C::BM * 128) + koff;
+          const uint32_t b = y0_addr + (k >> 2) * (C::BN * 128) + koff;
+          umma_ss(tmem + C::TM_S, make_sdesc_sw128(a, 16, 1024), make_sdesc_sw128(b, 16, 1024), idesc_s, k > 0);
+        }
+        if (kMode != MODE_FWD) {
+#pragma unroll
+          for (int k = 0; k < kD / 16; ++k) {
+            const uint32_t koff = (k & 3) * 32;
+            const uint32_t a = x1_addr + (k >> 2) * (C::BM * 128) + koff;
+            const uint32_t b = y1_addr + (k >> 2) * (C::BN * 128) + koff;
+            umma_ss(tmem + C::TM_DP, make_sdesc_sw128(a, 16, 1024), make_sdesc_sw128(b, 16, 1024), idesc_s, k > 0);
+          }
+        }
+        umma_commit(bar_s_full);
+        mbar_wait(bar_p_full, t & 1);
+        tc_fence_after();
+        // Accumulate: A (bf16) from TMEM, B = streamed tile read MN-major, K = BN streamed rows.
+        if (kMode == MODE_FWD) {
+#pragma unroll
+          for (int k = 0; k < C::BN / 16; ++k)
+            umma_ts(tmem + C::TM_ACC0, tmem + C::TM_S + k * 8,
+                    make_sdesc_sw128(y1_addr + k * 2048, C::BN * 128, 1024), idesc_acc, (t > 0 || k > 0));
+        } else if (kMode == MODE_DQ) {
+#pragma unroll
+          for (int k = 0; k < C::BN / 16; ++k)
+            umma_ts(tmem + C::TM_ACC0, tmem + C::TM_S + k * 8,
+                    make_sdesc_sw128(y0_addr + k * 2048, C::BN * 128, 1024), idesc_acc, (t > 0 || k > 0));
+        } else {
+#pragma unroll
+          for (int k = 0; k < C::BN / 16; ++k) {
+            // dV += P^T dO
+            umma_ts(tmem + C::TM_ACC0, tmem + C::TM_S + k * 8,
+                    make_sdesc_sw128(y1_addr + k * 2048, C::BN * 128, 1024), idesc_acc, (t > 0 || k > 0));
+            // dK += dS^T Q
+            umma_ts(tmem + C::TM_ACC1, tmem + C::TM_DP + k * 8,
+                    make_sdesc_sw128(y0_addr + k * 2048, C::BN * 128, 1024), idesc_acc, (t > 0 || k > 0));
+          }
+        }
+        umma_commit(bar_y_empty + st);
+      }
+      umma_commit(bar_acc);
+    }
+  } else {
+    // ------------------------------------------------------------ row threads
+    const int r = threadIdx.x;  // 0..127 == TMEM lane
+    const int row = row0 + r;
+    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    const uint32_t t_s = tmem + lane_off + C::TM_S;
+    const uint32_t t_dp = tmem + lane_off + C::TM_DP;
+    const size_t roff = static_cast<size_t>(bh) * args.T_rows_pad + row;
+    const int my_idx = args.row_idx[roff];
+    const int my_hash = args.row_hash[roff];
+    const float sl = args.scale_log2;
+    const int excl = args.exclude_self;
+    const int use_hash = args.use_hash;
+
+    if (kMode == MODE_FWD) {
+      const float NEG_INF = -INFINITY;
+      const float mask_val = sl >= 0.f ? NEG_INF : INFINITY;
+      float m_run = NEG_INF;   // log2-domain max used for exponentiation (lags by < 8)
+      float m_true = NEG_INF;  // exact running max of scaled logits (log2 domain)
+      float l_run = 0.f;
+      for (int t = 0; t < n_tiles; ++t) {
+        const int entry = list_s[t];
+        const bool full = (entry & 0x8000) != 0;
+        const int st = t % C::NS;
+        const int* kidx = reinterpret_cast<const int*>(smem + C::OFF_STAGE + st * C::STAGE_BYTES + 2 * C::Y_BYTES);
+        const int* khash = kidx + C::BN;
+        mbar_wait(bar_s_full, t & 1);
+        tc_fence_after();
+        float s[C::BN];
+#pragma unroll
+        for (int c = 0; c < C::BN; c += 32) {
+          uint32_t v[32];
+          tmem_ld32(t_s + c, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) s[c + i] = __uint_as_float(v[i]);
+        }
+        if (!full) {
+#pragma unroll
+          for (int c = 0; c < C::BN; c += 4) {
+            const int4 ki = *reinterpret_cast<const int4*>(kidx + c);
+            const int4 kh = *reinterpret_cast<const int4*>(khash + c);
+            if (!visible(my_idx, ki.x, my_hash, kh.x, excl, use_hash)) s[c + 0] = mask_val;
+            if (!visible(my_idx, ki.y, my_hash, kh.y, excl, use_hash)) s[c + 1] = mask_val;
+            if (!visible(my_idx, ki.z, my_hash, kh.z, excl, use_hash)) s[c + 2] = mask_val;
+            if (!visible(my_idx, ki.w, my_hash, kh.w, excl, use_hash)) s[c + 3] = mask_val;
+          }
+        }
+        float mx = s[0];
+        if (sl >= 0.f) {
+#pragma unroll
+          for (int c = 1; c < C::BN; ++c) mx = fmaxf(mx, s[c]);
+        } else {
+#pragma unroll
+          for (int c = 1; c < C::BN; ++c) mx = fminf(mx, s[c]);
+        }
+        const float m_tile = mx * sl;  // -inf when the whole row is masked in this tile
+        m_true = fmaxf(m_true, m_tile);
+        // Rebase to a new max (log2 units) only when the max grows by >= 2^8: P stays
+        // <= 256 and the final normalisation by l keeps the result exact.
+        float alpha = 1.f;
+        const bool rebase = m_tile > m_run + 8.0f || (m_run == NEG_INF && m_tile != NEG_INF);
+        if (rebase) {
+          alpha = (m_run == NEG_INF) ? 0.f : ex2(m_run - m_tile);
+          l_run *= alpha;
+          m_run = m_tile;
+        }
+        const float m_use = (m_run == NEG_INF) ? 0.f : m_run;
+        float lsum = 0.f;
+#pragma unroll
+        for (int c = 0; c < C::BN; c += 32) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float p0 = ex2(fmaf(s[c + 2 * i], sl, -m_use));
+            const float p1 = ex2(fmaf(s[c + 2 * i + 1], sl, -m_use));
+            lsum += p0 + p1;
+            pk[i] = pack_bf16(p0, p1);
+          }
+          tmem_st16(t_s + c / 2, pk);
+        }
+        if (rebase && t > 0) {
+          // The previous P.V has completed: s_full of this tile was committed after it.
+#pragma unroll 1
+          for (int c = 0; c < kD; c += 32) {
+            uint32_t v[32];
+            tmem_ld32(tmem + lane_off + C::TM_ACC0 + c, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+            tmem_st32(tmem + lane_off + C::TM_ACC0 + c, v);
+          }
+        }
+        l_run += lsum;
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(bar_p_full);
+      }
+      // ---------------- epilogue: O / l, M, L, lse2
+      if (n_tiles > 0) {
+        mbar_wait(bar_acc, 0);
+        tc_fence_after();
+      }
+      if (row < args.T_rows) {
+        const float inv_l = (l_run > 0.f) ? 1.f / l_run : 0.f;
+        __nv_bfloat16* orow = args.out_o + (static_cast<size_t>(bh) * args.T_rows + row) * kD;
+#pragma unroll
+        for (int c = 0; c < kD; c += 32) {
+          uint32_t v[32];
+          if (n_tiles > 0) {
+            tmem_ld32(tmem + lane_off + C::TM_ACC0 + c, v);
+            tmem_wait_ld();
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0u;
+          }
+          uint4 o4[4];
+          uint32_t* ow = reinterpret_cast<uint32_t*>(o4);
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            ow[i] = pack_bf16(__uint_as_float(v[2 * i]) * inv_l, __uint_as_float(v[2 * i + 1]) * inv_l);
+          uint4* dst = reinterpret_cast<uint4*>(orow + c);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) dst[i] = o4[i];
+        }
+        const size_t so = static_cast<size_t>(bh) * args.T_rows + row;
+        const float LN2 = 0.6931471805599453f;
+        const bool dead = !(l_run > 0.f);
+        args.out0[so] = dead ? NEG_INF : m_true * LN2;                                  // M
+        args.out1[so] = dead ? 0.f : l_run * ex2(((m_run == NEG_INF) ? 0.f : m_run) - m_true);  // L
+        args.out_lse2[static_cast<size_t>(bh) * args.T_rows_pad + row] =
+            dead ? INFINITY : (((m_run == NEG_INF) ? 0.f : m_run) + __log2f(l_run));
+      }
+    } else {
+      // ---------------- backward passes: P and dS recomputed from (lse2, delta)
+      float my_lse = 0.f, my_delta = 0.f;
+      if (kMode == MODE_DQ) {
+        my_lse = args.lse2[roff];
+        my_delta = args.delta[roff];
+      }
+      for (int t = 0; t < n_tiles; ++t) {
+        const int entry = list_s[t];
+        const bool full = (entry & 0x8000) != 0;
+        const int st = t % C::NS;
+        const int* cidx = reinterpret_cast<const int*>(smem + C::OFF_STAGE + st * C::STAGE_BYTES + 2 * C::Y_BYTES);
+        const int* chash = cidx + C::BN;
+        const float* clse = reinterpret_cast<const float*>(chash + C::BN);
+        const float* cdelta = clse + C::BN;
+        mbar_wait(bar_s_full, t & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < C::BN; c += 32) {
+          uint32_t sv[32], dv[32];
+          tmem_ld32(t_s + c, sv);
+          tmem_ld32(t_dp + c, dv);
+          tmem_wait_ld();
+          uint32_t pk_p[16], pk_ds[16];
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            float pp[2], dd[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int cc = c + i + e;
+              float p, ds;
+              if (kMode == MODE_DQ) {
+                p = ex2(fmaf(__uint_as_float(sv[i + e]), sl, -my_lse));
+                if (!full && !visible(my_idx, cidx[cc], my_hash, chash[cc], excl, use_hash)) p = 0.f;
+                ds = p * (__uint_as_float(dv[i + e]) - my_delta);
+              } else {
+                p = ex2(fmaf(__uint_as_float(sv[i + e]), sl, -clse[cc]));
+                if (!full && !visible(cidx[cc], my_idx, chash[cc], my_hash, excl, use_hash)) p = 0.f;
+                ds = p * (__uint_as_float(dv[i + e]) - cdelta[cc]);
+              }
+              pp[e] = p;
+              dd[e] = ds;
+            }
+            pk_p[i / 2] = pack_bf16(pp[0], pp[1]);
+            pk_ds[i / 2] = pack_bf16(dd[0], dd[1]);
+          }
+          if (kMode == MODE_DQ) {
+            tmem_st16(t_s + c / 2, pk_ds);
+          } else {
+            tmem_st16(t_s + c / 2, pk_p);
+            tmem_st16(t_dp + c / 2, pk_ds);
+          }
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(bar_p_full);
+      }
+      if (n_tiles > 0) {
+        mbar_wait(bar_acc, 0);
+        tc_fence_after();
+      }
+      if (row < args.T_rows) {
+        const size_t ro = (static_cast<size_t>(bh) * args.T_rows + row) * kD;
+        const int n_out = (kMode == MODE_DKDV) ? 2 : 1;
+        for (int o = 0; o < n_out; ++o) {
+          // DQ: out0 = scale * dQ.  DKDV: out0 = scale * dK (ACC1), out1 = dV (ACC0).
+          const int col = (kMode == MODE_DKDV && o == 0) ? C::TM_ACC1 : C::TM_ACC0;
+          const float mul = (o == 0) ? args.scale : 1.f;
+          float* dst = ((o == 0) ? args.out0 : args.out1) + ro;
+#pragma unroll
+          for (int c = 0; c < kD; c += 32) {
+            uint32_t v[32];
+            if (n_tiles > 0) {
+              tmem_ld32(tmem + lane_off + col + c, v);
+              tmem_wait_ld();
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = 0u;
+            }
+            float4* d4 = reinterpret_cast<float4*>(dst + c);
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              d4[i] = make_float4(__uint_as_float(v[4 * i]) * mul, __uint_as_float(v[4 * i + 1]) * mul,
+                                  __uint_as_float(v[4 * i + 2]) * mul, __uint_as_float(v[4 * i + 3]) * mul);
+          }
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_dealloc<C::TM_COLS>(tmem);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+
+static int make_map(CUtensorMap* map, const void* base, int BH, int T, int D, int box_rows) {
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(T), static_cast<cuuint64_t>(BH)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(D) * 2, static_cast<cuuint64_t>(T) * D * 2};
+  cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows), 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return encode_tensor_map_bf16_3d(map, base, dims, strides, box, estr);
+}
+
+template <int kMode, int kD>
+static int launch_mode(const AttnLaunch& L, cudaStream_t stream) {
+  using C = Cfg<kMode, kD>;
+  CUtensorMap mx0, mx1, my0, my1;
+  int rc = 0;
+  rc |= make_map(&mx0, L.x0, L.BH, L.T_rows, kD, C::BM);
+  rc |= make_map(&mx1, L.x1 ? L.x1 : L.x0, L.BH, L.T_rows, kD, C::BM);
+  rc |= make_map(&my0, L.y0, L.BH, L.T_cols, kD, C::BN);
+  rc |= make_map(&my1, L.y1, L.BH, L.T_cols, kD, C::BN);
+  if (rc) return SCFA_ERR_CUDA;
+  AttnArgs a;
+  a.BH = L.BH;
+  a.T_rows = L.T_rows;
+  a.T_cols = L.T_cols;
+  a.T_rows_pad = L.T_rows_pad;
+  a.T_cols_pad = L.T_cols_pad;
+  a.row_idx = L.row_idx;
+  a.row_hash = L.row_hash;
+  a.col_idx = L.col_idx;
+  a.col_hash = L.col_hash;
+  a.lse2 = L.lse2;
+  a.delta = L.delta;
+  a.list = L.list;
+  a.list_count = L.list_count;
+  a.list_stride = L.list_stride;
+  a.n_row_blocks = L.n_row_blocks;
+  a.out_o = L.out_o;
+  a.out0 = L.out0;
+  a.out1 = L.out1;
+  a.out_lse2 = L.out_lse2;
+  a.scale_log2 = L.scale * 1.4426950408889634f;
+  a.scale = L.scale;
+  a.exclude_self = L.exclude_self;
+  a.use_hash = L.use_hash;
+  auto kern = scfa_attn_kernel<kMode, kD>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES) != cudaSuccess)
+      return SCFA_ERR_CUDA;
+    attr_set = true;
+  }
+  if (L.list_stride > C::MAX_LIST) return SCFA_ERR_SHAPE;
+  dim3 grid(L.n_row_blocks, L.BH);
+  if (L.n_row_blocks == 0 || L.BH == 0) return SCFA_OK;
+  kern<<<grid, 192, C::SMEM_BYTES, stream>>>(mx0, mx1, my0, my1, a);
+  return cudaGetLastError() == cudaSuccess ? SCFA_OK : SCFA_ERR_CUDA;
+}
+
+int launch_attention(const AttnLaunch& L, cudaStream_t stream) {
+  if (L.D == 64) {
+    if (L.mode == MODE_FWD) return launch_mode<MODE_FWD, 64>(L, stream);
+    if (L.mode == MODE_DQ) return launch_mode<MODE_DQ, 64>(L, stream);
+    if (L.mode == MODE_DKDV) return launch_mode<MODE_DKDV, 64>(L, stream);
+  } else if (L.D == 128) {
+    if (L.mode == MODE_FWD) return launch_mode<MODE_FWD, 128>(L, stream);
+    if (L.mode == MODE_DQ) return launch_mode<MODE_DQ, 128>(L, stream);
+    if (L.mode == MODE_DKDV) return launch_mode<MODE_DKDV, 128>(L, stream);
+  }
+  return SCFA_ERR_SHAPE;
+}
+
+int attention_block_rows(int mode) { return 128; }
+int attention_block_cols(int mode) { return mode == MODE_FWD ? 128 : 64; }
+
+}  // namespace scfa

@@ -1,0 +1,201 @@
+// scfa_capi.cu — extern "C" attention entry points, error reporting, TMA descriptors.
+#include <cudaTypedefs.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <mutex>
+
+#include "scfa_common.cuh"
+#include "scfa_internal.h"
+
+namespace scfa {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+int encode_tensor_map_bf16_3d(CUtensorMap* map, const void* base, const cuuint64_t* dims,
+                              const cuuint64_t* strides_bytes, const cuuint32_t* box, const cuuint32_t* elem_strides) {
+  auto fn = get_encode();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return 1;
+  }
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides_bytes, box,
+                  elem_strides, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+    return 1;
+  }
+  return 0;
+}
+
+static int check_attn_args(int64_t BH, int64_t T_q, int64_t T_kv, int64_t D, int64_t Tq_pad, int64_t Tkv_pad,
+                           const void* q, const void* k, const void* v) {
+  if (D != 64 && D != 128) {
+    set_error("head dim %lld unsupported (64 or 128)", static_cast<long long>(D));
+    return SCFA_ERR_SHAPE;
+  }
+  if (Tq_pad < ((T_q + 127) / 128) * 128 || Tkv_pad < ((T_kv + 127) / 128) * 128) {
+    set_error("padded index vectors too short");
+    return SCFA_ERR_SHAPE;
+  }
+  if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(v)) & 15) {
+    set_error("operands must be 16-byte aligned");
+    return SCFA_ERR_SHAPE;
+  }
+  if (BH > 65535) {
+    set_error("too many (b, h) slices");
+    return SCFA_ERR_SHAPE;
+  }
+  return SCFA_OK;
+}
+
+}  // namespace scfa
+
+using namespace scfa;
+
+extern "C" int scfa_abi_version(void) { return 1; }
+
+extern "C" const char* scfa_last_error(void) { return g_err; }
+
+extern "C" int scfa_attn_fwd(const void* q, const void* k, const void* v, int64_t BH, int64_t T_q, int64_t T_kv,
+                             int64_t D, const int32_t* q_idx, const int32_t* q_hash, const int32_t* k_idx,
+                             const int32_t* k_hash, int64_t Tq_pad, int64_t Tkv_pad, const uint16_t* list,
+                             const int32_t* list_count, int64_t list_stride, float scale, int flags, void* o, float* m,
+                             float* l, float* lse2, void* stream) {
+  int rc = check_attn_args(BH, T_q, T_kv, D, Tq_pad, Tkv_pad, q, k, v);
+  if (rc) return rc;
+  if (BH == 0 || T_q == 0) return SCFA_OK;
+  AttnLaunch L{};
+  L.mode = 0;
+  L.D = static_cast<int>(D);
+  L.BH = static_cast<int>(BH);
+  L.T_rows = static_cast<int>(T_q);
+  L.T_cols = static_cast<int>(T_kv > 0 ? T_kv : 1);
+  L.T_rows_pad = static_cast<int>(Tq_pad);
+  L.T_cols_pad = static_cast<int>(Tkv_pad);
+  L.x0 = q;
+  L.x1 = nullptr;
+  // With no keys every row is stranded and no tile is listed; the streamed maps
+  // then only need a valid address, never a load.
+  L.y0 = T_kv > 0 ? k : q;
+  L.y1 = T_kv > 0 ? v : q;
+  if (T_kv == 0) L.T_cols = static_cast<int>(T_q);
+  L.row_idx = q_idx;
+  L.row_hash = (flags & SCFA_FLAG_HASH) ? q_hash : q_idx;
+  L.col_idx = k_idx;
+  L.col_hash = (flags & SCFA_FLAG_HASH) ? k_hash : k_idx;
+  L.list = list;
+  L.list_count = list_count;
+  L.list_stride = static_cast<int>(list_stride);
+  L.n_row_blocks = static_cast<int>((T_q + 127) / 128);
+  L.out_o = static_cast<__nv_bfloat16*>(o);
+  L.out0 = m;
+  L.out1 = l;
+  L.out_lse2 = lse2;
+  L.scale = scale;
+  L.exclude_self = (flags & SCFA_FLAG_EXCLUDE_SELF) ? 1 : 0;
+  L.use_hash = (flags & SCFA_FLAG_HASH) ? 1 : 0;
+  rc = launch_attention(L, static_cast<cudaStream_t>(stream));
+  if (rc && !g_err[0]) set_error("attention forward launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+  return rc;
+}
+
+static int bwd_common(int mode, const void* q, const void* k, const void* v, const void* d_out, int64_t BH,
+                      int64_t T_q, int64_t T_kv, int64_t D, const int32_t* q_idx, const int32_t* q_hash,
+                      const int32_t* k_idx, const int32_t* k_hash, int64_t Tq_pad, int64_t Tkv_pad, const float* lse2,
+                      const float* delta, const uint16_t* list, const int32_t* list_count, int64_t list_stride,
+                      float scale, int flags, float* out0, float* out1, void* stream) {
+  int rc = check_attn_args(BH, T_q, T_kv, D, Tq_pad, Tkv_pad, q, k, v);
+  if (rc) return rc;
+  const bool hash = (flags & SCFA_FLAG_HASH) != 0;
+  AttnLaunch L{};
+  L.mode = mode;
+  L.D = static_cast<int>(D);
+  L.BH = static_cast<int>(BH);
+  L.scale = scale;
+  L.exclude_self = (flags & SCFA_FLAG_EXCLUDE_SELF) ? 1 : 0;
+  L.use_hash = hash ? 1 : 0;
+  L.lse2 = lse2;
+  L.delta = delta;
+  L.list = list;
+  L.list_count = list_count;
+  L.list_stride = static_cast<int>(list_stride);
+  L.out0 = out0;
+  L.out1 = out1;
+  if (mode == 1) {  // dQ: rows = queries
+    if (BH == 0 || T_q == 0) return SCFA_OK;
+    L.T_rows = static_cast<int>(T_q);
+    L.T_cols = static_cast<int>(T_kv > 0 ? T_kv : 1);
+    L.T_rows_pad = static_cast<int>(Tq_pad);
+    L.T_cols_pad = static_cast<int>(Tkv_pad);
+    L.x0 = q;
+    L.x1 = d_out;
+    L.y0 = T_kv > 0 ? k : q;
+    L.y1 = T_kv > 0 ? v : q;
+    if (T_kv == 0) L.T_cols = static_cast<int>(T_q);
+    L.row_idx = q_idx;
+    L.row_hash = hash ? q_hash : q_idx;
+    L.col_idx = k_idx;
+    L.col_hash = hash ? k_hash : k_idx;
+  } else {  // dK/dV: rows = keys
+    if (BH == 0 || T_kv == 0) return SCFA_OK;
+    L.T_rows = static_cast<int>(T_kv);
+    L.T_cols = static_cast<int>(T_q > 0 ? T_q : 1);
+    L.T_rows_pad = static_cast<int>(Tkv_pad);
+    L.T_cols_pad = static_cast<int>(Tq_pad);
+    L.x0 = k;
+    L.x1 = v;
+    L.y0 = T_q > 0 ? q : k;
+    L.y1 = T_q > 0 ? d_out : k;
+    if (T_q == 0) L.T_cols = static_cast<int>(T_kv);
+    L.row_idx = k_idx;
+    L.row_hash = hash ? k_hash : k_idx;
+    L.col_idx = q_idx;
+    L.col_hash = hash ? q_hash : q_idx;
+  }
+  L.n_row_blocks = (L.T_rows + 127) / 128;
+  rc = launch_attention(L, static_cast<cudaStream_t>(stream));
+  if (rc && !g_err[0]) set_error("attention backward launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+  return rc;
+}
+
+extern "C" int scfa_attn_bwd_dq(const void* q, const void* k, const void* v, const void* d_out, int64_t BH,
+                                int64_t T_q, int64_t T_kv, int64_t D, const int32_t* q_idx, const int32_t* q_hash,
+                                const int32_t* k_idx, const int32_t* k_hash, int64_t Tq_pad, int64_t Tkv_pad,
+                                const float* lse2, const float* delta, const uint16_t* list,
+                                const int32_t* list_count, int64_t list_stride, float scale, int flags, float* dq,
+                                void* stream) {
+  return bwd_common(1, q, k, v, d_out, BH, T_q, T_kv, D, q_idx, q_hash, k_idx, k_hash, Tq_pad, Tkv_pad, lse2, delta,
+                    list, list_count, list_stride, scale, flags, dq, nullptr, stream);
+}
+
+extern "C" int scfa_attn_bwd_dkdv(const void* q, const void* k, const void* v, const void* d_out, int64_t BH,
+                                  int64_t T_q, int64_t T_kv, int64_t D, const int32_t* q_idx, const int32_t* q_hash,
+                                  const int32_t* k_idx, const int32_t* k_hash, int64_t Tq_pad, int64_t Tkv_pad,
+                                  const float* lse2, const float* delta, const uint16_t* list,
+                                  const int32_t* list_count, int64_t list_stride, float scale, int flags, float* dk,
+                                  float* dv, void* stream) {
+  return bwd_common(2, q, k, v, d_out, BH, T_q, T_kv, D, q_idx, q_hash, k_idx, k_hash, Tq_pad, Tkv_pad, lse2, delta,
+                    list, list_count, list_stride, scale, flags, dk, dv, stream);
+}

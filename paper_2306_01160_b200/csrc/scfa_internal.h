@@ -1,0 +1,53 @@
+// scfa_internal.h — declarations shared between the .cu translation units.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/scfa_b200.h"
+
+namespace scfa {
+
+// Index sentinels (reference pkg/src/scfa/tensors.py:22-24 plus out-of-range slots).
+constexpr int32_t kQueryPad = -1;         // QUERY_PAD
+constexpr int32_t kKeyPad = 1000000000;   // KEY_PAD = 10**9
+constexpr int32_t kColOob = 0x7fffffff;   // key slot past the end of a buffer
+constexpr int32_t kQHashOob = -3;         // bucket sentinel of a query slot past the end
+constexpr int32_t kKHashOob = -2;         // bucket sentinel of a key slot past the end
+
+struct AttnLaunch {
+  int mode;  // 0 fwd, 1 dq, 2 dkdv
+  int D;
+  int BH;
+  int T_rows, T_cols, T_rows_pad, T_cols_pad;
+  const void* x0;
+  const void* x1;
+  const void* y0;
+  const void* y1;
+  const int* row_idx;
+  const int* row_hash;
+  const int* col_idx;
+  const int* col_hash;
+  const float* lse2;
+  const float* delta;
+  const uint16_t* list;
+  const int* list_count;
+  int list_stride;
+  int n_row_blocks;
+  __nv_bfloat16* out_o;
+  float* out0;
+  float* out1;
+  float* out_lse2;
+  float scale;
+  int exclude_self;
+  int use_hash;
+};
+
+int launch_attention(const AttnLaunch& L, cudaStream_t stream);
+int encode_tensor_map_bf16_3d(CUtensorMap* map, const void* base, const cuuint64_t* dims,
+                              const cuuint64_t* strides_bytes, const cuuint32_t* box,
+                              const cuuint32_t* elem_strides);
+void set_error(const char* fmt, ...);
+
+}  // namespace scfa

@@ -1,0 +1,583 @@
+// scfa_prep.cu — index preparation for the SCFA path (HBM-bound integer / byte work).
+//
+//   qk_compact   : stable keep-first permutation per (b, h)   (qk_sparse.py:41-71)
+//   hash_sort    : stable LSD radix sort by bucket per (b, h) (hash_sparse.py:89-133)
+//   gather_rows  : row gather fused with (B,T,H,D)->(B,H,T,D)  (take_along_axis + to_heads)
+//   scatter_rows : inverse routing fused with from_heads       (qk_postprocess / hash_scatter)
+//   build_aux    : padded int32 index / bucket vectors         (pad_index, qk_sparse.py:74-83)
+//   pack_index, validate_*, bwd_prep (delta = rowsum(dO*O), lse2)
+#include <cstdarg>
+#include <cstdio>
+
+#include "scfa_common.cuh"
+#include "scfa_internal.h"
+
+namespace scfa {
+
+// ------------------------------------------------------------------ helpers
+
+SCFA_DEVICE double load_num(const void* p, int dt, int64_t i) {
+  switch (dt) {
+    case SCFA_DT_F32: return static_cast<double>(static_cast<const float*>(p)[i]);
+    case SCFA_DT_F64: return static_cast<const double*>(p)[i];
+    case SCFA_DT_U8: return static_cast<double>(static_cast<const uint8_t*>(p)[i]);
+    case SCFA_DT_I32: return static_cast<double>(static_cast<const int32_t*>(p)[i]);
+    default: return static_cast<double>(static_cast<const int64_t*>(p)[i]);
+  }
+}
+
+SCFA_DEVICE int64_t load_int(const void* p, int dt, int64_t i) {
+  switch (dt) {
+    case SCFA_DT_I32: return static_cast<const int32_t*>(p)[i];
+    case SCFA_DT_I64: return static_cast<const int64_t*>(p)[i];
+    case SCFA_DT_U8: return static_cast<const uint8_t*>(p)[i];
+    case SCFA_DT_F32: return static_cast<int64_t>(static_cast<const float*>(p)[i]);
+    default: return static_cast<int64_t>(static_cast<const double*>(p)[i]);
+  }
+}
+
+SCFA_DEVICE void flag_error(int32_t* err, int code) {
+  if (err) atomicCAS(err, 0, code);
+}
+
+SCFA_DEVICE uint32_t lanemask_lt() {
+  uint32_t r;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+  return r;
+}
+
+// Block-wide exclusive scan of one int per warp (<= 32 warps); returns the
+// exclusive prefix for the calling warp and the block total in *total.
+SCFA_DEVICE int warp_offsets(int warp_val, int* sm /*32+1*/, int* total) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = (blockDim.x + 31) >> 5;
+  if (lane == 0) sm[warp] = warp_val;
+  __syncthreads();
+  if (warp == 0) {
+    int v = lane < nwarps ? sm[lane] : 0;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int n = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += n;
+    }
+    sm[lane] = incl - v;
+    if (lane == 31) sm[32] = incl;
+  }
+  __syncthreads();
+  int r = sm[warp];
+  *total = sm[32];
+  __syncthreads();
+  return r;
+}
+
+// ------------------------------------------------------------------ QK compaction
+
+__global__ void qk_compact_kernel(const void* keep, int dt, int64_t T, int64_t H, int64_t sb, int64_t st,
+                                  int64_t sh, int32_t* perm, int32_t* rank, int32_t* counts, int32_t* err) {
+  __shared__ int sm[33];
+  const int64_t bh = blockIdx.x;
+  const int64_t b = bh / H, h = bh % H;
+  const int64_t base = b * sb + h * sh;
+  const int lane = threadIdx.x & 31;
+
+  // pass 1: kept count (and {0,1} check)
+  int cnt = 0;
+  for (int64_t t = threadIdx.x; t < T; t += blockDim.x) {
+    const double v = load_num(keep, dt, base + t * st);
+    if (v == 1.0) ++cnt;
+    else if (v != 0.0) flag_error(err, SCFA_ERR_SHAPE);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  int total_kept;
+  warp_offsets(cnt, sm, &total_kept);
+  if (threadIdx.x == 0) counts[bh] = total_kept;
+
+  // pass 2: slots.  kept t -> #kept before t ; dropped t -> total_kept + #dropped before t
+  int running = 0;
+  for (int64_t c0 = 0; c0 < T; c0 += blockDim.x) {
+    const int64_t t = c0 + threadIdx.x;
+    const bool kept = (t < T) && (load_num(keep, dt, base + t * st) == 1.0);
+    const uint32_t bal = __ballot_sync(0xffffffffu, kept);
+    const int in_warp = __popc(bal & lanemask_lt());
+    int chunk_total;
+    const int woff = warp_offsets(lane == 0 ? __popc(bal) : 0, sm, &chunk_total);
+    if (t < T) {
+      const int kb = running + woff + in_warp;
+      const int slot = kept ? kb : total_kept + static_cast<int>(t - kb);
+      perm[bh * T + slot] = static_cast<int32_t>(t);
+      rank[bh * T + t] = slot;
+    }
+    running += chunk_total;
+  }
+}
+
+// ------------------------------------------------------------------ hash radix sort
+
+constexpr int kSortThreads = 1024;
+
+struct SortSmem {
+  uint16_t wcnt[32][256];
+  int bin_base[256];
+  int tile_tot[256];
+  int hist[256];
+  int red[33];
+  long long mx[2];
+};
+
+__global__ void __launch_bounds__(kSortThreads) hash_sort_kernel(
+    const void* hash, int hdt, int64_t T, int64_t H, int64_t sb, int64_t st, int64_t sh, const void* pos, int pdt,
+    int64_t ps_bh, int64_t ps_t, int32_t* perm, int32_t* rank, int32_t* scratch, int32_t* err) {
+  __shared__ SortSmem S;
+  const int64_t bh = blockIdx.x;
+  const int64_t b = bh / H, h = bh % H;
+  const int64_t hbase = b * sb + h * sh;
+  const int64_t pbase = bh * ps_bh;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // validate and find the largest key of each kind
+  long long mh = 0, mp = 0;
+  for (int64_t t = threadIdx.x; t < T; t += blockDim.x) {
+    const long long hv = load_int(hash, hdt, hbase + t * st);
+    if (hv < 0 || hv > 0x7fffffffLL) flag_error(err, SCFA_ERR_SHAPE);
+    mh = max(mh, hv);
+    if (pos) {
+      const long long pv = load_int(pos, pdt, pbase + t * ps_t);
+      if (pv < 0 || pv > 0x7fffffffLL) flag_error(err, SCFA_ERR_SHAPE);
+      mp = max(mp, pv);
+    }
+  }
+  if (threadIdx.x == 0) { S.mx[0] = 0; S.mx[1] = 0; }
+  __syncthreads();
+  atomicMax(reinterpret_cast<unsigned long long*>(&S.mx[0]), static_cast<unsigned long long>(max(mh, 0LL)));
+  atomicMax(reinterpret_cast<unsigned long long*>(&S.mx[1]), static_cast<unsigned long long>(max(mp, 0LL)));
+  __syncthreads();
+  const long long max_h = S.mx[0], max_p = S.mx[1];
+  auto nbytes = [](long long m) { int n = 0; while (m > 0) { ++n; m >>= 8; } return n; };
+  const int pos_passes = pos ? nbytes(max_p) : 0;
+  const int hash_passes = nbytes(max_h);
+  const int passes = pos_passes + hash_passes;
+
+  // the final pass must land in `perm`
+  int32_t* bufs[2] = {perm + bh * T, scratch + bh * T};
+  int cur = (passes & 1) ? 1 : 0;
+  for (int64_t s = threadIdx.x; s < T; s += blockDim.x) bufs[cur][s] = static_cast<int32_t>(s);
+  __syncthreads();
+
+  for (int p = 0; p < passes; ++p) {
+    const bool by_pos = p < pos_passes;
+    const int shift = 8 * (by_pos ? p : p - pos_passes);
+    const int32_t* src = bufs[cur];
+    int32_t* dst = bufs[cur ^ 1];
+    auto digit = [&](int32_t t) -> int {
+      const long long key = by_pos ? load_int(pos, pdt, pbase + t * ps_t) : load_int(hash, hdt, hbase + t * st);
+      return static_cast<int>((key >> shift) & 255);
+    };
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) S.hist[i] = 0;
+    for (int i = threadIdx.x; i < 32 * 256; i += blockDim.x) (&S.wcnt[0][0])[i] = 0;
+    __syncthreads();
+    for (int64_t s = threadIdx.x; s < T; s += blockDim.x) atomicAdd(&S.hist[digit(src[s])], 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int acc = 0;
+      for (int i = 0; i < 256; ++i) { S.bin_base[i] = acc; acc += S.hist[i]; }
+    }
+    __syncthreads();
+    for (int64_t c0 = 0; c0 < T; c0 += blockDim.x) {
+      const int64_t s = c0 + threadIdx.x;
+      const bool act = s < T;
+      const int32_t val = act ? src[s] : 0;
+      const int d = act ? digit(val) : 256 + lane;  // inactive lanes never match a real digit
+      const uint32_t same = __match_any_sync(0xffffffffu, d);
+      const int r_in = __popc(same & lanemask_lt());
+      if (act && r_in == 0) S.wcnt[warp][d] = static_cast<uint16_t>(__popc(same));
+      __syncthreads();
+      if (threadIdx.x < 256) {
+        int acc = 0;
+        for (int w = 0; w < 32; ++w) {
+          const int c = S.wcnt[w][threadIdx.x];
+          S.wcnt[w][threadIdx.x] = static_cast<uint16_t>(acc);
+          acc += c;
+        }
+        S.tile_tot[threadIdx.x] = acc;
+      }
+      __syncthreads();
+      if (act) dst[S.bin_base[d] + S.wcnt[warp][d] + r_in] = val;
+      __syncthreads();
+      if (threadIdx.x < 256) {
+        S.bin_base[threadIdx.x] += S.tile_tot[threadIdx.x];
+        for (int w = 0; w < 32; ++w) S.wcnt[w][threadIdx.x] = 0;
+      }
+      __syncthreads();
+    }
+    cur ^= 1;
+  }
+  // cur == 0 now (perm)
+  for (int64_t s = threadIdx.x; s < T; s += blockDim.x) rank[bh * T + perm[bh * T + s]] = static_cast<int32_t>(s);
+}
+
+// ------------------------------------------------------------------ gather / scatter
+
+__global__ void gather_rows_kernel(const uint8_t* __restrict__ src, int eb, int64_t H, int64_t D, int64_t sb,
+                                   int64_t st, int64_t sh, const int32_t* __restrict__ perm, int64_t T_perm,
+                                   int64_t n_slots, uint8_t* __restrict__ dst, int64_t n_rows) {
+  const int64_t row_bytes = D * eb;
+  const int vecs = static_cast<int>(row_bytes / 16);
+  const int64_t total = n_rows * vecs;
+  for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < total;
+       g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = g / vecs;
+    const int v = static_cast<int>(g - r * vecs);
+    const int64_t bh = r / n_slots, s = r - bh * n_slots;
+    const int64_t b = bh / H, h = bh - b * H;
+    const int64_t t = perm[bh * T_perm + s];
+    const uint4* sp = reinterpret_cast<const uint4*>(src + (b * sb + t * st + h * sh) * eb) + v;
+    uint4* dp = reinterpret_cast<uint4*>(dst + r * row_bytes) + v;
+    *dp = __ldg(sp);
+  }
+}
+
+template <typename TS, typename TD>
+SCFA_DEVICE TD cvt(TS x);
+template <> SCFA_DEVICE float cvt<float, float>(float x) { return x; }
+template <> SCFA_DEVICE __nv_bfloat16 cvt<__nv_bfloat16, __nv_bfloat16>(__nv_bfloat16 x) { return x; }
+template <> SCFA_DEVICE float cvt<__nv_bfloat16, float>(__nv_bfloat16 x) { return __bfloat162float(x); }
+template <> SCFA_DEVICE __nv_bfloat16 cvt<float, __nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
+
+template <typename TS, typename TD>
+__global__ void scatter_rows_kernel(const TS* __restrict__ src, int64_t H, int64_t T, int64_t D,
+                                    const int32_t* __restrict__ rank, int64_t n_slots, TD* __restrict__ dst,
+                                    int64_t db, int64_t dt, int64_t dh, int64_t n_rows) {
+  const int per = static_cast<int>(D / 8);  // 8 elements per thread
+  const int64_t total = n_rows * per;
+  for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < total;
+       g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = g / per;  // destination row in (b, t, h) order, h fastest
+    const int c = static_cast<int>(g - r * per) * 8;
+    const int64_t h = r % H;
+    const int64_t t = (r / H) % T;
+    const int64_t b = r / (H * T);
+    const int64_t bh = b * H + h;
+    const int32_t slot = rank[bh * T + t];
+    TD out[8];
+    if (slot < n_slots) {
+      const TS* sp = src + (bh * n_slots + slot) * D + c;
+      TS in[8];
+      if (sizeof(TS) == 2) {
+        *reinterpret_cast<uint4*>(in) = __ldg(reinterpret_cast<const uint4*>(sp));
+      } else {
+        reinterpret_cast<uint4*>(in)[0] = __ldg(reinterpret_cast<const uint4*>(sp));
+        reinterpret_cast<uint4*>(in)[1] = __ldg(reinterpret_cast<const uint4*>(sp) + 1);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) out[i] = cvt<TS, TD>(in[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) out[i] = cvt<float, TD>(0.f);
+    }
+    TD* dp = dst + b * db + t * dt + h * dh + c;
+    if (sizeof(TD) == 2) {
+      *reinterpret_cast<uint4*>(dp) = *reinterpret_cast<uint4*>(out);
+    } else {
+      reinterpret_cast<uint4*>(dp)[0] = reinterpret_cast<uint4*>(out)[0];
+      reinterpret_cast<uint4*>(dp)[1] = reinterpret_cast<uint4*>(out)[1];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ aux vectors
+
+__global__ void build_aux_kernel(const int32_t* __restrict__ perm, const int32_t* __restrict__ counts, int64_t H,
+                                 int64_t T_perm, int64_t n_slots, int64_t T_pad, int32_t pad_value, int32_t oob_value,
+                                 const void* hash, int hdt, int64_t sb, int64_t st, int64_t sh, int32_t hash_oob,
+                                 const void* pos, int pdt, int64_t ps_bh, int64_t ps_t,
+                                 int32_t* __restrict__ idx_out, int32_t* __restrict__ hash_out, int64_t total) {
+  for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < total;
+       g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t bh = g / T_pad, s = g - bh * T_pad;
+    int32_t iv, hv = hash_oob;
+    if (s < n_slots) {
+      const int32_t t = perm[bh * T_perm + s];
+      const int32_t tv = pos ? static_cast<int32_t>(load_int(pos, pdt, bh * ps_bh + static_cast<int64_t>(t) * ps_t)) : t;
+      iv = (counts && s >= counts[bh]) ? pad_value : tv;
+      if (hash_out) {
+        const int64_t b = bh / H, h = bh - b * H;
+        hv = static_cast<int32_t>(load_int(hash, hdt, b * sb + h * sh + static_cast<int64_t>(t) * st));
+      }
+    } else {
+      iv = oob_value;
+    }
+    idx_out[g] = iv;
+    if (hash_out) hash_out[g] = hv;
+  }
+}
+
+__global__ void pack_index_kernel(const void* src, int dt, int64_t T, int64_t s_bh, int64_t s_t, int64_t T_pad,
+                                  int32_t oob_value, int32_t* dst, int64_t total) {
+  for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < total;
+       g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t bh = g / T_pad, t = g - bh * T_pad;
+    int32_t v = oob_value;
+    if (t < T) {
+      long long x = load_int(src, dt, bh * s_bh + t * s_t);
+      if (x > 0x7fffffffLL) x = 0x7fffffffLL;
+      if (x < -0x7fffffffLL) x = -0x7fffffffLL;
+      v = static_cast<int32_t>(x);
+    }
+    dst[g] = v;
+  }
+}
+
+// rank[bh, idx[b, s, h]] = s for s < n_slots; every other position -> n_slots (routes to zero)
+__global__ void fill_i32_kernel(int32_t* dst, int32_t v, int64_t n) {
+  for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < n;
+       g += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[g] = v;
+}
+
+__global__ void invert_index_kernel(const void* idx, int dt, int64_t H, int64_t n_slots, int64_t sb, int64_t ss,
+                                    int64_t sh, int64_t T, int32_t* rank, int32_t* err, int64_t total) {
+  for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < total;
+       g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t bh = g / n_slots, s = g - bh * n_slots;
+    const int64_t b = bh / H, h = bh - b * H;
+    const int64_t t = load_int(idx, dt, b * sb + s * ss + h * sh);
+    if (t < 0 || t >= T) { flag_error(err, SCFA_ERR_SHAPE); continue; }
+    rank[bh * T + t] = static_cast<int32_t>(s);
+  }
+}
+
+// ------------------------------------------------------------------ contract checks
+
+__global__ void validate_qk_kernel(const int32_t* q_idx, const int32_t* k_idx, int64_t T_q, int64_t T_kv,
+                                   int64_t Tq_pad, int64_t Tkv_pad, int32_t* err) {
+  const int64_t bh = blockIdx.x;
+  const int32_t* q = q_idx + bh * Tq_pad;
+  const int32_t* k = k_idx + bh * Tkv_pad;
+  for (int64_t t = threadIdx.x; t + 1 < T_q; t += blockDim.x) {
+    const int32_t a = q[t], c = q[t + 1];
+    if (a == kQueryPad && c != kQueryPad) flag_error(err, SCFA_ERR_CONTRACT);
+    if (a != kQueryPad && c != kQueryPad && c <= a) flag_error(err, SCFA_ERR_CONTRACT);
+  }
+  for (int64_t t = threadIdx.x; t < T_kv; t += blockDim.x) {
+    const int32_t a = k[t];
+    if (t + 1 < T_kv) {
+      const int32_t c = k[t + 1];
+      if (a == kKeyPad && c != kKeyPad) flag_error(err, SCFA_ERR_CONTRACT);
+      if (a != kKeyPad && c != kKeyPad && c <= a) flag_error(err, SCFA_ERR_CONTRACT);
+    }
+    if (a != kKeyPad && a >= kKeyPad) flag_error(err, SCFA_ERR_CONTRACT);
+  }
+}
+
+__global__ void validate_sorted_kernel(const int32_t* idx, const int32_t* hash, int64_t T, int64_t T_pad,
+                                       int32_t* err) {
+  const int64_t bh = blockIdx.x;
+  const int32_t* ix = idx + bh * T_pad;
+  const int32_t* hs = hash + bh * T_pad;
+  for (int64_t t = threadIdx.x; t + 1 < T; t += blockDim.x) {
+    if (hs[t + 1] < hs[t]) flag_error(err, SCFA_ERR_CONTRACT);
+    else if (hs[t + 1] == hs[t] && ix[t + 1] <= ix[t]) flag_error(err, SCFA_ERR_CONTRACT);
+  }
+}
+
+// ------------------------------------------------------------------ backward prep
+
+__global__ void bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ d_out,
+                                const float* __restrict__ lse2_in, const float* __restrict__ m,
+                                const float* __restrict__ l, int64_t T_q, int64_t D, int64_t Tq_pad,
+                                float* __restrict__ delta, float* __restrict__ lse2_out, int64_t total_rows) {
+  const int tpr = static_cast<int>(D / 8);  // threads per row, 16 B each
+  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t r = g / tpr;  // padded row index
+  const int part = static_cast<int>(g - r * tpr);
+  float acc = 0.f;
+  const bool live = r < total_rows;
+  const int64_t bh = live ? r / Tq_pad : 0, t = live ? r - bh * Tq_pad : 0;
+  const bool valid = live && t < T_q;
+  if (valid) {
+    const int64_t off = (bh * T_q + t) * D + part * 8;
+    uint4 a = __ldg(reinterpret_cast<const uint4*>(o + off));
+    uint4 c = __ldg(reinterpret_cast<const uint4*>(d_out + off));
+    const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+    const __nv_bfloat162* c2 = reinterpret_cast<const __nv_bfloat162*>(&c);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 x = __bfloat1622float2(a2[i]);
+      const float2 y = __bfloat1622float2(c2[i]);
+      acc = fmaf(x.x, y.x, acc);
+      acc = fmaf(x.y, y.y, acc);
+    }
+  }
+  // reduce over the tpr lanes of a row (tpr is a power of two <= 32 and rows never straddle warps)
+  for (int w = tpr >> 1; w > 0; w >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, w);
+  if (live && part == 0) {
+    delta[r] = valid ? acc : 0.f;
+    float lv = INFINITY;
+    if (valid) {
+      if (lse2_in) {
+        lv = lse2_in[r];
+      } else {
+        const float M = m[bh * T_q + t], L = l[bh * T_q + t];
+        lv = (L > 0.f) ? M * 1.4426950408889634f + log2f(L) : INFINITY;
+      }
+    }
+    lse2_out[r] = lv;
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+
+static int grid_for(int64_t work, int threads) {
+  int64_t g = (work + threads - 1) / threads;
+  if (g > 148 * 64) g = 148 * 64;
+  if (g < 1) g = 1;
+  return static_cast<int>(g);
+}
+
+static int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return SCFA_ERR_CUDA;
+  }
+  return SCFA_OK;
+}
+
+}  // namespace scfa
+
+using namespace scfa;
+
+extern "C" int scfa_qk_compact(const void* keep, int keep_dtype, int64_t B, int64_t T, int64_t H, int64_t sb,
+                               int64_t st, int64_t sh, int32_t* perm, int32_t* rank, int32_t* counts,
+                               int32_t* err_flag, void* stream) {
+  if (B < 0 || T < 0 || H < 0) { set_error("negative extent"); return SCFA_ERR_SHAPE; }
+  if (B * H == 0 || T == 0) {
+    if (B * H > 0) cudaMemsetAsync(counts, 0, B * H * sizeof(int32_t), static_cast<cudaStream_t>(stream));
+    return SCFA_OK;
+  }
+  qk_compact_kernel<<<static_cast<unsigned>(B * H), 1024, 0, static_cast<cudaStream_t>(stream)>>>(
+      keep, keep_dtype, T, H, sb, st, sh, perm, rank, counts, err_flag);
+  return check_launch("qk_compact");
+}
+
+extern "C" int scfa_hash_sort(const void* hash, int hash_dtype, int64_t B, int64_t T, int64_t H, int64_t sb,
+                              int64_t st, int64_t sh, const void* pos, int pos_dtype, int64_t ps_bh, int64_t ps_t,
+                              int32_t* perm, int32_t* rank, int32_t* scratch, int32_t* err_flag, void* stream) {
+  if (B * H == 0 || T == 0) return SCFA_OK;
+  hash_sort_kernel<<<static_cast<unsigned>(B * H), kSortThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      hash, hash_dtype, T, H, sb, st, sh, pos, pos_dtype, ps_bh, ps_t, perm, rank, scratch, err_flag);
+  return check_launch("hash_sort");
+}
+
+extern "C" int scfa_gather_rows(const void* src, int elem_bytes, int64_t B, int64_t H, int64_t D, int64_t sb,
+                                int64_t st, int64_t sh, const int32_t* perm, int64_t T_perm, int64_t n_slots,
+                                void* dst, void* stream) {
+  if ((D * elem_bytes) % 16 != 0) { set_error("row bytes must be a multiple of 16"); return SCFA_ERR_SHAPE; }
+  if (((sb | st | sh) * elem_bytes) % 16 != 0 || (reinterpret_cast<uintptr_t>(src) & 15) ||
+      (reinterpret_cast<uintptr_t>(dst) & 15)) {
+    set_error("gather rows must be 16-byte aligned");
+    return SCFA_ERR_SHAPE;
+  }
+  const int64_t n_rows = B * H * n_slots;
+  if (n_rows == 0) return SCFA_OK;
+  const int64_t work = n_rows * (D * elem_bytes / 16);
+  gather_rows_kernel<<<grid_for(work, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint8_t*>(src), elem_bytes, H, D, sb, st, sh, perm, T_perm, n_slots,
+      static_cast<uint8_t*>(dst), n_rows);
+  return check_launch("gather_rows");
+}
+
+extern "C" int scfa_scatter_rows(const void* src, int src_bytes, int64_t B, int64_t H, int64_t T, int64_t D,
+                                 const int32_t* rank, int64_t n_slots, void* dst, int dst_bytes, int64_t db,
+                                 int64_t dt, int64_t dh, void* stream) {
+  if (D % 8 != 0) { set_error("D must be a multiple of 8"); return SCFA_ERR_SHAPE; }
+  const int64_t n_rows = B * T * H;
+  if (n_rows == 0) return SCFA_OK;
+  const int64_t work = n_rows * (D / 8);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int g = grid_for(work, 256);
+  if (src_bytes == 2 && dst_bytes == 2)
+    scatter_rows_kernel<__nv_bfloat16, __nv_bfloat16><<<g, 256, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(src), H, T, D, rank, n_slots, static_cast<__nv_bfloat16*>(dst), db, dt,
+        dh, n_rows);
+  else if (src_bytes == 4 && dst_bytes == 4)
+    scatter_rows_kernel<float, float><<<g, 256, 0, s>>>(static_cast<const float*>(src), H, T, D, rank, n_slots,
+                                                       static_cast<float*>(dst), db, dt, dh, n_rows);
+  else if (src_bytes == 4 && dst_bytes == 2)
+    scatter_rows_kernel<float, __nv_bfloat16><<<g, 256, 0, s>>>(static_cast<const float*>(src), H, T, D, rank,
+                                                               n_slots, static_cast<__nv_bfloat16*>(dst), db, dt,
+                                                               dh, n_rows);
+  else if (src_bytes == 2 && dst_bytes == 4)
+    scatter_rows_kernel<__nv_bfloat16, float><<<g, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(src), H, T, D,
+                                                               rank, n_slots, static_cast<float*>(dst), db, dt,
+                                                               dh, n_rows);
+  else { set_error("unsupported element sizes"); return SCFA_ERR_SHAPE; }
+  return check_launch("scatter_rows");
+}
+
+extern "C" int scfa_build_aux(const int32_t* perm, const int32_t* counts, int64_t B, int64_t H, int64_t T_perm,
+                              int64_t n_slots, int64_t T_pad, int32_t pad_value, int32_t oob_value,
+                              const void* hash, int hash_dtype, int64_t sb, int64_t st, int64_t sh,
+                              int32_t hash_oob, const void* pos, int pos_dtype, int64_t ps_bh, int64_t ps_t,
+                              int32_t* idx_out, int32_t* hash_out, void* stream) {
+  const int64_t total = B * H * T_pad;
+  if (total == 0) return SCFA_OK;
+  build_aux_kernel<<<grid_for(total, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      perm, counts, H, T_perm, n_slots, T_pad, pad_value, oob_value, hash, hash_dtype, sb, st, sh, hash_oob, pos,
+      pos_dtype, ps_bh, ps_t, idx_out, hash ? hash_out : nullptr, total);
+  return check_launch("build_aux");
+}
+
+extern "C" int scfa_pack_index(const void* src, int dtype, int64_t BH, int64_t T, int64_t s_bh, int64_t s_t,
+                               int64_t T_pad, int32_t oob_value, int32_t* dst, void* stream) {
+  const int64_t total = BH * T_pad;
+  if (total == 0) return SCFA_OK;
+  pack_index_kernel<<<grid_for(total, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      src, dtype, T, s_bh, s_t, T_pad, oob_value, dst, total);
+  return check_launch("pack_index");
+}
+
+extern "C" int scfa_validate_qk(const int32_t* q_idx, const int32_t* k_idx, int64_t BH, int64_t T_q, int64_t T_kv,
+                                int64_t Tq_pad, int64_t Tkv_pad, int32_t* err_flag, void* stream) {
+  if (BH == 0) return SCFA_OK;
+  validate_qk_kernel<<<static_cast<unsigned>(BH), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      q_idx, k_idx, T_q, T_kv, Tq_pad, Tkv_pad, err_flag);
+  return check_launch("validate_qk");
+}
+
+extern "C" int scfa_validate_sorted(const int32_t* idx, const int32_t* hash, int64_t BH, int64_t T, int64_t T_pad,
+                                    int32_t* err_flag, void* stream) {
+  if (BH == 0) return SCFA_OK;
+  validate_sorted_kernel<<<static_cast<unsigned>(BH), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      idx, hash, T, T_pad, err_flag);
+  return check_launch("validate_sorted");
+}
+
+extern "C" int scfa_bwd_prep(const void* o, const void* d_out, const float* lse2_in, const float* m, const float* l,
+                             int64_t BH, int64_t T_q, int64_t D, int64_t Tq_pad, float scale, float* delta,
+                             float* lse2_out, void* stream) {
+  (void)scale;
+  if (D % 8 != 0 || D / 8 > 32 || ((D / 8) & (D / 8 - 1))) { set_error("bwd_prep: unsupported D"); return SCFA_ERR_SHAPE; }
+  const int64_t rows = BH * Tq_pad;
+  if (rows == 0) return SCFA_OK;
+  const int64_t threads = rows * (D / 8);
+  bwd_prep_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(d_out), lse2_in, m, l, T_q, D, Tq_pad,
+      delta, lse2_out, rows);
+  return check_launch("bwd_prep");
+}
+
+extern "C" int scfa_invert_index(const void* idx, int dtype, int64_t B, int64_t n_slots, int64_t H, int64_t sb,
+                                 int64_t ss, int64_t sh, int64_t T, int32_t* rank, int32_t* err_flag, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t n = B * H * T;
+  if (n == 0) return SCFA_OK;
+  fill_i32_kernel<<<grid_for(n, 256), 256, 0, s>>>(rank, static_cast<int32_t>(n_slots), n);
+  const int64_t total = B * H * n_slots;
+  if (total > 0)
+    invert_index_kernel<<<grid_for(total, 256), 256, 0, s>>>(idx, dtype, H, n_slots, sb, ss, sh, T, rank, err_flag,
+                                                              total);
+  return check_launch("invert_index");
+}

@@ -1,0 +1,300 @@
+"""Hash-sparse attention: bucket sort, banded kernels, inverse scatter — on the GPU.
+
+API mirror of pkg/src/scfa/hash_sparse.py.  Bucket ids arrive as (B, T, H)
+(boundary) or (B, H, T) (engine) integer tensors; a stable per-(b, h) radix
+sort by bucket (ties kept in position order, hash_sparse.py:89-94) produces
+a permutation that drives a fused gather+transpose of Q/K/V, the exact tile
+lists and the tcgen05 kernels; the inverse permutation routes outputs back.
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._kernel import (
+    FlashOutputs,
+    Problem,
+    as_operand,
+    attention_backward,
+    attention_forward,
+    check_forward_operands,
+    pack_index,
+)
+from .errors import NumericError, ParameterError, ShapeError
+from .tensors import DOMAIN_BUCKETS, DOMAIN_PROJECTIONS, BlockSpec, pad128, stream
+
+_OOB_QI, _OOB_KI = -1, 0x7FFFFFFF
+_OOB_QH, _OOB_KH = -3, -2
+
+
+@dataclass
+class SortedBatch:
+    """Operands reordered by bucket plus provenance (hash_sparse.py:71-86).
+
+    q/k/v (B, H, T, D) bf16; q_idx/k_idx (B, H, T) int32 original positions;
+    q_hash/k_hash (B, H, T) int32 sorted bucket ids.
+    """
+
+    q: torch.Tensor
+    k: torch.Tensor
+    v: torch.Tensor
+    q_idx: torch.Tensor
+    k_idx: torch.Tensor
+    q_hash: torch.Tensor
+    k_hash: torch.Tensor
+    problem: object = None
+    q_rank: torch.Tensor = None  # (B*H, T_Q) position -> sorted slot
+    k_rank: torch.Tensor = None
+    q_perm: torch.Tensor = None  # (B*H, T_Q) sorted slot -> position
+    k_perm: torch.Tensor = None
+
+
+def random_buckets(B, T, H, nb, seed):
+    """Uniform bucket ids, same stream as hash_sparse.py:55-60 (numpy, int64)."""
+    if nb < 1:
+        raise ParameterError(f"number of buckets must be >= 1, got {nb}")
+    return stream(seed, DOMAIN_BUCKETS).integers(0, nb, size=(B, T, H), dtype=np.int64)
+
+
+def lsh_buckets(x, nb, seed):
+    """Angular LSH codes for (B, T, H, D) vectors (hash_sparse.py:34-52).
+
+    The projections are drawn from the reference's Philox streams on the host
+    so ids agree with the reference; the projection + argmax runs on the GPU.
+    """
+    if nb < 2 or nb % 2 != 0:
+        raise ParameterError(f"number of buckets must be even and >= 2, got {nb}")
+    x = torch.as_tensor(x)
+    B, T, H, D = x.shape
+    dev = x.device if x.is_cuda else torch.device("cuda")
+    R = np.stack([stream(seed, DOMAIN_PROJECTIONS, b * H + h).standard_normal((D, nb // 2))
+                  for b in range(B) for h in range(H)]).reshape(B, H, D, nb // 2)
+    R = torch.from_numpy(R).to(dev)
+    rot = torch.einsum("bthd,bhdn->bthn", x.to(dev, torch.float64), R)
+    return torch.cat([rot, -rot], dim=-1).argmax(dim=-1)
+
+
+def normalize_keys(q):
+    """Shared-QK keys: rows scaled to unit norm (hash_sparse.py:63-68)."""
+    q = torch.as_tensor(q)
+    n = torch.linalg.vector_norm(q.float(), dim=-1, keepdim=True)
+    if bool((n == 0).any()):
+        raise NumericError("cannot normalize zero-norm rows")
+    return (q.float() / n).to(q.dtype)
+
+
+def _hash_view(h, B, H, T, layout):
+    """Element strides (sb, st, sh) of a bucket tensor in 'bth' or 'bht' layout."""
+    h = torch.as_tensor(h)
+    if layout == "bht":
+        if tuple(h.shape) != (B, H, T):
+            raise ShapeError("hash tensors must be (B, H, T) matching the operands")
+        return h, h.stride(0), h.stride(2), h.stride(1)
+    if tuple(h.shape) != (B, T, H):
+        raise ShapeError("hash tensors must be (B, T, H) matching the operands")
+    return h, h.stride(0), h.stride(1), h.stride(2)
+
+
+def _sort(hash_t, sb, st, sh, B, H, T, err, pos=None):
+    dev = hash_t.device
+    perm = torch.empty((B * H, T), dtype=torch.int32, device=dev)
+    rank = torch.empty((B * H, T), dtype=torch.int32, device=dev)
+    scratch = torch.empty((B * H, T), dtype=torch.int32, device=dev)
+    if pos is not None:
+        pos2 = pos.reshape(B * H, T)
+        pargs = (_lib.ptr(pos2), _lib.dtype_code(pos2), pos2.stride(0), pos2.stride(1))
+    else:
+        pargs = (None, 0, 0, 0)
+    _lib.call("scfa_hash_sort", _lib.ptr(hash_t), _lib.dtype_code(hash_t), B, T, H, sb, st, sh, *pargs,
+              _lib.ptr(perm), _lib.ptr(rank), _lib.ptr(scratch), _lib.ptr(err), _lib.stream_ptr())
+    return perm, rank
+
+
+def _aux(perm, hash_t, sb, st, sh, B, H, T, oob_i, oob_h, pos=None):
+    T_pad = pad128(T)
+    dev = perm.device
+    idx = torch.empty((B * H, T_pad), dtype=torch.int32, device=dev)
+    hsh = torch.empty((B * H, T_pad), dtype=torch.int32, device=dev)
+    if pos is not None:
+        pos2 = pos.reshape(B * H, T)
+        pargs = (_lib.ptr(pos2), _lib.dtype_code(pos2), pos2.stride(0), pos2.stride(1))
+    else:
+        pargs = (None, 0, 0, 0)
+    _lib.call("scfa_build_aux", _lib.ptr(perm), None, B, H, T, T, T_pad, 0, int(oob_i),
+              _lib.ptr(hash_t), _lib.dtype_code(hash_t), sb, st, sh, int(oob_h), *pargs,
+              _lib.ptr(idx), _lib.ptr(hsh), _lib.stream_ptr())
+    return idx, hsh
+
+
+def _gather(x, perm, layout):
+    """Rows of x ('bthd' or 'bhtd') in perm order -> (B, H, T, D)."""
+    if layout == "bthd":
+        B, T, H, D = x.shape
+        sb, st, sh = x.stride(0), x.stride(1), x.stride(2)
+    else:
+        B, H, T, D = x.shape
+        sb, st, sh = x.stride(0), x.stride(2), x.stride(1)
+    out = torch.empty((B, H, perm.shape[1], D), dtype=x.dtype, device=x.device)
+    _lib.call("scfa_gather_rows", _lib.ptr(x), x.element_size(), B, H, D, sb, st, sh, _lib.ptr(perm),
+              perm.shape[1], perm.shape[1], _lib.ptr(out), _lib.stream_ptr())
+    return out
+
+
+def _scatter(src, rank, layout, out_dtype=None):
+    """(B, H, T, D) sorted rows -> original positions, in 'bthd' or 'bhtd' layout."""
+    B, H, T, D = src.shape
+    src = src.contiguous()
+    dt = out_dtype or src.dtype
+    if layout == "bthd":
+        out = torch.empty((B, T, H, D), dtype=dt, device=src.device)
+        db, dtt, dh = out.stride(0), out.stride(1), out.stride(2)
+    else:
+        out = torch.empty((B, H, T, D), dtype=dt, device=src.device)
+        db, dtt, dh = out.stride(0), out.stride(2), out.stride(1)
+    _lib.call("scfa_scatter_rows", _lib.ptr(src), src.element_size(), B, H, T, D, _lib.ptr(rank), T,
+              _lib.ptr(out), out.element_size(), db, dtt, dh, _lib.stream_ptr())
+    return out
+
+
+def _sort_batch(q, k, v, q_hash, k_hash, layout, q_pos=None, k_pos=None, check=True):
+    """Shared by sort_by_bucket (engine layout) and hash_sparse_attention (boundary layout)."""
+    if layout == "bhtd":
+        check_forward_operands(q, k, v)
+        B, H, T_Q, D = q.shape
+        T_KV = k.shape[2]
+        hl = "bht"
+    else:
+        if q.dim() != 4 or k.dim() != 4 or k.shape != v.shape or q.shape[0] != k.shape[0] or q.shape[2] != k.shape[
+                2] or q.shape[3] != k.shape[3]:
+            raise ShapeError(f"operand shapes disagree: {tuple(q.shape)}, {tuple(k.shape)}, {tuple(v.shape)}")
+        B, T_Q, H, D = q.shape
+        T_KV = k.shape[1]
+        hl = "bth"
+    dev = q.device
+    qh, qsb, qst, qsh = _hash_view(torch.as_tensor(q_hash, device=dev), B, H, T_Q, hl)
+    same = (k_hash is q_hash) and T_Q == T_KV and q_pos is None and k_pos is None
+    if same:
+        kh, ksb, kst, ksh = qh, qsb, qst, qsh
+    else:
+        kh, ksb, kst, ksh = _hash_view(torch.as_tensor(k_hash, device=dev), B, H, T_KV, hl)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    q_perm, q_rank = _sort(qh, qsb, qst, qsh, B, H, T_Q, err, q_pos)
+    if same:
+        k_perm, k_rank = q_perm, q_rank
+    else:
+        k_perm, k_rank = _sort(kh, ksb, kst, ksh, B, H, T_KV, err, k_pos)
+    if check and int(err.item()):
+        raise ShapeError("bucket ids must be non-negative (and < 2**31)")
+    q_s = _gather(q, q_perm, layout)
+    k_s = _gather(k, k_perm, layout)
+    v_s = _gather(v, k_perm, layout)
+    qi, qhs = _aux(q_perm, qh, qsb, qst, qsh, B, H, T_Q, _OOB_QI, _OOB_QH, q_pos)
+    ki, khs = _aux(k_perm, kh, ksb, kst, ksh, B, H, T_KV, _OOB_KI, _OOB_KH, k_pos)
+    problem = Problem(B, H, T_Q, T_KV, D, qi, ki, qhs, khs, flags=_lib.FLAG_HASH)
+    return SortedBatch(
+        q=q_s, k=k_s, v=v_s,
+        q_idx=qi[:, :T_Q].view(B, H, T_Q), k_idx=ki[:, :T_KV].view(B, H, T_KV),
+        q_hash=qhs[:, :T_Q].view(B, H, T_Q), k_hash=khs[:, :T_KV].view(B, H, T_KV),
+        problem=problem, q_rank=q_rank, k_rank=k_rank, q_perm=q_perm, k_perm=k_perm,
+    )
+
+
+def sort_by_bucket(q, k, v, q_hash, k_hash, q_idx=None, k_idx=None):
+    """Reorder engine-layout operands by (bucket, position) (hash_sparse.py:97-133)."""
+    q, k, v = as_operand(q), as_operand(k), as_operand(v)
+    dev = q.device
+    qp = None if q_idx is None else torch.as_tensor(q_idx, device=dev)
+    kp = None if k_idx is None else torch.as_tensor(k_idx, device=dev)
+    if qp is not None:
+        qp = qp.expand(q.shape[0], q.shape[1], q.shape[2])
+    if kp is not None:
+        kp = kp.expand(k.shape[0], k.shape[1], k.shape[2])
+    return _sort_batch(q, k, v, q_hash, k_hash, "bhtd", qp, kp)
+
+
+def _problem_of(sb, exclude_self, validate=True):
+    flags = _lib.FLAG_HASH | (_lib.FLAG_EXCLUDE_SELF if exclude_self else 0)
+    prob = sb.problem
+    B, H, T_Q, D = sb.q.shape
+    T_KV = sb.k.shape[2]
+    if prob is None or prob.T_q != T_Q or prob.T_kv != T_KV:
+        dev = sb.q.device
+        BH = B * H
+        prob = Problem(B, H, T_Q, T_KV, D,
+                       pack_index(sb.q_idx, BH, T_Q, _OOB_QI, dev), pack_index(sb.k_idx, BH, T_KV, _OOB_KI, dev),
+                       pack_index(sb.q_hash, BH, T_Q, _OOB_QH, dev), pack_index(sb.k_hash, BH, T_KV, _OOB_KH, dev),
+                       flags=flags)
+        if validate and BH:
+            prob.validate("hash")
+        return prob
+    if prob.flags != flags:
+        clone = Problem(prob.B, prob.H, prob.T_q, prob.T_kv, prob.D, prob.q_idx, prob.k_idx, prob.q_hash,
+                        prob.k_hash, flags=flags)
+        prob = clone
+    return prob
+
+
+def hash_forward_kernel(sorted_batch, scale=None, blocks=BlockSpec(), exclude_self=True, workers=None):
+    """Banded forward over a SortedBatch (hash_sparse.py:145-179)."""
+    sb = sorted_batch
+    sb.q, sb.k, sb.v = as_operand(sb.q), as_operand(sb.k), as_operand(sb.v)
+    check_forward_operands(sb.q, sb.k, sb.v)
+    prob = _problem_of(sb, exclude_self)
+    return attention_forward(prob, sb.q, sb.k, sb.v, scale, blocks)
+
+
+def hash_backward_kernel(sorted_batch, outputs, d_out_sorted, scale=None, blocks=BlockSpec(), exclude_self=True,
+                         workers=None):
+    """Gradients w.r.t. the sorted operands, fp32 (hash_sparse.py:182-213)."""
+    sb = sorted_batch
+    check_forward_operands(sb.q, sb.k, sb.v)
+    if tuple(d_out_sorted.shape) != tuple(sb.q.shape):
+        raise ShapeError(f"dO shape {tuple(d_out_sorted.shape)} != {tuple(sb.q.shape)}")
+    prob = getattr(outputs, "_problem", None)
+    want = _lib.FLAG_HASH | (_lib.FLAG_EXCLUDE_SELF if exclude_self else 0)
+    if prob is None or prob.flags != want or prob.T_q != sb.q.shape[2]:
+        prob = _problem_of(sb, exclude_self)
+    return attention_backward(prob, as_operand(sb.q), as_operand(sb.k), as_operand(sb.v), outputs, d_out_sorted,
+                              scale)
+
+
+def hash_scatter(o_sorted, q_idx):
+    """out[..., q_idx[p], :] = o_sorted[..., p, :] in engine layout (hash_sparse.py:216-220)."""
+    o_sorted = torch.as_tensor(o_sorted)
+    B, H, T, D = o_sorted.shape
+    idx = torch.as_tensor(q_idx, device=o_sorted.device)
+    rank = torch.empty((B * H, T), dtype=torch.int32, device=o_sorted.device)
+    err = torch.zeros(1, dtype=torch.int32, device=o_sorted.device)
+    # idx is (B, H, T): element (b, s, h) at b*s0 + s*s2 + h*s1
+    _lib.call("scfa_invert_index", _lib.ptr(idx), _lib.dtype_code(idx), B, T, H, idx.stride(0), idx.stride(2),
+              idx.stride(1), T, _lib.ptr(rank), _lib.ptr(err), _lib.stream_ptr())
+    return _scatter(o_sorted, rank, "bhtd")
+
+
+def hash_sparse_attention(q, k, v, q_hash, k_hash, scale=None, blocks=BlockSpec(), exclude_self=True,
+                          workers=None):
+    """End-to-end hash-sparse attention in boundary layout (hash_sparse.py:223-238)."""
+    q, k, v = as_operand(q), as_operand(k), as_operand(v)
+    sb = _sort_batch(q, k, v, q_hash, k_hash, "bthd")
+    prob = _problem_of(sb, exclude_self)
+    outputs = attention_forward(prob, sb.q, sb.k, sb.v, scale, blocks)
+    return _scatter(outputs.O, sb.q_rank, "bthd")
+
+
+def hash_sparse_attention_fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, exclude_self=True):
+    """Forward + backward through the whole hash path, boundary layout in and out.
+
+    Returns (O bf16, dQ, dK, dV fp32), each (B, T, H, D).  The reference
+    composes the same from sort_by_bucket -> hash_forward_kernel ->
+    hash_backward_kernel(dO sorted by q order) -> inverse permutation.
+    """
+    q, k, v = as_operand(q), as_operand(k), as_operand(v)
+    sb = _sort_batch(q, k, v, q_hash, k_hash, "bthd", check=False)
+    prob = _problem_of(sb, exclude_self)
+    outputs = attention_forward(prob, sb.q, sb.k, sb.v, scale)
+    d_out_s = _gather(as_operand(d_out), sb.q_perm, "bthd")
+    dq, dk, dv = attention_backward(prob, sb.q, sb.k, sb.v, outputs, d_out_s, scale)
+    return (_scatter(outputs.O, sb.q_rank, "bthd"), _scatter(dq, sb.q_rank, "bthd"),
+            _scatter(dk, sb.k_rank, "bthd"), _scatter(dv, sb.k_rank, "bthd"))

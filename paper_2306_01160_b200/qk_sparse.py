@@ -1,0 +1,276 @@
+"""QK-sparse attention: per-head query/key dropping on the GPU.
+
+API mirror of pkg/src/scfa/qk_sparse.py.  Boundary tensors are (B, T, H, D)
+with keep indicators (B, T, H); the kernels run on compacted engine-layout
+operands (B, H, T_c, D) whose original positions travel in padded int32
+index vectors (query pad -1, key pad 10**9, qk_sparse.py:1-8).
+
+Device work per call: one compaction kernel per side (stable keep-first
+order), one row-gather per operand fused with the (B,T,H,D)->(B,H,T,D)
+transpose, the padded index vectors, the tcgen05 attention kernels, and one
+scatter fused with the inverse transpose.  The only host synchronisation is
+the read of the buffer sizes (max kept count), which the reference also
+needs before it can allocate (qk_sparse.py:58).
+"""
+
+from typing import NamedTuple
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._kernel import (
+    FlashOutputs,
+    Problem,
+    as_operand,
+    attention_backward,
+    attention_forward,
+    check_forward_operands,
+    pack_index,
+)
+from .errors import ShapeError
+from .tensors import DOMAIN_KEEP, KEY_PAD, QUERY_PAD, BlockSpec, pad128, stream
+
+_OOB_Q = QUERY_PAD
+_OOB_K = 0x7FFFFFFF
+
+
+class CompactResult(NamedTuple):
+    compact: torch.Tensor  # (B, buffer_size, H, D) boundary layout
+    index: torch.Tensor  # (B, buffer_size, H) original positions
+    indices_per_head: torch.Tensor  # (B, H) kept counts; None when index was given
+
+
+class QkPrepared(NamedTuple):
+    q_c: torch.Tensor  # (B, H, T_cq, D) bf16
+    k_c: torch.Tensor  # (B, H, T_ck, D)
+    v_c: torch.Tensor  # (B, H, T_ck, D)
+    q_idx: torch.Tensor  # (B, H, T_cq) int32 padded positions
+    k_idx: torch.Tensor  # (B, H, T_ck)
+    scatter_index: torch.Tensor  # (B, T_cq, H) unpadded query gather order
+    T_Q: int
+    problem: object = None  # engine Problem (padded vectors, schedules)
+    q_rank: torch.Tensor = None  # (B*H, T_Q) position -> slot
+    k_rank: torch.Tensor = None  # (B*H, T_KV)
+
+
+def _keep_tensor(keep, shape, device):
+    keep = torch.as_tensor(keep, device=device)
+    if tuple(keep.shape) != tuple(shape):
+        raise ShapeError(f"keep shape {tuple(keep.shape)} != {tuple(shape)}")
+    return keep
+
+
+def _compact_perm(keep, B, T, H, counts_out, err):
+    """Run the compaction kernel; returns (perm, rank) as (B*H, T) int32."""
+    dev = keep.device
+    perm = torch.empty((B * H, T), dtype=torch.int32, device=dev)
+    rank = torch.empty((B * H, T), dtype=torch.int32, device=dev)
+    _lib.call("scfa_qk_compact", _lib.ptr(keep), _lib.dtype_code(keep), B, T, H,
+              keep.stride(0), keep.stride(1), keep.stride(2),
+              _lib.ptr(perm), _lib.ptr(rank), _lib.ptr(counts_out), _lib.ptr(err), _lib.stream_ptr())
+    return perm, rank
+
+
+def _gather(x_btHd, perm, n_slots):
+    """(B, T, H, D) boundary tensor -> (B, H, n_slots, D) rows in `perm` order."""
+    B, T, H, D = x_btHd.shape
+    out = torch.empty((B, H, n_slots, D), dtype=x_btHd.dtype, device=x_btHd.device)
+    _lib.call("scfa_gather_rows", _lib.ptr(x_btHd), x_btHd.element_size(), B, H, D,
+              x_btHd.stride(0), x_btHd.stride(1), x_btHd.stride(2), _lib.ptr(perm), perm.shape[1],
+              n_slots, _lib.ptr(out), _lib.stream_ptr())
+    return out
+
+
+def _aux(perm, counts, B, H, n_slots, pad, oob):
+    T_pad = pad128(n_slots)
+    out = torch.empty((B * H, T_pad), dtype=torch.int32, device=perm.device)
+    _lib.call("scfa_build_aux", _lib.ptr(perm), _lib.ptr(counts), B, H, perm.shape[1], n_slots, T_pad,
+              int(pad), int(oob), None, 0, 0, 0, 0, 0, None, 0, 0, 0, _lib.ptr(out), None, _lib.stream_ptr())
+    return out
+
+
+def compact(keep, x, index=None):
+    """Gather kept rows of x (B, T, H, D) into a dense prefix per head (qk_sparse.py:41-71)."""
+    x = as_operand(x) if not (isinstance(x, torch.Tensor) and x.is_cuda) else x.contiguous()
+    B, T, H, D = x.shape
+    dev = x.device
+    if index is None:
+        keep = _keep_tensor(keep, (B, T, H), dev)
+        cnt = torch.zeros(B * H + 1, dtype=torch.int32, device=dev)
+        perm, _ = _compact_perm(keep, B, T, H, cnt[: B * H], cnt[B * H:])
+        host = cnt.cpu()
+        if int(host[B * H]):
+            raise ShapeError("keep entries must be 0 or 1")
+        counts = host[: B * H].to(torch.int64).reshape(B, H)
+        buffer = int(counts.max()) if counts.numel() else 0
+        index = perm[:, :buffer].reshape(B, H, buffer).transpose(1, 2)
+        counts_out = counts.to(dev)
+    else:
+        index = torch.as_tensor(index, device=dev)
+        if index.dim() != 3 or index.shape[0] != B or index.shape[2] != H:
+            raise ShapeError(f"index shape {tuple(index.shape)} incompatible with x")
+        if index.numel() and (int(index.min()) < 0 or int(index.max()) >= T):
+            raise ShapeError("supplied index out of range")
+        buffer = index.shape[1]
+        perm = index.transpose(1, 2).reshape(B * H, buffer).to(torch.int32).contiguous()
+        counts_out = None
+    g = _gather(x, perm, buffer)  # (B, H, buffer, D)
+    return CompactResult(g.transpose(1, 2), index, counts_out)
+
+
+def pad_index(index, indices_per_head, pad_idx):
+    """Slots past each head's kept count -> pad_idx (qk_sparse.py:74-83); returns a copy."""
+    index = torch.as_tensor(index)
+    B, buf, H = index.shape
+    counts = torch.as_tensor(indices_per_head, device=index.device)
+    slot = torch.arange(buf, device=index.device).view(1, buf, 1)
+    out = index.to(torch.int64).clone()
+    out[slot >= counts.view(B, 1, H)] = int(pad_idx)
+    return out
+
+
+def qk_tile_schedule(q_idx, k_idx, blocks=BlockSpec()):
+    """Reference j_stop per query block for one head's padded index vectors (qk_sparse.py:86-92)."""
+    from ._kernel import causal_j_stops
+
+    return causal_j_stops(q_idx, k_idx, blocks)
+
+
+def qk_preprocess(q, k, v, q_keep, k_keep):
+    """Compact, pad and transpose boundary-layout inputs (qk_sparse.py:196-211)."""
+    q, k, v = as_operand(q), as_operand(k), as_operand(v)
+    if q.dim() != 4 or k.dim() != 4 or k.shape != v.shape:
+        raise ShapeError(f"operand shapes disagree: {tuple(q.shape)}, {tuple(k.shape)}, {tuple(v.shape)}")
+    B, T_Q, H, D = q.shape
+    T_KV = k.shape[1]
+    if T_KV >= KEY_PAD:
+        raise ShapeError(f"T_KV must be < {KEY_PAD}")
+    dev = q.device
+    qk_ = _keep_tensor(q_keep, (B, T_Q, H), dev)
+    kk_ = _keep_tensor(k_keep, (B, T_KV, H), dev)
+    BH = B * H
+    cnt = torch.zeros(2 * BH + 1, dtype=torch.int32, device=dev)
+    q_perm, q_rank = _compact_perm(qk_, B, T_Q, H, cnt[:BH], cnt[2 * BH:])
+    k_perm, k_rank = _compact_perm(kk_, B, T_KV, H, cnt[BH: 2 * BH], cnt[2 * BH:])
+    host = cnt.cpu()  # the one host sync: buffer sizes
+    if int(host[2 * BH]):
+        raise ShapeError("keep entries must be 0 or 1")
+    T_cq = int(host[:BH].max()) if BH else 0
+    T_ck = int(host[BH: 2 * BH].max()) if BH else 0
+    q_c = _gather(q, q_perm, T_cq)
+    k_c = _gather(k, k_perm, T_ck)
+    v_c = _gather(v, k_perm, T_ck)
+    q_aux = _aux(q_perm, cnt[:BH], B, H, T_cq, QUERY_PAD, _OOB_Q)
+    k_aux = _aux(k_perm, cnt[BH: 2 * BH], B, H, T_ck, KEY_PAD, _OOB_K)
+    problem = Problem(B, H, T_cq, T_ck, D, q_aux, k_aux)
+    return QkPrepared(
+        q_c=q_c, k_c=k_c, v_c=v_c,
+        q_idx=q_aux[:, :T_cq].view(B, H, T_cq),
+        k_idx=k_aux[:, :T_ck].view(B, H, T_ck),
+        scatter_index=q_perm[:, :T_cq].view(B, H, T_cq).transpose(1, 2),
+        T_Q=T_Q, problem=problem, q_rank=q_rank, k_rank=k_rank,
+    )
+
+
+def _problem_from(q_c, k_c, q_idx, k_idx, validate=True):
+    check_forward_operands(q_c, k_c, k_c)
+    B, H, T_Q, D = q_c.shape
+    T_KV = k_c.shape[2]
+    dev = q_c.device
+    pq = pack_index(q_idx, B * H, T_Q, _OOB_Q, dev)
+    pk = pack_index(k_idx, B * H, T_KV, _OOB_K, dev)
+    prob = Problem(B, H, T_Q, T_KV, D, pq, pk)
+    if validate and B * H:
+        prob.validate("qk")
+    return prob
+
+
+def qk_forward_kernel(q_c, k_c, v_c, q_idx, k_idx, scale=None, blocks=BlockSpec(), workers=None):
+    """Irregular-causal forward over compacted operands (qk_sparse.py:120-148)."""
+    q_c, k_c, v_c = as_operand(q_c), as_operand(k_c), as_operand(v_c)
+    check_forward_operands(q_c, k_c, v_c)
+    B, H, T_Q, _ = q_c.shape
+    if tuple(torch.as_tensor(q_idx).shape) != (B, H, T_Q) or tuple(torch.as_tensor(k_idx).shape) != (
+            B, H, k_c.shape[2]):
+        raise ShapeError("index tensors do not match the compacted operands")
+    prob = _problem_from(q_c, k_c, q_idx, k_idx)
+    return attention_forward(prob, q_c, k_c, v_c, scale, blocks)
+
+
+def qk_backward_kernel(q_c, k_c, v_c, outputs, d_out_c, q_idx, k_idx, scale=None, blocks=BlockSpec(),
+                       workers=None):
+    """Gradients w.r.t. compacted operands, fp32 (qk_sparse.py:151-183)."""
+    q_c, k_c, v_c = as_operand(q_c), as_operand(k_c), as_operand(v_c)
+    check_forward_operands(q_c, k_c, v_c)
+    if tuple(d_out_c.shape) != tuple(q_c.shape):
+        raise ShapeError(f"dO shape {tuple(d_out_c.shape)} != {tuple(q_c.shape)}")
+    prob = getattr(outputs, "_problem", None)
+    if prob is None or prob.T_q != q_c.shape[2] or prob.T_kv != k_c.shape[2]:
+        prob = _problem_from(q_c, k_c, q_idx, k_idx)
+    return attention_backward(prob, q_c, k_c, v_c, outputs, d_out_c, scale)
+
+
+def _scatter(o_kernel, rank, T_Q, out_dtype=None):
+    """(B, H, T_c, D) -> (B, T_Q, H, D); positions whose slot is >= T_c get zeros."""
+    B, H, T_c, D = o_kernel.shape
+    o_kernel = o_kernel.contiguous()
+    dt = out_dtype or o_kernel.dtype
+    out = torch.empty((B, T_Q, H, D), dtype=dt, device=o_kernel.device)
+    _lib.call("scfa_scatter_rows", _lib.ptr(o_kernel), o_kernel.element_size(), B, H, T_Q, D,
+              _lib.ptr(rank), T_c, _lib.ptr(out), out.element_size(),
+              out.stride(0), out.stride(1), out.stride(2), _lib.stream_ptr())
+    return out
+
+
+def _rank_from_index(scatter_index, T_Q):
+    idx = torch.as_tensor(scatter_index)
+    B, T_c, H = idx.shape
+    rank = torch.empty((B * H, T_Q), dtype=torch.int32, device=idx.device)
+    err = torch.zeros(1, dtype=torch.int32, device=idx.device)
+    _lib.call("scfa_invert_index", _lib.ptr(idx), _lib.dtype_code(idx), B, T_c, H,
+              idx.stride(0), idx.stride(1), idx.stride(2), T_Q, _lib.ptr(rank), _lib.ptr(err), _lib.stream_ptr())
+    return rank
+
+
+def qk_postprocess(o_kernel, scatter_index, T_Q, rank=None):
+    """Scatter kernel outputs back to (B, T, H, D); dropped rows are zero (qk_sparse.py:214-225)."""
+    o_kernel = torch.as_tensor(o_kernel)
+    if rank is None:
+        rank = _rank_from_index(scatter_index, T_Q)
+    return _scatter(o_kernel, rank, T_Q)
+
+
+def qk_sparse_attention(q, k, v, q_keep, k_keep, scale=None, blocks=BlockSpec(), workers=None):
+    """End-to-end QK-sparse attention in boundary layout (qk_sparse.py:228-239)."""
+    prep = qk_preprocess(q, k, v, q_keep, k_keep)
+    outputs = attention_forward(prep.problem, prep.q_c, prep.k_c, prep.v_c, scale, blocks)
+    return qk_postprocess(outputs.O, prep.scatter_index, prep.T_Q, rank=prep.q_rank)
+
+
+def qk_sparse_attention_fwd_bwd(q, k, v, q_keep, k_keep, d_out, scale=None):
+    """Forward + backward through the whole QK path in boundary layout.
+
+    Returns (O bf16, dQ, dK, dV fp32), all (B, T, H, D); dropped positions get
+    zero outputs and zero gradients.  The reference composes the same thing
+    from qk_preprocess -> qk_forward_kernel -> qk_backward_kernel.
+    """
+    prep = qk_preprocess(q, k, v, q_keep, k_keep)
+    B, T_Q, H, D = q.shape
+    T_KV = k.shape[1]
+    outputs = attention_forward(prep.problem, prep.q_c, prep.k_c, prep.v_c, scale)
+    d_out = as_operand(d_out)
+    # dO rows follow the queries' compaction order
+    q_perm = prep.scatter_index.transpose(1, 2).reshape(B * H, -1)
+    d_out_c = _gather(d_out, q_perm.contiguous(), prep.q_c.shape[2])
+    dq, dk, dv = attention_backward(prep.problem, prep.q_c, prep.k_c, prep.v_c, outputs, d_out_c, scale)
+    o = _scatter(outputs.O, prep.q_rank, T_Q)
+    return o, _scatter(dq, prep.q_rank, T_Q), _scatter(dk, prep.k_rank, T_KV), _scatter(dv, prep.k_rank, T_KV)
+
+
+def random_keep(B, T, H, drop_prob, seed):
+    """Keep indicators with drop probability drop_prob, same stream as qk_sparse.py:242-247 (numpy)."""
+    if not 0.0 <= drop_prob <= 1.0:
+        raise ShapeError(f"drop probability must be in [0, 1], got {drop_prob}")
+    g = stream(seed, DOMAIN_KEEP)
+    return (g.random((B, T, H)) >= drop_prob).astype(np.float64)

@@ -1,0 +1,97 @@
+"""GPU parity: the tcgen05 kernels against the NumPy oracle on identical bf16 inputs.
+
+Tolerance (north star): max-abs <= 2e-2 on outputs and gradients against the
+float64 oracle fed the same bf16-rounded inputs; gradients come back fp32.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import bf16_round, make_batch
+from oracle import scfa_oracle as orc
+
+import paper_2306_01160_b200 as scfa
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-2
+
+
+def _t(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def _np(x):
+    return x.detach().float().cpu().numpy().astype(np.float64)
+
+
+def _check(name, got, want, tol=TOL):
+    err = float(np.max(np.abs(got - want))) if want.size else 0.0
+    assert np.isfinite(got).all(), f"{name}: non-finite values"
+    assert err <= tol, f"{name}: max-abs {err:.3e} > {tol}"
+
+
+@pytest.mark.parametrize("T", [128, 200, 384])
+def test_dense_forward_backward(T):
+    B, H, D = 1, 2, 64
+    q, k, v = make_batch(B, H, T, D, seed=1)
+    dO = bf16_round(np.random.default_rng(3).standard_normal((B, H, T, D)))
+    vis = orc.visibility(np.arange(T), np.arange(T))
+    O, M, L = orc.attention(q, k, v, vis)
+    dq, dk, dv = orc.attention_grads(q, k, v, vis, dO)
+    out = scfa.flash_forward(_t(q), _t(k), _t(v))
+    _check("O", _np(out.O), O)
+    _check("M", _np(out.M), M, 1e-3)
+    np.testing.assert_allclose(_np(out.L), L, rtol=2e-2)
+    gq, gk, gv = scfa.flash_backward(_t(q), _t(k), _t(v), out, _t(dO))
+    _check("dQ", _np(gq), dq)
+    _check("dK", _np(gk), dk)
+    _check("dV", _np(gv), dv)
+    assert out.tiles_computed == scfa.dense_tile_count(T) * B * H
+
+
+@pytest.mark.parametrize("T,drop", [(256, 0.5), (1024, 0.5), (300, 0.9), (200, 0.0)])
+def test_qk_end_to_end(T, drop):
+    B, H, D = 2, 2, 64
+    qb, kb, vb = (np.swapaxes(x, 1, 2) for x in make_batch(B, H, T, D, seed=5))
+    qk = scfa.random_keep(B, T, H, drop, 11)
+    kk = scfa.random_keep(B, T, H, drop, 12)
+    dO = bf16_round(np.random.default_rng(4).standard_normal((B, T, H, D)))
+    vis = orc.visibility(np.arange(T), np.arange(T))[None, None] & (qk.transpose(0, 2, 1)[..., :, None] > 0) & (
+        kk.transpose(0, 2, 1)[..., None, :] > 0)
+    eng = lambda x: np.swapaxes(x, 1, 2)
+    O, _, _ = orc.attention(eng(qb), eng(kb), eng(vb), vis)
+    O = O * (qk.transpose(0, 2, 1)[..., None] > 0)
+    dq, dk, dv = orc.attention_grads(eng(qb), eng(kb), eng(vb), vis, eng(dO))
+    dq = dq * (qk.transpose(0, 2, 1)[..., None] > 0)
+    dk = dk * (kk.transpose(0, 2, 1)[..., None] > 0)
+    dv = dv * (kk.transpose(0, 2, 1)[..., None] > 0)
+    o = scfa.qk_sparse_attention(_t(qb), _t(kb), _t(vb), _t(qk), _t(kk))
+    _check("O", _np(o), eng(O))
+    o2, gq, gk, gv = scfa.qk_sparse_attention_fwd_bwd(_t(qb), _t(kb), _t(vb), _t(qk), _t(kk), _t(dO))
+    _check("O2", _np(o2), eng(O))
+    _check("dQ", _np(gq), eng(dq))
+    _check("dK", _np(gk), eng(dk))
+    _check("dV", _np(gv), eng(dv))
+
+
+@pytest.mark.parametrize("T,nb", [(256, 4), (1000, 16), (512, 1)])
+def test_hash_end_to_end(T, nb):
+    B, H, D = 2, 2, 64
+    qb, kb, vb = (np.swapaxes(x, 1, 2) for x in make_batch(B, H, T, D, seed=7))
+    hb = scfa.random_buckets(B, T, H, nb, 9)
+    dO = bf16_round(np.random.default_rng(5).standard_normal((B, T, H, D)))
+    eng = lambda x: np.swapaxes(x, 1, 2)
+    hh = hb.transpose(0, 2, 1)
+    pos = np.arange(T)
+    vis = orc.visibility(pos, pos, hh, hh, exclude_self=True)
+    O, _, _ = orc.attention(eng(qb), eng(kb), eng(vb), vis)
+    dq, dk, dv = orc.attention_grads(eng(qb), eng(kb), eng(vb), vis, eng(dO))
+    ht = _t(hb)
+    o = scfa.hash_sparse_attention(_t(qb), _t(kb), _t(vb), ht, ht)
+    _check("O", _np(o), eng(O))
+    o2, gq, gk, gv = scfa.hash_sparse_attention_fwd_bwd(_t(qb), _t(kb), _t(vb), ht, ht, _t(dO))
+    _check("O2", _np(o2), eng(O))
+    _check("dQ", _np(gq), eng(dq))
+    _check("dK", _np(gk), eng(dk))
+    _check("dV", _np(gv), eng(dv))
