@@ -315,8 +315,10 @@ __global__ void __launch_bounds__(192, 2)
           }
           tmem_st16(t_s + c / 2, pk);
         }
-        if (rebase && t > 0) {
-          // The previous P.V has completed: s_full of this tile was committed after it.
+        // tcgen05.ld/st are warp-collective: the whole warp rescales when any row must
+        // (alpha == 1 for the others, an exact no-op).  The previous P.V has completed:
+        // s_full of this tile was committed after it.
+        if (__any_sync(0xffffffffu, rebase && t > 0)) {
 #pragma unroll 1
           for (int c = 0; c < kD; c += 32) {
             uint32_t v[32];
@@ -337,35 +339,39 @@ __global__ void __launch_bounds__(192, 2)
         mbar_wait(bar_acc, 0);
         tc_fence_after();
       }
-      if (row < args.T_rows) {
-        const float inv_l = (l_run > 0.f) ? 1.f / l_run : 0.f;
-        __nv_bfloat16* orow = args.out_o + (static_cast<size_t>(bh) * args.T_rows + row) * kD;
+      // tcgen05.ld is warp-collective: every thread loads, only in-range rows store.
+      const bool live = row < args.T_rows;
+      const float inv_l = (l_run > 0.f) ? 1.f / l_run : 0.f;
+      __nv_bfloat16* orow = args.out_o + (static_cast<size_t>(bh) * args.T_rows + row) * kD;
 #pragma unroll
-        for (int c = 0; c < kD; c += 32) {
-          uint32_t v[32];
-          if (n_tiles > 0) {
-            tmem_ld32(tmem + lane_off + C::TM_ACC0 + c, v);
-            tmem_wait_ld();
-          } else {
+      for (int c = 0; c < kD; c += 32) {
+        uint32_t v[32];
+        if (n_tiles > 0) {
+          tmem_ld32(tmem + lane_off + C::TM_ACC0 + c, v);
+          tmem_wait_ld();
+        } else {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = 0u;
-          }
-          uint4 o4[4];
-          uint32_t* ow = reinterpret_cast<uint32_t*>(o4);
+          for (int i = 0; i < 32; ++i) v[i] = 0u;
+        }
+        uint4 o4[4];
+        uint32_t* ow = reinterpret_cast<uint32_t*>(o4);
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            ow[i] = pack_bf16(__uint_as_float(v[2 * i]) * inv_l, __uint_as_float(v[2 * i + 1]) * inv_l);
+        for (int i = 0; i < 16; ++i)
+          ow[i] = pack_bf16(__uint_as_float(v[2 * i]) * inv_l, __uint_as_float(v[2 * i + 1]) * inv_l);
+        if (live) {
           uint4* dst = reinterpret_cast<uint4*>(orow + c);
 #pragma unroll
           for (int i = 0; i < 4; ++i) dst[i] = o4[i];
         }
+      }
+      if (live) {
         const size_t so = static_cast<size_t>(bh) * args.T_rows + row;
         const float LN2 = 0.6931471805599453f;
         const bool dead = !(l_run > 0.f);
-        args.out0[so] = dead ? NEG_INF : m_true * LN2;                                  // M
-        args.out1[so] = dead ? 0.f : l_run * ex2(((m_run == NEG_INF) ? 0.f : m_run) - m_true);  // L
-        args.out_lse2[static_cast<size_t>(bh) * args.T_rows_pad + row] =
-            dead ? INFINITY : (((m_run == NEG_INF) ? 0.f : m_run) + __log2f(l_run));
+        const float m_use = (m_run == NEG_INF) ? 0.f : m_run;
+        args.out0[so] = dead ? NEG_INF : m_true * LN2;                  // M
+        args.out1[so] = dead ? 0.f : l_run * ex2(m_use - m_true);         // L relative to M
+        args.out_lse2[static_cast<size_t>(bh) * args.T_rows_pad + row] = dead ? INFINITY : (m_use + __log2f(l_run));
       }
     } else {
       // ---------------- backward passes: P and dS recomputed from (lse2, delta)
@@ -428,24 +434,25 @@ __global__ void __launch_bounds__(192, 2)
         mbar_wait(bar_acc, 0);
         tc_fence_after();
       }
-      if (row < args.T_rows) {
-        const size_t ro = (static_cast<size_t>(bh) * args.T_rows + row) * kD;
-        const int n_out = (kMode == MODE_DKDV) ? 2 : 1;
-        for (int o = 0; o < n_out; ++o) {
-          // DQ: out0 = scale * dQ.  DKDV: out0 = scale * dK (ACC1), out1 = dV (ACC0).
-          const int col = (kMode == MODE_DKDV && o == 0) ? C::TM_ACC1 : C::TM_ACC0;
-          const float mul = (o == 0) ? args.scale : 1.f;
-          float* dst = ((o == 0) ? args.out0 : args.out1) + ro;
+      const bool live = row < args.T_rows;
+      const size_t ro = (static_cast<size_t>(bh) * args.T_rows + row) * kD;
+      const int n_out = (kMode == MODE_DKDV) ? 2 : 1;
+      for (int o = 0; o < n_out; ++o) {
+        // DQ: out0 = scale * dQ.  DKDV: out0 = scale * dK (ACC1), out1 = dV (ACC0).
+        const int col = (kMode == MODE_DKDV && o == 0) ? C::TM_ACC1 : C::TM_ACC0;
+        const float mul = (o == 0) ? args.scale : 1.f;
+        float* dst = ((o == 0) ? args.out0 : args.out1) + ro;
 #pragma unroll
-          for (int c = 0; c < kD; c += 32) {
-            uint32_t v[32];
-            if (n_tiles > 0) {
-              tmem_ld32(tmem + lane_off + col + c, v);
-              tmem_wait_ld();
-            } else {
+        for (int c = 0; c < kD; c += 32) {
+          uint32_t v[32];
+          if (n_tiles > 0) {
+            tmem_ld32(tmem + lane_off + col + c, v);
+            tmem_wait_ld();
+          } else {
 #pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] = 0u;
-            }
+            for (int i = 0; i < 32; ++i) v[i] = 0u;
+          }
+          if (live) {
             float4* d4 = reinterpret_cast<float4*>(dst + c);
 #pragma unroll
             for (int i = 0; i < 8; ++i)
