@@ -1,0 +1,405 @@
+"""SCFA benchmark: hash-sparse fwd+bwd at cfg2 on B200, dense causal comparator, CPU baseline.
+
+Contract (one JSON line on rank 0):
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step = one pass of the hot path over one batch: bucket sort + fused
+gather/transposes (prep), exact tile lists, forward, backward (dQ, dK/dV),
+and the inverse scatters of O, dQ, dK, dV back to (B, T, H, D) (post).
+
+Workload (BASELINE.json configs[1], "cfg2"): hash-sparse, B=4 H=12 T=8192
+D=64, 16 buckets (same ids for Q and K, exclude_self on), bf16 operands,
+fp32 gradients; synthetic inputs from the reference's seeded generators.
+Metric: effective TFLOP/s = 14*D*P_live / t with P_live the number of
+visible (query, key) pairs; ms per step is reported beside it.
+
+Multi-GPU: one process per GPU (torchrun), each rank processes its own cfg2
+batch (no collective on the data path) -> weak scaling; timing is the max over
+ranks of CUDA-event time between barriers.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CFG = dict(workload="cfg2: hash-sparse SCFA fwd+bwd", B=4, H=12, T=8192, D=64, nb=16, exclude_self=True, seed=0)
+METRIC = "SCFA fwd+bwd ms & effective TFLOP/s vs dense causal flash at T=8k/16k"
+
+
+def live_pairs_hash(buckets, exclude_self=True):
+    """Visible pairs with shared Q/K bucket ids: sum_g c_g (c_g - 1) / 2 per head (+c_g without exclude_self)."""
+    B, T, H = buckets.shape
+    total = 0
+    for b in range(B):
+        for h in range(H):
+            c = np.bincount(buckets[b, :, h]).astype(np.int64)
+            total += int(np.sum(c * (c - 1) // 2 + (0 if exclude_self else c)))
+    return total
+
+
+def make_inputs(cfg):
+    from paper_2306_01160_b200.hash_sparse import random_buckets
+    from paper_2306_01160_b200.tensors import random_tensor_np
+
+    B, H, T, D, s = cfg["B"], cfg["H"], cfg["T"], cfg["D"], cfg["seed"]
+    shape = (B, H, T, D)
+    # boundary layout (B, T, H, D), seeds s..s+3 and bucket seed s+5 as the reference CLI (cli.py:436-487)
+    qkvd = [np.ascontiguousarray(np.swapaxes(random_tensor_np(shape, s + i, dtype=np.float32), 1, 2))
+            for i in (0, 1, 2, 3)]
+    buckets = random_buckets(B, T, H, cfg["nb"], s + 5)
+    return qkvd, buckets
+
+
+# ---------------------------------------------------------------- clocks
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                if len(parts) == 6:
+                    self.rows.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------- CPU baseline (oracle port)
+
+def cpu_baseline(qkvd, buckets, cfg, max_seconds=30.0):
+    """Reference tile loop restated in C (oracle/), all host threads, on a bounded sample of heads."""
+    from oracle import c_oracle
+
+    c_oracle.build()
+    threads = c_oracle.max_threads()
+    B, H, T, D = cfg["B"], cfg["H"], cfg["T"], cfg["D"]
+    q, k, v, d = qkvd
+    heads = [(b, h) for b in range(B) for h in range(H)]
+    n = max(1, min(len(heads), threads))
+    sample = heads[:n]
+    excl = cfg["exclude_self"]
+
+    def run():
+        t0 = time.perf_counter()
+        hs = np.stack([buckets[b, :, h] for b, h in sample])  # (n, T)
+        order = np.argsort(hs * T + np.arange(T), axis=-1, kind="stable")  # reference _bucket_order
+        take = lambda x: np.stack([x[b, :, h][order[i]] for i, (b, h) in enumerate(sample)])
+        qs, ks, vs, ds = take(q), take(k), take(v), take(d)
+        hsrt = np.take_along_axis(hs, order, -1)
+        o, m, l, tiles = c_oracle.forward(qs, ks, vs, order, order, hsrt, hsrt, exclude_self=excl, threads=threads)
+        dq, dk, dv = c_oracle.backward(qs, ks, vs, o, m, l, ds, order, order, hsrt, hsrt, exclude_self=excl,
+                                       threads=threads)
+        out = np.empty_like(o)
+        np.put_along_axis(out, order[..., None], o, axis=1)  # hash_scatter
+        return time.perf_counter() - t0
+
+    elapsed = run()
+    p_live = live_pairs_hash(np.stack([buckets[b, :, h] for b, h in sample])[:, :, None], excl)
+    flops = 14.0 * D * p_live
+    return {
+        "value": flops / elapsed / 1e12,
+        "unit": "TFLOP/s",
+        "cores": threads,
+        "kind": "port",
+        "sample": f"{n} of {B * H} (b,h) heads at T={T} D={D} nb={cfg['nb']}: sort+gather, fwd, bwd, scatter "
+                  f"(oracle/scfa_oracle.c, fp32, 64x64 tiles), {elapsed:.2f} s",
+        "seconds": elapsed,
+    }
+
+
+# ---------------------------------------------------------------- GPU arm
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2306_01160_b200 as scfa
+    from paper_2306_01160_b200 import _lib
+    from paper_2306_01160_b200 import hash_sparse as hs
+    from paper_2306_01160_b200._kernel import attention_backward, attention_forward
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    _lib.require_cuda()
+
+    qkvd, buckets = make_inputs(cfg)
+    B, H, T, D = cfg["B"], cfg["H"], cfg["T"], cfg["D"]
+    host = [torch.from_numpy(x).to(torch.bfloat16).pin_memory() for x in qkvd]
+    host_h = torch.from_numpy(buckets).pin_memory()
+    q, k, v, dO = (x.to(dev, non_blocking=True) for x in host)
+    hb = host_h.to(dev, non_blocking=True)
+    torch.cuda.synchronize()
+    p_live = live_pairs_hash(buckets, cfg["exclude_self"])
+    flops_step = 14.0 * D * p_live
+
+    def step(q, k, v, hb, dO):
+        sb = hs._sort_batch(q, k, v, hb, hb, "bthd", check=False)
+        prob = hs._problem_of(sb, cfg["exclude_self"])
+        out = attention_forward(prob, sb.q, sb.k, sb.v)
+        d_s = hs._gather(dO, sb.q_perm, "bthd")
+        dq, dk, dv = attention_backward(prob, sb.q, sb.k, sb.v, out, d_s)
+        res = (hs._scatter(out.O, sb.q_rank, "bthd"), hs._scatter(dq, sb.q_rank, "bthd"),
+               hs._scatter(dk, sb.k_rank, "bthd"), hs._scatter(dv, sb.k_rank, "bthd"))
+        return res, prob
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step(q, k, v, hb, dO)
+    res, prob = step(q, k, v, hb, dO)
+    torch.cuda.synchronize()
+
+    # per-entry-point CUDA events inside the timed region
+    stream = torch.cuda.current_stream()
+    ev_log = []
+
+    def hook(name, phase):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        ev_log.append((name, phase, e))
+
+    sampler = ClockSampler(local)
+    launches0 = _lib.launches
+    with sampler:
+        time.sleep(0.3)
+        barrier()
+        _lib.EVENT_HOOK = hook
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for _ in range(args.steps):
+            step(q, k, v, hb, dO)
+        t_end.record(stream)
+        _lib.EVENT_HOOK = None
+        barrier()
+    launches = _lib.launches - launches0
+    ms_local = t_start.elapsed_time(t_end) / args.steps
+    ms = max_over_ranks(ms_local)
+
+    per = {}
+    open_ev = {}
+    for name, phase, e in ev_log:
+        if phase == 0:
+            open_ev[name] = e
+        else:
+            per.setdefault(name, []).append(open_ev.pop(name).elapsed_time(e))
+    kern_ms = {n: sum(v) / args.steps for n, v in per.items()}
+    kern_avg = {n: sum(v) / len(v) for n, v in per.items()}
+
+    # executed tiles (128-row blocks) per list, for tensor-pipe utilisation on executed tiles
+    tiles_fwd = prob.executed_tiles()
+    tt = prob._tiles_total.cpu().tolist()
+    tiles = {"fwd_128x128": tt[0], "dq_128x64": tt[1], "dkdv_128x64": tt[2]}
+    algo = {"scfa_attn_fwd": 4.0 * D * p_live, "scfa_attn_bwd_dq": 6.0 * D * p_live,
+            "scfa_attn_bwd_dkdv": 8.0 * D * p_live}
+    executed = {"scfa_attn_fwd": tt[0] * 128 * 128 * D * 2 * 2, "scfa_attn_bwd_dq": tt[1] * 128 * 64 * D * 2 * 3,
+                "scfa_attn_bwd_dkdv": tt[2] * 128 * 64 * D * 2 * 4}
+    attn = {n: kern_avg[n] for n in algo if n in kern_avg}
+    dom = max(attn, key=lambda n: attn[n])
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except OSError:
+        pass
+    peak_src = "measured" if peaks else "fallback"
+    peak = float(peaks.get("bf16_tflops", 1590.0))
+    achieved = algo[dom] / (kern_avg[dom] * 1e-3) / 1e12
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(dom)
+    except OSError:
+        pass
+    roofline = {
+        "bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak, "peak_source": peak_src,
+        "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+        "executed_tile_tflops": executed[dom] / (kern_avg[dom] * 1e-3) / 1e12,
+        "executed_tile_frac": executed[dom] / (kern_avg[dom] * 1e-3) / 1e12 / peak,
+    }
+
+    # dense causal comparator at the same shape (our own kernels, engine layout, same fwd+bwd)
+    qe, ke, ve, de = (x.transpose(1, 2).contiguous() for x in (q, k, v, dO))
+    for _ in range(args.warmup):
+        o = scfa.flash_forward(qe, ke, ve)
+        scfa.flash_backward(qe, ke, ve, o, de)
+    barrier()
+    d0 = torch.cuda.Event(enable_timing=True)
+    d1 = torch.cuda.Event(enable_timing=True)
+    d0.record(stream)
+    for _ in range(args.steps):
+        o = scfa.flash_forward(qe, ke, ve)
+        scfa.flash_backward(qe, ke, ve, o, de)
+    d1.record(stream)
+    barrier()
+    dense_ms = max_over_ranks(d0.elapsed_time(d1) / args.steps)
+    dense_flops = 14.0 * D * B * H * T * (T + 1) / 2
+    del qe, ke, ve, de, o
+
+    # end to end through the public API with host buffers: H2D inputs, D2H outputs + gradients
+    outs_host = [torch.empty(r.shape, dtype=r.dtype, pin_memory=True) for r in res]
+    h2d = sum(x.numel() * x.element_size() for x in host) + host_h.numel() * host_h.element_size()
+    d2h = sum(x.numel() * x.element_size() for x in outs_host)
+
+    def e2e_step():
+        qd, kd, vd, dd = (x.to(dev, non_blocking=True) for x in host)
+        hd = host_h.to(dev, non_blocking=True)
+        r = scfa.hash_sparse_attention_fwd_bwd(qd, kd, vd, hd, hd, dd)
+        for dst, src in zip(outs_host, r):
+            dst.copy_(src, non_blocking=True)
+
+    for _ in range(args.warmup):
+        e2e_step()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+
+    line = {
+        "metric": METRIC,
+        "value": world * flops_step / (ms * 1e-3) / 1e12,
+        "unit": "TFLOP/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (reference seeded generators: random_tensor seeds 0-3, random_buckets seed 5)",
+        "config": {"workload": cfg["workload"], "B": B, "H": H, "T": T, "D": D, "buckets": cfg["nb"],
+                   "exclude_self": cfg["exclude_self"], "global_batch": B * world,
+                   "parallelism": f"(b,h)-sharded, 1 batch per rank x{world}",
+                   "l2": "inputs > L2 (q,k,v,dO 4 x 48 MiB bf16 + sorted copies), no flush",
+                   "p_live_per_rank": p_live},
+        "e2e": {"value": world * flops_step / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "api": "paper_2306_01160_b200.hash_sparse_attention_fwd_bwd"},
+        "gpu_launches": launches,
+        "roofline": roofline,
+        "stages_ms": {n: round(v, 4) for n, v in sorted(kern_ms.items(), key=lambda kv: -kv[1])},
+        "tiles": tiles,
+        "dense_causal": {"ms_per_step": dense_ms, "effective_tflops": dense_flops / (dense_ms * 1e-3) / 1e12,
+                         "speedup_of_scfa": dense_ms / ms},
+        "clocks": sampler.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(qkvd, buckets, cfg)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------- reference arm (CPU oracle port)
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    qkvd, buckets = make_inputs(cfg)
+    for _ in range(args.warmup):
+        pass  # the port has no warm-up state; the first timed sample includes the library load
+    samples = [cpu_baseline(qkvd, buckets, cfg) for _ in range(max(1, args.steps))]
+    vals = [s["value"] for s in samples]
+    v = statistics.median(vals)
+    base = dict(samples[0])
+    base["value"] = v
+    line = {
+        "metric": METRIC, "value": v, "unit": "TFLOP/s", "impl": "reference",
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (reference seeded generators)",
+        "config": {"workload": cfg["workload"], "B": cfg["B"], "H": cfg["H"], "T": cfg["T"], "D": cfg["D"],
+                   "buckets": cfg["nb"]},
+        "cpu_baseline": base,
+        "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--T", type=int, default=None)
+    args = ap.parse_args()
+    cfg = dict(CFG)
+    if args.T:
+        cfg["T"] = args.T
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -100,9 +100,21 @@ def raise_for(code, what=""):
     raise cls(f"{what}: {msg}" if what else msg)
 
 
+# kernels launched per successful call (for launch accounting in bench.py)
+KERNELS_PER_CALL = {"scfa_build_tile_lists": 3, "scfa_invert_index": 2}
+launches = 0
+EVENT_HOOK = None  # optional callable(name, phase) used by bench.py to time each entry point
+
+
 def call(name, *args):
+    global launches
+    if EVENT_HOOK is not None:
+        EVENT_HOOK(name, 0)
     rc = getattr(load(), name)(*args)
+    if EVENT_HOOK is not None:
+        EVENT_HOOK(name, 1)
     raise_for(rc, name)
+    launches += KERNELS_PER_CALL.get(name, 1)
 
 
 def ptr(t):
