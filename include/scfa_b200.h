@@ -141,12 +141,14 @@ int scfa_validate_sorted(const int32_t* idx, const int32_t* hash, int64_t BH, in
  * rows_are_queries = 1: stationary side = queries (fwd, dQ); 0: keys (dK/dV).
  * Block sizes: row_block 128; col_block 128 (fwd) or 64 (bwd).
  * list (B*H, n_row_blocks, list_stride) uint16 with list_stride >= n_col_blocks;
- * list_count (B*H, n_row_blocks) int32; tiles_total (1 int64, accumulated).  */
+ * list_count (B*H, n_row_blocks) int32; tiles_total (1 int64, accumulated, may be NULL).
+ * workspace: >= 16 * B*H * (n_row_blocks + n_col_blocks) bytes, 16-byte aligned.  */
 int scfa_build_tile_lists(const int32_t* q_idx, const int32_t* q_hash, const int32_t* k_idx,
                           const int32_t* k_hash, int64_t BH, int64_t T_q, int64_t T_kv,
                           int64_t Tq_pad, int64_t Tkv_pad, int rows_are_queries, int row_block,
                           int col_block, int flags, uint16_t* list, int32_t* list_count,
-                          int64_t list_stride, unsigned long long* tiles_total, void* stream);
+                          int64_t list_stride, unsigned long long* tiles_total, void* workspace,
+                          int64_t workspace_bytes, void* stream);
 
 /* Reference schedule at arbitrary BlockSpec(B_m, B_n) (tensors.py:63-78):
  * j_start/j_stop per query block exactly as causal_j_stops (flags without

@@ -105,12 +105,13 @@ class Problem:
         slot = {(True, 128): 0, (True, 64): 1, (False, 64): 2}.get(key, None)
         total_ptr = None if slot is None else ctypes.c_void_p(self._tiles_total.data_ptr() + 8 * slot)
         qh, kh = self._hash_ptrs()
+        ws = torch.empty((self.BH * (max(n_rb, 1) + stride) * 16,), dtype=torch.uint8, device=dev)
         _lib.call(
             "scfa_build_tile_lists",
             _lib.ptr(self.q_idx), qh, _lib.ptr(self.k_idx), kh,
             self.BH, self.T_q, self.T_kv, self.Tq_pad, self.Tkv_pad,
             1 if rows_are_queries else 0, 128, int(col_block), self.flags,
-            _lib.ptr(lst), _lib.ptr(cnt), stride, total_ptr, _lib.stream_ptr(),
+            _lib.ptr(lst), _lib.ptr(cnt), stride, total_ptr, _lib.ptr(ws), ws.numel(), _lib.stream_ptr(),
         )
         self._lists[key] = (lst, cnt, stride)
         return self._lists[key]

@@ -49,7 +49,7 @@ _SIGS = {
     "scfa_pack_index": [_P, _I, _L, _L, _L, _L, _L, ctypes.c_int32, _P, _P],
     "scfa_validate_qk": [_P, _P, _L, _L, _L, _L, _L, _P, _P],
     "scfa_validate_sorted": [_P, _P, _L, _L, _L, _P, _P],
-    "scfa_build_tile_lists": [_P, _P, _P, _P, _L, _L, _L, _L, _L, _I, _I, _I, _I, _P, _P, _L, _P, _P],
+    "scfa_build_tile_lists": [_P, _P, _P, _P, _L, _L, _L, _L, _L, _I, _I, _I, _I, _P, _P, _L, _P, _P, _L, _P],
     "scfa_ref_schedule": [_P, _P, _P, _P, _L, _L, _L, _L, _L, _L, _L, _I, _P, _P, _P, _P],
     "scfa_attn_fwd": [_P, _P, _P, _L, _L, _L, _L, _P, _P, _P, _P, _L, _L, _P, _P, _L, _F, _I, _P, _P, _P,
                       _P, _P],

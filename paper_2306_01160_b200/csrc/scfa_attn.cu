@@ -85,9 +85,74 @@ struct AttnArgs {
   int use_hash;
 };
 
-SCFA_DEVICE bool visible(int qi, int ki, int qh, int kh, int excl, int use_hash) {
-  bool ok = excl ? (qi > ki) : (qi >= ki);
-  return ok && (!use_hash || qh == kh);
+// ---- per-row visibility interval -------------------------------------------------
+// Inside one tile the streamed columns are sorted by (bucket, position) (hash) or by
+// position (QK / dense), with pads and out-of-range slots at the tail.  The columns a
+// stationary row can see therefore form ONE contiguous run [lo, hi): the row's bucket
+// run, cut at the causal boundary.  It is found with a few binary searches in shared
+// memory per row and tile, and applied as a 32-bit mask per 32 columns (R2P + FSEL).
+
+// first i in [0, n) with a[i] >= x  (a ascending on [0, n))
+SCFA_DEVICE int lower_bound(const int* a, int n, int x) {
+  int lo = 0;
+  while (n > 0) {
+    const int h = n >> 1;
+    if (a[lo + h] < x) { lo += h + 1; n -= h + 1; } else { n = h; }
+  }
+  return lo;
+}
+// first i in [0, n) with a[i] > x
+SCFA_DEVICE int upper_bound(const int* a, int n, int x) {
+  int lo = 0;
+  while (n > 0) {
+    const int h = n >> 1;
+    if (a[lo + h] <= x) { lo += h + 1; n -= h + 1; } else { n = h; }
+  }
+  return lo;
+}
+
+// rows are queries (fwd, dQ): columns are keys.  visible <=> k_idx <(=) q_idx [and same bucket]
+template <int BN>
+SCFA_DEVICE void interval_q_rows(const int* kidx, const int* khash, int nv, int qi, int qh, bool excl, bool use_hash,
+                                 int& lo, int& hi) {
+  if (!use_hash) {  // keys ascending over all BN slots (pads 10^9, out-of-range INT_MAX)
+    lo = 0;
+    hi = excl ? lower_bound(kidx, BN, qi) : upper_bound(kidx, BN, qi);
+  } else {          // valid slots [0, nv) sorted by (bucket, position)
+    const int a = lower_bound(khash, nv, qh);
+    const int e = a + upper_bound(khash + a, nv - a, qh);
+    lo = a;
+    hi = a + (excl ? lower_bound(kidx + a, e - a, qi) : upper_bound(kidx + a, e - a, qi));
+  }
+}
+
+// rows are keys (dK/dV): columns are queries.  visible <=> q_idx >(=) k_idx [and same bucket]
+template <int BN>
+SCFA_DEVICE void interval_k_rows(const int* qidx, const int* qhash, int nv, int ki, int kh, bool excl, bool use_hash,
+                                 int& lo, int& hi) {
+  if (!use_hash) {  // real queries ascending, then pads / out-of-range (-1) at the tail
+    int nreal = 0, n = BN;
+    while (n > 0) {
+      const int h = n >> 1;
+      if (qidx[nreal + h] >= 0) { nreal += h + 1; n -= h + 1; } else { n = h; }
+    }
+    lo = excl ? upper_bound(qidx, nreal, ki) : lower_bound(qidx, nreal, ki);
+    hi = nreal;
+  } else {
+    const int a = lower_bound(qhash, nv, kh);
+    const int e = a + upper_bound(qhash + a, nv - a, kh);
+    lo = a + (excl ? upper_bound(qidx + a, e - a, ki) : lower_bound(qidx + a, e - a, ki));
+    hi = e;
+  }
+}
+
+SCFA_DEVICE uint32_t bits_below(int n) { return n <= 0 ? 0u : (n >= 32 ? 0xffffffffu : ((1u << n) - 1u)); }
+
+// 32-column visibility words of the run [lo, hi)
+template <int NW>
+SCFA_DEVICE void run_mask(int lo, int hi, uint32_t (&w)[NW]) {
+#pragma unroll
+  for (int i = 0; i < NW; ++i) w[i] = bits_below(hi - 32 * i) & ~bits_below(lo - 32 * i);
 }
 
 template <int kMode, int kD>
@@ -260,36 +325,38 @@ __global__ void __launch_bounds__(192, 2)
         const int st = t % C::NS;
         const int* kidx = reinterpret_cast<const int*>(smem + C::OFF_STAGE + st * C::STAGE_BYTES + 2 * C::Y_BYTES);
         const int* khash = kidx + C::BN;
+        constexpr int NW = C::BN / 32;
+        uint32_t vis[NW];
+        // The stage's index vectors landed with its K/V tiles (y_full precedes s_full),
+        // but s_full is what this thread waits on; compute the run after that wait.
         mbar_wait(bar_s_full, t & 1);
         tc_fence_after();
+        uint32_t raw[C::BN];
+#pragma unroll
+        for (int c = 0; c < C::BN; c += 32) tmem_ld32(t_s + c, *reinterpret_cast<uint32_t(*)[32]>(&raw[c]));
+        if (full) {
+#pragma unroll
+          for (int i = 0; i < NW; ++i) vis[i] = 0xffffffffu;
+        } else {
+          const int nv = min(C::BN, args.T_cols - (entry & 0x7fff) * C::BN);
+          int lo, hi;
+          interval_q_rows<C::BN>(kidx, khash, nv, my_idx, my_hash, excl, use_hash, lo, hi);
+          run_mask<NW>(lo, hi, vis);
+        }
+        tmem_wait_ld();
         float s[C::BN];
 #pragma unroll
-        for (int c = 0; c < C::BN; c += 32) {
-          uint32_t v[32];
-          tmem_ld32(t_s + c, v);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) s[c + i] = __uint_as_float(v[i]);
-        }
-        if (!full) {
-#pragma unroll
-          for (int c = 0; c < C::BN; c += 4) {
-            const int4 ki = *reinterpret_cast<const int4*>(kidx + c);
-            const int4 kh = *reinterpret_cast<const int4*>(khash + c);
-            if (!visible(my_idx, ki.x, my_hash, kh.x, excl, use_hash)) s[c + 0] = mask_val;
-            if (!visible(my_idx, ki.y, my_hash, kh.y, excl, use_hash)) s[c + 1] = mask_val;
-            if (!visible(my_idx, ki.z, my_hash, kh.z, excl, use_hash)) s[c + 2] = mask_val;
-            if (!visible(my_idx, ki.w, my_hash, kh.w, excl, use_hash)) s[c + 3] = mask_val;
-          }
-        }
-        float mx = s[0];
+        for (int c = 0; c < C::BN; ++c) s[c] = ((vis[c >> 5] >> (c & 31)) & 1u) ? __uint_as_float(raw[c]) : mask_val;
+        float mq[4] = {mask_val, mask_val, mask_val, mask_val};
         if (sl >= 0.f) {
 #pragma unroll
-          for (int c = 1; c < C::BN; ++c) mx = fmaxf(mx, s[c]);
+          for (int c = 0; c < C::BN; ++c) mq[c & 3] = fmaxf(mq[c & 3], s[c]);
         } else {
 #pragma unroll
-          for (int c = 1; c < C::BN; ++c) mx = fminf(mx, s[c]);
+          for (int c = 0; c < C::BN; ++c) mq[c & 3] = fminf(mq[c & 3], s[c]);
         }
+        const float mx = (sl >= 0.f) ? fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]))
+                                     : fminf(fminf(mq[0], mq[1]), fminf(mq[2], mq[3]));
         const float m_tile = mx * sl;  // -inf when the whole row is masked in this tile
         m_true = fmaxf(m_true, m_tile);
         // Rebase to a new max (log2 units) only when the max grows by >= 2^8: P stays
@@ -302,7 +369,7 @@ __global__ void __launch_bounds__(192, 2)
           m_run = m_tile;
         }
         const float m_use = (m_run == NEG_INF) ? 0.f : m_run;
-        float lsum = 0.f;
+        float ls[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int c = 0; c < C::BN; c += 32) {
           uint32_t pk[16];
@@ -310,11 +377,13 @@ __global__ void __launch_bounds__(192, 2)
           for (int i = 0; i < 16; ++i) {
             const float p0 = ex2(fmaf(s[c + 2 * i], sl, -m_use));
             const float p1 = ex2(fmaf(s[c + 2 * i + 1], sl, -m_use));
-            lsum += p0 + p1;
+            ls[(2 * i) & 3] += p0;
+            ls[(2 * i + 1) & 3] += p1;
             pk[i] = pack_bf16(p0, p1);
           }
           tmem_st16(t_s + c / 2, pk);
         }
+        const float lsum = (ls[0] + ls[1]) + (ls[2] + ls[3]);
         // tcgen05.ld/st are warp-collective: the whole warp rescales when any row must
         // (alpha == 1 for the others, an exact no-op).  The previous P.V has completed:
         // s_full of this tile was committed after it.
@@ -388,36 +457,54 @@ __global__ void __launch_bounds__(192, 2)
         const int* chash = cidx + C::BN;
         const float* clse = reinterpret_cast<const float*>(chash + C::BN);
         const float* cdelta = clse + C::BN;
+        constexpr int NW = C::BN / 32;
+        uint32_t vis[NW];
         mbar_wait(bar_s_full, t & 1);
         tc_fence_after();
+        if (full) {
+#pragma unroll
+          for (int i = 0; i < NW; ++i) vis[i] = 0xffffffffu;
+        } else {
+          const int nv = min(C::BN, args.T_cols - (entry & 0x7fff) * C::BN);
+          int lo, hi;
+          if (kMode == MODE_DQ)
+            interval_q_rows<C::BN>(cidx, chash, nv, my_idx, my_hash, excl, use_hash, lo, hi);
+          else
+            interval_k_rows<C::BN>(cidx, chash, nv, my_idx, my_hash, excl, use_hash, lo, hi);
+          run_mask<NW>(lo, hi, vis);
+        }
 #pragma unroll
         for (int c = 0; c < C::BN; c += 32) {
           uint32_t sv[32], dv[32];
           tmem_ld32(t_s + c, sv);
           tmem_ld32(t_dp + c, dv);
           tmem_wait_ld();
+          const uint32_t w = vis[c >> 5];
           uint32_t pk_p[16], pk_ds[16];
 #pragma unroll
-          for (int i = 0; i < 32; i += 2) {
-            float pp[2], dd[2];
+          for (int i = 0; i < 32; i += 4) {
+            float lse4[4], del4[4];
+            if (kMode == MODE_DQ) {
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int cc = c + i + e;
-              float p, ds;
-              if (kMode == MODE_DQ) {
-                p = ex2(fmaf(__uint_as_float(sv[i + e]), sl, -my_lse));
-                if (!full && !visible(my_idx, cidx[cc], my_hash, chash[cc], excl, use_hash)) p = 0.f;
-                ds = p * (__uint_as_float(dv[i + e]) - my_delta);
-              } else {
-                p = ex2(fmaf(__uint_as_float(sv[i + e]), sl, -clse[cc]));
-                if (!full && !visible(cidx[cc], my_idx, chash[cc], my_hash, excl, use_hash)) p = 0.f;
-                ds = p * (__uint_as_float(dv[i + e]) - cdelta[cc]);
-              }
+              for (int e = 0; e < 4; ++e) { lse4[e] = my_lse; del4[e] = my_delta; }
+            } else {
+              const float4 a = *reinterpret_cast<const float4*>(clse + c + i);
+              const float4 b = *reinterpret_cast<const float4*>(cdelta + c + i);
+              lse4[0] = a.x; lse4[1] = a.y; lse4[2] = a.z; lse4[3] = a.w;
+              del4[0] = b.x; del4[1] = b.y; del4[2] = b.z; del4[3] = b.w;
+            }
+            float pp[4], dd[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              float p = ex2(fmaf(__uint_as_float(sv[i + e]), sl, -lse4[e]));
+              p = ((w >> (i + e)) & 1u) ? p : 0.f;
               pp[e] = p;
-              dd[e] = ds;
+              dd[e] = p * (__uint_as_float(dv[i + e]) - del4[e]);
             }
             pk_p[i / 2] = pack_bf16(pp[0], pp[1]);
+            pk_p[i / 2 + 1] = pack_bf16(pp[2], pp[3]);
             pk_ds[i / 2] = pack_bf16(dd[0], dd[1]);
+            pk_ds[i / 2 + 1] = pack_bf16(dd[2], dd[3]);
           }
           if (kMode == MODE_DQ) {
             tmem_st16(t_s + c / 2, pk_ds);

@@ -232,7 +232,8 @@ extern "C" int scfa_build_tile_lists(const int32_t* q_idx, const int32_t* q_hash
                                      const int32_t* k_hash, int64_t BH, int64_t T_q, int64_t T_kv, int64_t Tq_pad,
                                      int64_t Tkv_pad, int rows_are_queries, int row_block, int col_block, int flags,
                                      uint16_t* list, int32_t* list_count, int64_t list_stride,
-                                     unsigned long long* tiles_total, void* stream) {
+                                     unsigned long long* tiles_total, void* workspace, int64_t workspace_bytes,
+                                     void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool rq = rows_are_queries != 0;
   const int64_t T_rows = rq ? T_q : T_kv, T_cols = rq ? T_kv : T_q;
@@ -249,12 +250,12 @@ extern "C" int scfa_build_tile_lists(const int32_t* q_idx, const int32_t* q_hash
   }
   if (BH == 0 || n_rb == 0) return SCFA_OK;
   const bool use_hash = (flags & SCFA_FLAG_HASH) != 0;
-  Summary* sums = nullptr;
-  const size_t bytes = static_cast<size_t>(BH) * (n_rb + n_cb) * sizeof(Summary);
-  if (cudaMallocAsync(reinterpret_cast<void**>(&sums), bytes, s) != cudaSuccess) {
-    set_error("tile list: workspace allocation failed");
-    return SCFA_ERR_CUDA;
+  const int64_t bytes = BH * (n_rb + n_cb) * static_cast<int64_t>(sizeof(Summary));
+  if (workspace == nullptr || workspace_bytes < bytes || (reinterpret_cast<uintptr_t>(workspace) & 15)) {
+    set_error("tile list: workspace must be >= %lld bytes, 16-byte aligned", static_cast<long long>(bytes));
+    return SCFA_ERR_SHAPE;
   }
+  Summary* sums = static_cast<Summary*>(workspace);
   Summary* rsum = sums;
   Summary* csum = sums + BH * n_rb;
   const int32_t* ri = rq ? q_idx : k_idx;
@@ -276,7 +277,6 @@ extern "C" int scfa_build_tile_lists(const int32_t* q_idx, const int32_t* q_hash
                                         T_kv, Tq_pad, Tkv_pad, rows_are_queries, row_block, col_block, flags, rsum,
                                         csum, static_cast<int>(n_rb), static_cast<int>(n_cb), list, list_count,
                                         list_stride, tiles_total);
-  cudaFreeAsync(sums, s);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error("tile list: %s", cudaGetErrorString(e));
