@@ -181,12 +181,9 @@ def run_ours(args, cfg):
     def step(q, k, v, hb, dO):
         sb = hs._sort_batch(q, k, v, hb, hb, "bthd", check=False)
         prob = hs._problem_of(sb, cfg["exclude_self"])
-        out = attention_forward(prob, sb.q, sb.k, sb.v)
-        d_s = hs._gather(dO, sb.q_perm, "bthd")
-        dq, dk, dv = attention_backward(prob, sb.q, sb.k, sb.v, out, d_s)
-        res = (hs._scatter(out.O, sb.q_rank, "bthd"), hs._scatter(dq, sb.q_rank, "bthd"),
-               hs._scatter(dk, sb.k_rank, "bthd"), hs._scatter(dv, sb.k_rank, "bthd"))
-        return res, prob
+        out = attention_forward(prob, sb.q, sb.k, sb.v, boundary=(T, False))
+        dq, dk, dv = attention_backward(prob, sb.q, sb.k, sb.v, out, dO, boundary=(T, T, False))
+        return (out.O, dq, dk, dv), prob
 
     def barrier():
         if world > 1:

@@ -167,38 +167,50 @@ int scfa_ref_schedule(const int32_t* q_idx, const int32_t* q_hash, const int32_t
  * o (B*H, T_q, D) bf16 (normalised output), m/l (B*H, T_q) f32 = FlashOutputs.M/L
  * (M = -inf, L = 0 for stranded rows), lse2 (B*H, Tq_pad) f32 log2-domain
  * logsumexp (+inf for stranded rows) consumed by the backward.
- * list/list_count: from scfa_build_tile_lists(rows_are_queries=1, 128, 128).  */
+ * list/list_count: from scfa_build_tile_lists(rows_are_queries=1, 128, 128).
+ * Output layout: out_boundary = 0 writes o as (B*H, T_q, D); out_boundary = 1 writes
+ * row s of slice (b, h) to o[b, q_idx[bh, s], h, :] of a (B, T_out, H, D) tensor (H
+ * heads) — the inverse scatter of qk_postprocess / hash_scatter fused into the
+ * epilogue; pad rows (q_idx outside [0, T_out)) are not written.                  */
 int scfa_attn_fwd(const void* q, const void* k, const void* v, int64_t BH, int64_t T_q,
                   int64_t T_kv, int64_t D, const int32_t* q_idx, const int32_t* q_hash,
                   const int32_t* k_idx, const int32_t* k_hash, int64_t Tq_pad, int64_t Tkv_pad,
                   const uint16_t* list, const int32_t* list_count, int64_t list_stride,
-                  float scale, int flags, void* o, float* m, float* l, float* lse2, void* stream);
+                  float scale, int flags, int64_t H, int64_t T_out, int out_boundary, void* o,
+                  float* m, float* l, float* lse2, void* stream);
 
 /* delta = rowsum(dO * O) (qk_sparse.py:168, hash_sparse.py:194, dense.py:81);
  * lse2 rebuilt from (M, L) when lse2_in is NULL (m_hat/inv_l, _kernel.py:152-154).
- * delta, lse2_out: (B*H, Tq_pad) f32 (pads: delta 0, lse2 +inf).              */
+ * delta, lse2_out: (B*H, Tq_pad) f32 (pads: delta 0, lse2 +inf).
+ * q_idx == NULL: o, d_out are (B*H, T_q, D).  q_idx != NULL (boundary mode): o, d_out
+ * are (B, T_out, H, D) and row s of slice bh is read at position q_idx[bh, s]; the dO
+ * rows are also written in kernel order to d_out_sorted (B*H, T_q, D) bf16 (pad rows 0). */
 int scfa_bwd_prep(const void* o, const void* d_out, const float* lse2_in, const float* m,
-                  const float* l, int64_t BH, int64_t T_q, int64_t D, int64_t Tq_pad, float scale,
-                  float* delta, float* lse2_out, void* stream);
+                  const float* l, int64_t BH, int64_t T_q, int64_t D, int64_t Tq_pad,
+                  const int32_t* q_idx, int64_t H, int64_t T_out, void* d_out_sorted, float* delta,
+                  float* lse2_out, void* stream);
 
 /* Backward pass 1 (dQ, query-block owner, _kernel.py:173-179).
- * list: scfa_build_tile_lists(rows_are_queries=1, 128, 64).  dq (B*H,T_q,D) f32. */
+ * list: scfa_build_tile_lists(rows_are_queries=1, 128, 64).  dq (B*H,T_q,D) f32,
+ * or (B, T_out, H, D) scattered by q_idx when out_boundary (as scfa_attn_fwd).      */
 int scfa_attn_bwd_dq(const void* q, const void* k, const void* v, const void* d_out, int64_t BH,
                      int64_t T_q, int64_t T_kv, int64_t D, const int32_t* q_idx,
                      const int32_t* q_hash, const int32_t* k_idx, const int32_t* k_hash,
                      int64_t Tq_pad, int64_t Tkv_pad, const float* lse2, const float* delta,
                      const uint16_t* list, const int32_t* list_count, int64_t list_stride,
-                     float scale, int flags, float* dq, void* stream);
+                     float scale, int flags, int64_t H, int64_t T_out, int out_boundary,
+                     float* dq, void* stream);
 
 /* Backward pass 2 (dK/dV, key-block owner over the transposed schedule,
  * _kernel.py:181-192).  list: scfa_build_tile_lists(rows_are_queries=0, 128, 64).
- * dk, dv (B*H, T_kv, D) f32.                                                    */
+ * dk, dv (B*H, T_kv, D) f32, or (B, T_out, H, D) scattered by k_idx when out_boundary. */
 int scfa_attn_bwd_dkdv(const void* q, const void* k, const void* v, const void* d_out, int64_t BH,
                        int64_t T_q, int64_t T_kv, int64_t D, const int32_t* q_idx,
                        const int32_t* q_hash, const int32_t* k_idx, const int32_t* k_hash,
                        int64_t Tq_pad, int64_t Tkv_pad, const float* lse2, const float* delta,
                        const uint16_t* list, const int32_t* list_count, int64_t list_stride,
-                       float scale, int flags, float* dk, float* dv, void* stream);
+                       float scale, int flags, int64_t H, int64_t T_out, int out_boundary,
+                       float* dk, float* dv, void* stream);
 
 #ifdef __cplusplus
 }

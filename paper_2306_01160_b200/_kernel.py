@@ -194,12 +194,28 @@ def _scale(scale, D):
     return float(default_scale(D) if scale is None else scale)
 
 
-def attention_forward(problem, q, k, v, scale=None, blocks=None):
-    """Launch the forward kernel over the exact tile list; returns FlashOutputs."""
+def _zeros_or_empty(shape, dtype, dev, zero):
+    return torch.zeros(shape, dtype=dtype, device=dev) if zero else torch.empty(shape, dtype=dtype, device=dev)
+
+
+def attention_forward(problem, q, k, v, scale=None, blocks=None, boundary=None):
+    """Launch the forward kernel over the exact tile list; returns FlashOutputs.
+
+    boundary=None: O is engine layout (B, H, T_q, D) in kernel (sorted/compacted) order.
+    boundary=(T_out, zero_fill): the epilogue writes each row straight to its original
+    position of a (B, T_out, H, D) tensor (fused inverse scatter); positions no row maps
+    to are zero-filled first when zero_fill (QK drops).  M, L stay in kernel order.
+    """
     B, H, T_q, D = q.shape
     T_kv = k.shape[2]
     dev = q.device
-    O = torch.empty((B, H, T_q, D), dtype=torch.bfloat16, device=dev)
+    if boundary is None:
+        O = torch.empty((B, H, T_q, D), dtype=torch.bfloat16, device=dev)
+        T_out, out_b = T_q, 0
+    else:
+        T_out, zero = boundary
+        O = _zeros_or_empty((B, T_out, H, D), torch.bfloat16, dev, zero)
+        out_b = 1
     M = torch.empty((B, H, T_q), dtype=torch.float32, device=dev)
     L = torch.empty((B, H, T_q), dtype=torch.float32, device=dev)
     lse2 = torch.empty((B * H, pad128(T_q)), dtype=torch.float32, device=dev)
@@ -211,28 +227,47 @@ def attention_forward(problem, q, k, v, scale=None, blocks=None):
             _lib.ptr(q), _lib.ptr(k), _lib.ptr(v), B * H, T_q, T_kv, D,
             _lib.ptr(problem.q_idx), qh, _lib.ptr(problem.k_idx), kh,
             problem.Tq_pad, problem.Tkv_pad, _lib.ptr(lst), _lib.ptr(cnt), stride,
-            _scale(scale, D), problem.flags,
+            _scale(scale, D), problem.flags, H, T_out, out_b,
             _lib.ptr(O), _lib.ptr(M), _lib.ptr(L), _lib.ptr(lse2), _lib.stream_ptr(),
         )
-    return FlashOutputs(O, M, L, problem=problem, blocks=blocks, lse2=lse2)
+    out = FlashOutputs(O, M, L, problem=problem, blocks=blocks, lse2=lse2)
+    out._boundary = boundary
+    return out
 
 
-def attention_backward(problem, q, k, v, outputs, d_out, scale=None):
-    """dQ, dK, dV (fp32, engine layout) recomputing P from the saved statistics."""
+def attention_backward(problem, q, k, v, outputs, d_out, scale=None, boundary=None):
+    """dQ, dK, dV (fp32) recomputing P from the saved statistics.
+
+    boundary=None: d_out and outputs.O are engine layout in kernel order and the
+    gradients come back the same way.  boundary=(T_q_out, T_kv_out, zero_fill):
+    outputs.O and d_out are (B, T_q_out, H, D); dO is gathered into kernel order
+    inside the delta pass, and dQ / dK / dV are written straight to their original
+    positions of (B, T_*_out, H, D) fp32 tensors.
+    """
     B, H, T_q, D = q.shape
     T_kv = k.shape[2]
     dev = q.device
-    if d_out.shape != q.shape:
-        raise ShapeError(f"dO shape {tuple(d_out.shape)} != {tuple(q.shape)}")
-    d_out = as_operand(d_out, dev)
-    O = as_operand(outputs.O, dev)
-    dq = torch.empty((B, H, T_q, D), dtype=torch.float32, device=dev)
-    dk = torch.empty((B, H, T_kv, D), dtype=torch.float32, device=dev)
-    dv = torch.empty((B, H, T_kv, D), dtype=torch.float32, device=dev)
     BH = B * H
+    Tq_pad = pad128(T_q)
+    O = as_operand(outputs.O, dev)
+    d_out = as_operand(d_out, dev)
+    if boundary is None:
+        if tuple(d_out.shape) != tuple(q.shape):
+            raise ShapeError(f"dO shape {tuple(d_out.shape)} != {tuple(q.shape)}")
+        dq = torch.empty((B, H, T_q, D), dtype=torch.float32, device=dev)
+        dk = torch.empty((B, H, T_kv, D), dtype=torch.float32, device=dev)
+        dv = torch.empty((B, H, T_kv, D), dtype=torch.float32, device=dev)
+        Tq_out, Tkv_out, out_b = T_q, T_kv, 0
+        d_sorted = d_out
+    else:
+        Tq_out, Tkv_out, zero = boundary
+        dq = _zeros_or_empty((B, Tq_out, H, D), torch.float32, dev, zero)
+        dk = _zeros_or_empty((B, Tkv_out, H, D), torch.float32, dev, zero)
+        dv = _zeros_or_empty((B, Tkv_out, H, D), torch.float32, dev, zero)
+        out_b = 1
+        d_sorted = torch.empty((B, H, T_q, D), dtype=torch.bfloat16, device=dev)
     if BH == 0:
         return dq, dk, dv
-    Tq_pad = pad128(T_q)
     delta = torch.empty((BH, Tq_pad), dtype=torch.float32, device=dev)
     lse2 = torch.empty((BH, Tq_pad), dtype=torch.float32, device=dev)
     lse_in = getattr(outputs, "_lse2", None)
@@ -242,25 +277,26 @@ def attention_backward(problem, q, k, v, outputs, d_out, scale=None):
         M = torch.as_tensor(M, device=dev).to(torch.float32).contiguous()
         Lv = torch.as_tensor(Lv, device=dev).to(torch.float32).contiguous()
     _lib.call("scfa_bwd_prep", _lib.ptr(O), _lib.ptr(d_out), _lib.ptr(lse_in), _lib.ptr(M), _lib.ptr(Lv),
-              BH, T_q, D, Tq_pad, _scale(scale, D), _lib.ptr(delta), _lib.ptr(lse2), _lib.stream_ptr())
+              BH, T_q, D, Tq_pad, _lib.ptr(problem.q_idx) if out_b else None, H, Tq_out,
+              _lib.ptr(d_sorted) if out_b else None, _lib.ptr(delta), _lib.ptr(lse2), _lib.stream_ptr())
     qh, kh = problem._hash_ptrs()
     if T_q > 0:
         lst, cnt, stride = problem.tile_list(True, 64)
         _lib.call(
             "scfa_attn_bwd_dq",
-            _lib.ptr(q), _lib.ptr(k), _lib.ptr(v), _lib.ptr(d_out), BH, T_q, T_kv, D,
+            _lib.ptr(q), _lib.ptr(k), _lib.ptr(v), _lib.ptr(d_sorted), BH, T_q, T_kv, D,
             _lib.ptr(problem.q_idx), qh, _lib.ptr(problem.k_idx), kh, problem.Tq_pad, problem.Tkv_pad,
             _lib.ptr(lse2), _lib.ptr(delta), _lib.ptr(lst), _lib.ptr(cnt), stride,
-            _scale(scale, D), problem.flags, _lib.ptr(dq), _lib.stream_ptr(),
+            _scale(scale, D), problem.flags, H, Tq_out, out_b, _lib.ptr(dq), _lib.stream_ptr(),
         )
     if T_kv > 0:
         lst, cnt, stride = problem.tile_list(False, 64)
         _lib.call(
             "scfa_attn_bwd_dkdv",
-            _lib.ptr(q), _lib.ptr(k), _lib.ptr(v), _lib.ptr(d_out), BH, T_q, T_kv, D,
+            _lib.ptr(q), _lib.ptr(k), _lib.ptr(v), _lib.ptr(d_sorted), BH, T_q, T_kv, D,
             _lib.ptr(problem.q_idx), qh, _lib.ptr(problem.k_idx), kh, problem.Tq_pad, problem.Tkv_pad,
             _lib.ptr(lse2), _lib.ptr(delta), _lib.ptr(lst), _lib.ptr(cnt), stride,
-            _scale(scale, D), problem.flags, _lib.ptr(dk), _lib.ptr(dv), _lib.stream_ptr(),
+            _scale(scale, D), problem.flags, H, Tkv_out, out_b, _lib.ptr(dk), _lib.ptr(dv), _lib.stream_ptr(),
         )
     return dq, dk, dv
 

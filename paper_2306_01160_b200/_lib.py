@@ -51,13 +51,13 @@ _SIGS = {
     "scfa_validate_sorted": [_P, _P, _L, _L, _L, _P, _P],
     "scfa_build_tile_lists": [_P, _P, _P, _P, _L, _L, _L, _L, _L, _I, _I, _I, _I, _P, _P, _L, _P, _P, _L, _P],
     "scfa_ref_schedule": [_P, _P, _P, _P, _L, _L, _L, _L, _L, _L, _L, _I, _P, _P, _P, _P],
-    "scfa_attn_fwd": [_P, _P, _P, _L, _L, _L, _L, _P, _P, _P, _P, _L, _L, _P, _P, _L, _F, _I, _P, _P, _P,
-                      _P, _P],
-    "scfa_bwd_prep": [_P, _P, _P, _P, _P, _L, _L, _L, _L, _F, _P, _P, _P],
+    "scfa_attn_fwd": [_P, _P, _P, _L, _L, _L, _L, _P, _P, _P, _P, _L, _L, _P, _P, _L, _F, _I, _L, _L, _I,
+                      _P, _P, _P, _P, _P],
+    "scfa_bwd_prep": [_P, _P, _P, _P, _P, _L, _L, _L, _L, _P, _L, _L, _P, _P, _P, _P],
     "scfa_attn_bwd_dq": [_P, _P, _P, _P, _L, _L, _L, _L, _P, _P, _P, _P, _L, _L, _P, _P, _P, _P, _L, _F, _I,
-                         _P, _P],
+                         _L, _L, _I, _P, _P],
     "scfa_attn_bwd_dkdv": [_P, _P, _P, _P, _L, _L, _L, _L, _P, _P, _P, _P, _L, _L, _P, _P, _P, _P, _L, _F,
-                           _I, _P, _P, _P],
+                           _I, _L, _L, _I, _P, _P, _P],
 }
 
 _lib = None

@@ -81,8 +81,9 @@ extern "C" const char* scfa_last_error(void) { return g_err; }
 extern "C" int scfa_attn_fwd(const void* q, const void* k, const void* v, int64_t BH, int64_t T_q, int64_t T_kv,
                              int64_t D, const int32_t* q_idx, const int32_t* q_hash, const int32_t* k_idx,
                              const int32_t* k_hash, int64_t Tq_pad, int64_t Tkv_pad, const uint16_t* list,
-                             const int32_t* list_count, int64_t list_stride, float scale, int flags, void* o, float* m,
-                             float* l, float* lse2, void* stream) {
+                             const int32_t* list_count, int64_t list_stride, float scale, int flags, int64_t H,
+                             int64_t T_out, int out_boundary, void* o, float* m, float* l, float* lse2,
+                             void* stream) {
   int rc = check_attn_args(BH, T_q, T_kv, D, Tq_pad, Tkv_pad, q, k, v);
   if (rc) return rc;
   if (BH == 0 || T_q == 0) return SCFA_OK;
@@ -90,6 +91,9 @@ extern "C" int scfa_attn_fwd(const void* q, const void* k, const void* v, int64_
   L.mode = 0;
   L.D = static_cast<int>(D);
   L.BH = static_cast<int>(BH);
+  L.H = static_cast<int>(H);
+  L.T_out = static_cast<int>(T_out);
+  L.out_boundary = out_boundary;
   L.T_rows = static_cast<int>(T_q);
   L.T_cols = static_cast<int>(T_kv > 0 ? T_kv : 1);
   L.T_rows_pad = static_cast<int>(Tq_pad);
@@ -125,7 +129,8 @@ static int bwd_common(int mode, const void* q, const void* k, const void* v, con
                       int64_t T_q, int64_t T_kv, int64_t D, const int32_t* q_idx, const int32_t* q_hash,
                       const int32_t* k_idx, const int32_t* k_hash, int64_t Tq_pad, int64_t Tkv_pad, const float* lse2,
                       const float* delta, const uint16_t* list, const int32_t* list_count, int64_t list_stride,
-                      float scale, int flags, float* out0, float* out1, void* stream) {
+                      float scale, int flags, int64_t H, int64_t T_out, int out_boundary, float* out0,
+                      float* out1, void* stream) {
   int rc = check_attn_args(BH, T_q, T_kv, D, Tq_pad, Tkv_pad, q, k, v);
   if (rc) return rc;
   const bool hash = (flags & SCFA_FLAG_HASH) != 0;
@@ -133,6 +138,9 @@ static int bwd_common(int mode, const void* q, const void* k, const void* v, con
   L.mode = mode;
   L.D = static_cast<int>(D);
   L.BH = static_cast<int>(BH);
+  L.H = static_cast<int>(H);
+  L.T_out = static_cast<int>(T_out);
+  L.out_boundary = out_boundary;
   L.scale = scale;
   L.exclude_self = (flags & SCFA_FLAG_EXCLUDE_SELF) ? 1 : 0;
   L.use_hash = hash ? 1 : 0;
@@ -184,18 +192,18 @@ extern "C" int scfa_attn_bwd_dq(const void* q, const void* k, const void* v, con
                                 int64_t T_q, int64_t T_kv, int64_t D, const int32_t* q_idx, const int32_t* q_hash,
                                 const int32_t* k_idx, const int32_t* k_hash, int64_t Tq_pad, int64_t Tkv_pad,
                                 const float* lse2, const float* delta, const uint16_t* list,
-                                const int32_t* list_count, int64_t list_stride, float scale, int flags, float* dq,
-                                void* stream) {
+                                const int32_t* list_count, int64_t list_stride, float scale, int flags, int64_t H,
+                                int64_t T_out, int out_boundary, float* dq, void* stream) {
   return bwd_common(1, q, k, v, d_out, BH, T_q, T_kv, D, q_idx, q_hash, k_idx, k_hash, Tq_pad, Tkv_pad, lse2, delta,
-                    list, list_count, list_stride, scale, flags, dq, nullptr, stream);
+                    list, list_count, list_stride, scale, flags, H, T_out, out_boundary, dq, nullptr, stream);
 }
 
 extern "C" int scfa_attn_bwd_dkdv(const void* q, const void* k, const void* v, const void* d_out, int64_t BH,
                                   int64_t T_q, int64_t T_kv, int64_t D, const int32_t* q_idx, const int32_t* q_hash,
                                   const int32_t* k_idx, const int32_t* k_hash, int64_t Tq_pad, int64_t Tkv_pad,
                                   const float* lse2, const float* delta, const uint16_t* list,
-                                  const int32_t* list_count, int64_t list_stride, float scale, int flags, float* dk,
-                                  float* dv, void* stream) {
+                                  const int32_t* list_count, int64_t list_stride, float scale, int flags, int64_t H,
+                                  int64_t T_out, int out_boundary, float* dk, float* dv, void* stream) {
   return bwd_common(2, q, k, v, d_out, BH, T_q, T_kv, D, q_idx, q_hash, k_idx, k_hash, Tq_pad, Tkv_pad, lse2, delta,
-                    list, list_count, list_stride, scale, flags, dk, dv, stream);
+                    list, list_count, list_stride, scale, flags, H, T_out, out_boundary, dk, dv, stream);
 }

@@ -20,6 +20,9 @@ struct AttnLaunch {
   int mode;  // 0 fwd, 1 dq, 2 dkdv
   int D;
   int BH;
+  int H;             // heads (for the boundary-layout epilogue)
+  int T_out;         // boundary-layout sequence length
+  int out_boundary;  // 1: epilogue scatters rows to (B, T_out, H, D) by original position
   int T_rows, T_cols, T_rows_pad, T_cols_pad;
   const void* x0;
   const void* x1;

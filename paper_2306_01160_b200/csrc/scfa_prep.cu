@@ -384,10 +384,16 @@ __global__ void validate_sorted_kernel(const int32_t* idx, const int32_t* hash, 
 
 // ------------------------------------------------------------------ backward prep
 
+// delta = rowsum(dO * O) per sorted/compacted row, lse2 from (M, L) when not given.
+// Boundary mode (q_idx != nullptr): O and dO are (B, T_out, H, D); row s of slice bh
+// lives at position q_idx[bh, s], and the dO row is also written to d_out_sorted
+// (BH, T_q, D) — the gather of dO into kernel order fused with the delta pass.
 __global__ void bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ d_out,
                                 const float* __restrict__ lse2_in, const float* __restrict__ m,
                                 const float* __restrict__ l, int64_t T_q, int64_t D, int64_t Tq_pad,
-                                float* __restrict__ delta, float* __restrict__ lse2_out, int64_t total_rows) {
+                                const int32_t* __restrict__ q_idx, int64_t H, int64_t T_out,
+                                __nv_bfloat16* __restrict__ d_out_sorted, float* __restrict__ delta,
+                                float* __restrict__ lse2_out, int64_t total_rows) {
   const int tpr = static_cast<int>(D / 8);  // threads per row, 16 B each
   const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const int64_t r = g / tpr;  // padded row index
@@ -397,9 +403,20 @@ __global__ void bwd_prep_kernel(const __nv_bfloat16* __restrict__ o, const __nv_
   const int64_t bh = live ? r / Tq_pad : 0, t = live ? r - bh * Tq_pad : 0;
   const bool valid = live && t < T_q;
   if (valid) {
-    const int64_t off = (bh * T_q + t) * D + part * 8;
-    uint4 a = __ldg(reinterpret_cast<const uint4*>(o + off));
-    uint4 c = __ldg(reinterpret_cast<const uint4*>(d_out + off));
+    int64_t off = (bh * T_q + t) * D + part * 8;
+    bool have = true;
+    if (q_idx) {
+      const int64_t pos = q_idx[r];
+      have = pos >= 0 && pos < T_out;
+      const int64_t b = bh / H, h = bh - b * H;
+      off = ((b * T_out + (have ? pos : 0)) * H + h) * D + part * 8;
+    }
+    uint4 a = make_uint4(0, 0, 0, 0), c = make_uint4(0, 0, 0, 0);
+    if (have) {
+      a = __ldg(reinterpret_cast<const uint4*>(o + off));
+      c = __ldg(reinterpret_cast<const uint4*>(d_out + off));
+    }
+    if (q_idx) *reinterpret_cast<uint4*>(d_out_sorted + (bh * T_q + t) * D + part * 8) = c;
     const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
     const __nv_bfloat162* c2 = reinterpret_cast<const __nv_bfloat162*>(&c);
 #pragma unroll
@@ -556,28 +573,15 @@ extern "C" int scfa_validate_sorted(const int32_t* idx, const int32_t* hash, int
 }
 
 extern "C" int scfa_bwd_prep(const void* o, const void* d_out, const float* lse2_in, const float* m, const float* l,
-                             int64_t BH, int64_t T_q, int64_t D, int64_t Tq_pad, float scale, float* delta,
-                             float* lse2_out, void* stream) {
-  (void)scale;
+                             int64_t BH, int64_t T_q, int64_t D, int64_t Tq_pad, const int32_t* q_idx, int64_t H,
+                             int64_t T_out, void* d_out_sorted, float* delta, float* lse2_out, void* stream) {
   if (D % 8 != 0 || D / 8 > 32 || ((D / 8) & (D / 8 - 1))) { set_error("bwd_prep: unsupported D"); return SCFA_ERR_SHAPE; }
+  if (q_idx && (!d_out_sorted || H < 1)) { set_error("bwd_prep: boundary mode needs d_out_sorted and H"); return SCFA_ERR_SHAPE; }
   const int64_t rows = BH * Tq_pad;
   if (rows == 0) return SCFA_OK;
   const int64_t threads = rows * (D / 8);
   bwd_prep_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(d_out), lse2_in, m, l, T_q, D, Tq_pad,
-      delta, lse2_out, rows);
+      q_idx, H, T_out, static_cast<__nv_bfloat16*>(d_out_sorted), delta, lse2_out, rows);
   return check_launch("bwd_prep");
-}
-
-extern "C" int scfa_invert_index(const void* idx, int dtype, int64_t B, int64_t n_slots, int64_t H, int64_t sb,
-                                 int64_t ss, int64_t sh, int64_t T, int32_t* rank, int32_t* err_flag, void* stream) {
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int64_t n = B * H * T;
-  if (n == 0) return SCFA_OK;
-  fill_i32_kernel<<<grid_for(n, 256), 256, 0, s>>>(rank, static_cast<int32_t>(n_slots), n);
-  const int64_t total = B * H * n_slots;
-  if (total > 0)
-    invert_index_kernel<<<grid_for(total, 256), 256, 0, s>>>(idx, dtype, H, n_slots, sb, ss, sh, T, rank, err_flag,
-                                                              total);
-  return check_launch("invert_index");
 }

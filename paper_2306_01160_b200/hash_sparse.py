@@ -275,12 +275,15 @@ def hash_scatter(o_sorted, q_idx):
 
 def hash_sparse_attention(q, k, v, q_hash, k_hash, scale=None, blocks=BlockSpec(), exclude_self=True,
                           workers=None):
-    """End-to-end hash-sparse attention in boundary layout (hash_sparse.py:223-238)."""
+    """End-to-end hash-sparse attention in boundary layout (hash_sparse.py:223-238).
+
+    The forward epilogue writes each sorted row straight back to its original
+    position (hash_scatter + from_heads fused).
+    """
     q, k, v = as_operand(q), as_operand(k), as_operand(v)
     sb = _sort_batch(q, k, v, q_hash, k_hash, "bthd")
     prob = _problem_of(sb, exclude_self)
-    outputs = attention_forward(prob, sb.q, sb.k, sb.v, scale, blocks)
-    return _scatter(outputs.O, sb.q_rank, "bthd")
+    return attention_forward(prob, sb.q, sb.k, sb.v, scale, blocks, boundary=(q.shape[1], False)).O
 
 
 def hash_sparse_attention_fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, exclude_self=True):
@@ -288,13 +291,14 @@ def hash_sparse_attention_fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, ex
 
     Returns (O bf16, dQ, dK, dV fp32), each (B, T, H, D).  The reference
     composes the same from sort_by_bucket -> hash_forward_kernel ->
-    hash_backward_kernel(dO sorted by q order) -> inverse permutation.
+    hash_backward_kernel(dO sorted by q order) -> inverse permutation; here the
+    permutations are fused into the kernels' loads (sorted copies) and epilogues.
     """
     q, k, v = as_operand(q), as_operand(k), as_operand(v)
     sb = _sort_batch(q, k, v, q_hash, k_hash, "bthd", check=False)
     prob = _problem_of(sb, exclude_self)
-    outputs = attention_forward(prob, sb.q, sb.k, sb.v, scale)
-    d_out_s = _gather(as_operand(d_out), sb.q_perm, "bthd")
-    dq, dk, dv = attention_backward(prob, sb.q, sb.k, sb.v, outputs, d_out_s, scale)
-    return (_scatter(outputs.O, sb.q_rank, "bthd"), _scatter(dq, sb.q_rank, "bthd"),
-            _scatter(dk, sb.k_rank, "bthd"), _scatter(dv, sb.k_rank, "bthd"))
+    T_Q, T_KV = q.shape[1], k.shape[1]
+    outputs = attention_forward(prob, sb.q, sb.k, sb.v, scale, boundary=(T_Q, False))
+    dq, dk, dv = attention_backward(prob, sb.q, sb.k, sb.v, outputs, as_operand(d_out), scale,
+                                    boundary=(T_Q, T_KV, False))
+    return outputs.O, dq, dk, dv

@@ -242,10 +242,14 @@ def qk_postprocess(o_kernel, scatter_index, T_Q, rank=None):
 
 
 def qk_sparse_attention(q, k, v, q_keep, k_keep, scale=None, blocks=BlockSpec(), workers=None):
-    """End-to-end QK-sparse attention in boundary layout (qk_sparse.py:228-239)."""
+    """End-to-end QK-sparse attention in boundary layout (qk_sparse.py:228-239).
+
+    The forward epilogue writes every kept query row straight to its original
+    position (the inverse scatter of qk_postprocess is fused); dropped rows are zero.
+    """
     prep = qk_preprocess(q, k, v, q_keep, k_keep)
-    outputs = attention_forward(prep.problem, prep.q_c, prep.k_c, prep.v_c, scale, blocks)
-    return qk_postprocess(outputs.O, prep.scatter_index, prep.T_Q, rank=prep.q_rank)
+    return attention_forward(prep.problem, prep.q_c, prep.k_c, prep.v_c, scale, blocks,
+                             boundary=(prep.T_Q, True)).O
 
 
 def qk_sparse_attention_fwd_bwd(q, k, v, q_keep, k_keep, d_out, scale=None):
@@ -256,16 +260,11 @@ def qk_sparse_attention_fwd_bwd(q, k, v, q_keep, k_keep, d_out, scale=None):
     from qk_preprocess -> qk_forward_kernel -> qk_backward_kernel.
     """
     prep = qk_preprocess(q, k, v, q_keep, k_keep)
-    B, T_Q, H, D = q.shape
-    T_KV = k.shape[1]
-    outputs = attention_forward(prep.problem, prep.q_c, prep.k_c, prep.v_c, scale)
-    d_out = as_operand(d_out)
-    # dO rows follow the queries' compaction order
-    q_perm = prep.scatter_index.transpose(1, 2).reshape(B * H, -1)
-    d_out_c = _gather(d_out, q_perm.contiguous(), prep.q_c.shape[2])
-    dq, dk, dv = attention_backward(prep.problem, prep.q_c, prep.k_c, prep.v_c, outputs, d_out_c, scale)
-    o = _scatter(outputs.O, prep.q_rank, T_Q)
-    return o, _scatter(dq, prep.q_rank, T_Q), _scatter(dk, prep.k_rank, T_KV), _scatter(dv, prep.k_rank, T_KV)
+    T_Q, T_KV = q.shape[1], k.shape[1]
+    outputs = attention_forward(prep.problem, prep.q_c, prep.k_c, prep.v_c, scale, boundary=(T_Q, True))
+    dq, dk, dv = attention_backward(prep.problem, prep.q_c, prep.k_c, prep.v_c, outputs, as_operand(d_out), scale,
+                                    boundary=(T_Q, T_KV, True))
+    return outputs.O, dq, dk, dv
 
 
 def random_keep(B, T, H, drop_prob, seed):
