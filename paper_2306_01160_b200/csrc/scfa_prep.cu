@@ -585,3 +585,16 @@ extern "C" int scfa_bwd_prep(const void* o, const void* d_out, const float* lse2
       q_idx, H, T_out, static_cast<__nv_bfloat16*>(d_out_sorted), delta, lse2_out, rows);
   return check_launch("bwd_prep");
 }
+
+extern "C" int scfa_invert_index(const void* idx, int dtype, int64_t B, int64_t n_slots, int64_t H, int64_t sb,
+                                 int64_t ss, int64_t sh, int64_t T, int32_t* rank, int32_t* err_flag, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t n = B * H * T;
+  if (n == 0) return SCFA_OK;
+  fill_i32_kernel<<<grid_for(n, 256), 256, 0, s>>>(rank, static_cast<int32_t>(n_slots), n);
+  const int64_t total = B * H * n_slots;
+  if (total > 0)
+    invert_index_kernel<<<grid_for(total, 256), 256, 0, s>>>(idx, dtype, H, n_slots, sb, ss, sh, T, rank, err_flag,
+                                                              total);
+  return check_launch("invert_index");
+}
