@@ -212,6 +212,11 @@ int scfa_attn_bwd_dkdv(const void* q, const void* k, const void* v, const void* 
                        float scale, int flags, int64_t H, int64_t T_out, int out_boundary,
                        float* dk, float* dv, void* stream);
 
+/* ---------------------------------------------------------------- diagnostics
+ * Route per-tile clock64 stamps of subsequent attention launches into `buf`
+ * (grid * tiles_per_cta * 8 int64; NULL disables).  Not part of the reference API. */
+int scfa_debug_timing(void* buf, int64_t tiles_per_cta);
+
 #ifdef __cplusplus
 }
 #endif

@@ -88,7 +88,18 @@ struct AttnArgs {
   float scale;
   int exclude_self;
   int use_hash;
+  long long* dbg;   // optional per-tile timestamps (diagnostics)
+  int dbg_tiles;
 };
+
+// Diagnostics: per-CTA, per-tile clock64 stamps (row thread 0: slots 0-2, MMA lane: 3-7).
+#define SCFA_STAMP(k)                                                                         \
+  if (args.dbg && threadIdx.x == 0 && tg < args.dbg_tiles)                                   \
+    args.dbg[(static_cast<size_t>(blockIdx.x) * args.dbg_tiles + tg) * 8 + (k)] = clock64();
+#define SCFA_MSTAMP(k) SCFA_STAMP_MMA(k)
+#define SCFA_STAMP_MMA(k)                                                                     \
+  if (args.dbg && tg < args.dbg_tiles)                                                       \
+    args.dbg[(static_cast<size_t>(blockIdx.x) * args.dbg_tiles + tg) * 8 + (k)] = clock64();
 
 // Work item -> (bh, row block).  Items run heaviest row block first (largest causal
 // reach), cycling over heads, and CTAs take items round-robin.
@@ -292,7 +303,9 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
         tc_fence_after();
         for (int t = 0; t < n; ++t, ++tg) {
           const int st = tg % C::NS;
+          SCFA_MSTAMP(6);
           mbar_wait(bar_y_full + st, (tg / C::NS) & 1);
+          SCFA_MSTAMP(7);
           tc_fence_after();
           const uint32_t y0_addr = smem_u32(smem + C::OFF_STAGE + st * C::STAGE_BYTES);
           const uint32_t y1_addr = y0_addr + C::Y_BYTES;
@@ -315,7 +328,9 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
           }
           umma_commit(bar_s_full);
           if (t == n - 1) umma_commit(bar_x_empty + xs);  // last read of this stationary slot issued
+          SCFA_MSTAMP(3);
           mbar_wait(bar_p_full, tg & 1);
+          SCFA_MSTAMP(4);
           if (t == 0 && ia >= C::NACC) mbar_wait(bar_acc_free + ab, ((ia / C::NACC) - 1) & 1);
           tc_fence_after();
           // Accumulate: A (bf16) from TMEM, B = streamed tile read MN-major, K = BN streamed rows.
@@ -336,6 +351,7 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
             }
           }
           umma_commit(bar_y_empty + st);
+          SCFA_MSTAMP(5);
         }
         umma_commit(bar_acc_full + ab);
         ++ia;
@@ -380,7 +396,9 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
           const int* khash = kidx + C::BN;
           constexpr int NW = C::BN / 32;
           uint32_t vis[NW];
+          SCFA_STAMP(0);
           mbar_wait(bar_s_full, tg & 1);
+          SCFA_STAMP(1);
           tc_fence_after();
           uint32_t raw[C::BN];
 #pragma unroll
@@ -452,6 +470,7 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
           tmem_wait_st();
           tc_fence_before();
           mbar_arrive(bar_p_full);
+          SCFA_STAMP(2);
         }
         // ---------------- epilogue: O / l (fused scatter), M, L, lse2
         if (n > 0) {
@@ -512,7 +531,9 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
           const float* cdelta = clse + C::BN;
           constexpr int NW = C::BN / 32;
           uint32_t vis[NW];
+          SCFA_STAMP(0);
           mbar_wait(bar_s_full, tg & 1);
+          SCFA_STAMP(1);
           tc_fence_after();
           if (full) {
 #pragma unroll
@@ -569,6 +590,7 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
           tmem_wait_st();
           tc_fence_before();
           mbar_arrive(bar_p_full);
+          SCFA_STAMP(2);
         }
         if (n > 0) {
           mbar_wait(bar_acc_full + ab, (ia / C::NACC) & 1);
@@ -627,6 +649,9 @@ static int make_map(CUtensorMap* map, const void* base, int BH, int T, int D, in
   return encode_tensor_map_bf16_3d(map, base, dims, strides, box, estr);
 }
 
+static long long* g_dbg_buf = nullptr;
+static int g_dbg_tiles = 0;
+
 static int sm_count() {
   int dev = 0, n = 148;
   cudaGetDevice(&dev);
@@ -672,6 +697,8 @@ static int launch_mode(const AttnLaunch& L, cudaStream_t stream) {
   a.scale = L.scale;
   a.exclude_self = L.exclude_self;
   a.use_hash = L.use_hash;
+  a.dbg = g_dbg_buf;
+  a.dbg_tiles = g_dbg_tiles;
   auto kern = scfa_attn_kernel<kMode, kD>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES) != cudaSuccess)
     return SCFA_ERR_CUDA;
@@ -697,4 +724,14 @@ int launch_attention(const AttnLaunch& L, cudaStream_t stream) {
   return SCFA_ERR_SHAPE;
 }
 
+void set_debug_buffer(long long* p, int tiles) {
+  g_dbg_buf = p;
+  g_dbg_tiles = tiles;
+}
+
 }  // namespace scfa
+
+extern "C" int scfa_debug_timing(void* buf, int64_t tiles_per_cta) {
+  scfa::set_debug_buffer(static_cast<long long*>(buf), static_cast<int>(tiles_per_cta));
+  return 0;
+}
