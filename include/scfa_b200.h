@@ -20,7 +20,7 @@
  *   - Layouts: boundary (B, T, H, D) and engine (B, H, T, D) are both
  *     accepted through explicit element strides; attention operands are
  *     engine-layout, contiguous, bf16.  Index/bucket vectors consumed by the
- *     attention kernels are int32, one row of T_pad entries per (b, h)
+ *     schedule are int32, one row of T_pad entries per (b, h)
  *     (T_pad = round_up(T, 128)), produced by scfa_build_aux / scfa_pack_index.
  */
 #ifndef SCFA_B200_H
@@ -134,21 +134,34 @@ int scfa_validate_sorted(const int32_t* idx, const int32_t* hash, int64_t BH, in
                          int64_t T_pad, int32_t* err_flag, void* stream);
 
 /* ---------------------------------------------------------------- schedules
- * Exact tile lists for the kernels.  Replaces the per-head schedule of
- * causal_j_stops (_kernel.py:45-53) and hash_tile_ranges (_kernel.py:56-79),
- * tightened: only tiles with >= 1 visible pair are listed, and tiles whose
- * pairs are all visible carry bit 15 ("no mask needed").
- * rows_are_queries = 1: stationary side = queries (fwd, dQ); 0: keys (dK/dV).
- * Block sizes: row_block 128; col_block 128 (fwd) or 64 (bwd).
- * list (B*H, n_row_blocks, list_stride) uint16 with list_stride >= n_col_blocks;
- * list_count (B*H, n_row_blocks) int32; tiles_total (1 int64, accumulated, may be NULL).
- * workspace: >= 16 * B*H * (n_row_blocks + n_col_blocks) bytes, 16-byte aligned.  */
-int scfa_build_tile_lists(const int32_t* q_idx, const int32_t* q_hash, const int32_t* k_idx,
-                          const int32_t* k_hash, int64_t BH, int64_t T_q, int64_t T_kv,
-                          int64_t Tq_pad, int64_t Tkv_pad, int rows_are_queries, int row_block,
-                          int col_block, int flags, uint16_t* list, int32_t* list_count,
-                          int64_t list_stride, unsigned long long* tiles_total, void* workspace,
-                          int64_t workspace_bytes, void* stream);
+ * scfa_build_schedule replaces the per-head schedules causal_j_stops
+ * (_kernel.py:45-53) and hash_tile_ranges (_kernel.py:56-79), and the mask
+ * construction of _tile_mask (_kernel.py:82-89).
+ *
+ * Visibility runs.  With keys sorted by position (QK / dense) or by
+ * (bucket, position) (hash), the keys a query sees form ONE contiguous run of
+ * key slots, and the queries that see a key form one run of query slots.
+ *   q_runs (B*H, Tq_pad) int32 pairs [lo, hi): visible key slots of each query slot.
+ *   k_runs (B*H, Tkv_pad) int32 pairs [lo, hi): query slots that see each key slot.
+ * Slots past T get the empty run.  Either may be NULL if no list needs it.
+ * runs_ready: bit 0 = q_runs already holds this problem's runs (not recomputed),
+ * bit 1 = the same for k_runs.
+ *
+ * Tile lists (uint16 column-block ids, ascending; bit 15 = "every pair visible",
+ * so no mask is needed).  They are exact: a tile is listed iff it holds at least
+ * one visible pair.
+ *   fwd : query rows in 128-row blocks x 128-key tiles   (scfa_attn_fwd)
+ *   dq  : query rows in 128-row blocks x 64-key tiles    (scfa_attn_bwd_dq)
+ *   dkdv: key rows in 128-row blocks x 64-query tiles    (scfa_attn_bwd_dkdv)
+ * list_* (B*H, n_row_blocks, stride_*) with stride >= n_col_blocks; count_*
+ * (B*H, n_row_blocks) int32.  A NULL list skips that list.  tiles[3] (may be
+ * NULL) accumulates the listed-tile totals.  flags: SCFA_FLAG_*.            */
+int scfa_build_schedule(const int32_t* q_idx, const int32_t* q_hash, const int32_t* k_idx,
+                        const int32_t* k_hash, int64_t BH, int64_t T_q, int64_t T_kv, int64_t Tq_pad,
+                        int64_t Tkv_pad, int flags, int32_t* q_runs, int32_t* k_runs,
+                        int runs_ready, uint16_t* list_fwd, int32_t* count_fwd, int64_t stride_fwd, uint16_t* list_dq,
+                        int32_t* count_dq, int64_t stride_dq, uint16_t* list_dkdv, int32_t* count_dkdv,
+                        int64_t stride_dkdv, unsigned long long* tiles, void* stream);
 
 /* Reference schedule at arbitrary BlockSpec(B_m, B_n) (tensors.py:63-78):
  * j_start/j_stop per query block exactly as causal_j_stops (flags without
@@ -164,20 +177,21 @@ int scfa_ref_schedule(const int32_t* q_idx, const int32_t* q_hash, const int32_t
  * qk_forward_kernel (qk_sparse.py:120-148) / hash_forward_kernel
  * (hash_sparse.py:145-179) / flash_forward (dense.py:33-63).
  * q (B*H, T_q, D), k/v (B*H, T_kv, D) bf16 contiguous, D in {64, 128}.
+ * q_idx: padded query positions (output routing), q_runs / list_fwd / count_fwd
+ * from scfa_build_schedule.  Causality, exclude_self and buckets are all encoded
+ * in the runs.
  * o (B*H, T_q, D) bf16 (normalised output), m/l (B*H, T_q) f32 = FlashOutputs.M/L
  * (M = -inf, L = 0 for stranded rows), lse2 (B*H, Tq_pad) f32 log2-domain
  * logsumexp (+inf for stranded rows) consumed by the backward.
- * list/list_count: from scfa_build_tile_lists(rows_are_queries=1, 128, 128).
  * Output layout: out_boundary = 0 writes o as (B*H, T_q, D); out_boundary = 1 writes
  * row s of slice (b, h) to o[b, q_idx[bh, s], h, :] of a (B, T_out, H, D) tensor (H
  * heads) — the inverse scatter of qk_postprocess / hash_scatter fused into the
  * epilogue; pad rows (q_idx outside [0, T_out)) are not written.                  */
 int scfa_attn_fwd(const void* q, const void* k, const void* v, int64_t BH, int64_t T_q,
-                  int64_t T_kv, int64_t D, const int32_t* q_idx, const int32_t* q_hash,
-                  const int32_t* k_idx, const int32_t* k_hash, int64_t Tq_pad, int64_t Tkv_pad,
-                  const uint16_t* list, const int32_t* list_count, int64_t list_stride,
-                  float scale, int flags, int64_t H, int64_t T_out, int out_boundary, void* o,
-                  float* m, float* l, float* lse2, void* stream);
+                  int64_t T_kv, int64_t D, const int32_t* q_idx, const int32_t* q_runs,
+                  int64_t Tq_pad, int64_t Tkv_pad, const uint16_t* list, const int32_t* list_count,
+                  int64_t list_stride, float scale, int64_t H, int64_t T_out, int out_boundary,
+                  void* o, float* m, float* l, float* lse2, void* stream);
 
 /* delta = rowsum(dO * O) (qk_sparse.py:168, hash_sparse.py:194, dense.py:81);
  * lse2 rebuilt from (M, L) when lse2_in is NULL (m_hat/inv_l, _kernel.py:152-154).
@@ -190,32 +204,34 @@ int scfa_bwd_prep(const void* o, const void* d_out, const float* lse2_in, const 
                   const int32_t* q_idx, int64_t H, int64_t T_out, void* d_out_sorted, float* delta,
                   float* lse2_out, void* stream);
 
-/* Backward pass 1 (dQ, query-block owner, _kernel.py:173-179).
- * list: scfa_build_tile_lists(rows_are_queries=1, 128, 64).  dq (B*H,T_q,D) f32,
- * or (B, T_out, H, D) scattered by q_idx when out_boundary (as scfa_attn_fwd).      */
+/* Backward pass 1 (dQ, query-block owner, _kernel.py:173-179).  q_runs, list_dq,
+ * count_dq from scfa_build_schedule.  dq (B*H, T_q, D) f32, or (B, T_out, H, D)
+ * scattered by q_idx when out_boundary (as scfa_attn_fwd).                          */
 int scfa_attn_bwd_dq(const void* q, const void* k, const void* v, const void* d_out, int64_t BH,
                      int64_t T_q, int64_t T_kv, int64_t D, const int32_t* q_idx,
-                     const int32_t* q_hash, const int32_t* k_idx, const int32_t* k_hash,
-                     int64_t Tq_pad, int64_t Tkv_pad, const float* lse2, const float* delta,
-                     const uint16_t* list, const int32_t* list_count, int64_t list_stride,
-                     float scale, int flags, int64_t H, int64_t T_out, int out_boundary,
+                     const int32_t* q_runs, int64_t Tq_pad, int64_t Tkv_pad, const float* lse2,
+                     const float* delta, const uint16_t* list, const int32_t* list_count,
+                     int64_t list_stride, float scale, int64_t H, int64_t T_out, int out_boundary,
                      float* dq, void* stream);
 
 /* Backward pass 2 (dK/dV, key-block owner over the transposed schedule,
- * _kernel.py:181-192).  list: scfa_build_tile_lists(rows_are_queries=0, 128, 64).
+ * _kernel.py:181-192).  k_runs, list_dkdv, count_dkdv from scfa_build_schedule.
  * dk, dv (B*H, T_kv, D) f32, or (B, T_out, H, D) scattered by k_idx when out_boundary. */
 int scfa_attn_bwd_dkdv(const void* q, const void* k, const void* v, const void* d_out, int64_t BH,
-                       int64_t T_q, int64_t T_kv, int64_t D, const int32_t* q_idx,
-                       const int32_t* q_hash, const int32_t* k_idx, const int32_t* k_hash,
-                       int64_t Tq_pad, int64_t Tkv_pad, const float* lse2, const float* delta,
-                       const uint16_t* list, const int32_t* list_count, int64_t list_stride,
-                       float scale, int flags, int64_t H, int64_t T_out, int out_boundary,
+                       int64_t T_q, int64_t T_kv, int64_t D, const int32_t* k_idx,
+                       const int32_t* k_runs, int64_t Tq_pad, int64_t Tkv_pad, const float* lse2,
+                       const float* delta, const uint16_t* list, const int32_t* list_count,
+                       int64_t list_stride, float scale, int64_t H, int64_t T_out, int out_boundary,
                        float* dk, float* dv, void* stream);
 
 /* ---------------------------------------------------------------- diagnostics
  * Route per-tile clock64 stamps of subsequent attention launches into `buf`
  * (grid * tiles_per_cta * 8 int64; NULL disables).  Not part of the reference API. */
 int scfa_debug_timing(void* buf, int64_t tiles_per_cta);
+
+/* Resident CTAs per SM the attention launcher chose for pass `mode` (0 fwd, 1 dQ,
+ * 2 dK/dV) at head dim D; 0 before the first launch, -1 for bad arguments.     */
+int scfa_debug_ctas_per_sm(int mode, int64_t D);
 
 #ifdef __cplusplus
 }

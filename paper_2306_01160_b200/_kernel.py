@@ -88,37 +88,53 @@ class Problem:
             return _lib.ptr(self.q_hash), _lib.ptr(self.k_hash)
         return _lib.ptr(self.q_idx), _lib.ptr(self.k_idx)
 
-    def tile_list(self, rows_are_queries, col_block):
-        key = (bool(rows_are_queries), int(col_block))
-        if key in self._lists:
-            return self._lists[key]
-        T_rows = self.T_q if rows_are_queries else self.T_kv
-        T_cols = self.T_kv if rows_are_queries else self.T_q
-        n_rb = -(-T_rows // 128)
-        n_cb = -(-T_cols // col_block)
-        stride = max(n_cb, 1)
-        dev = self.q_idx.device
-        lst = torch.empty((self.BH, max(n_rb, 1), stride), dtype=torch.int16, device=dev)
-        cnt = torch.zeros((self.BH, max(n_rb, 1)), dtype=torch.int32, device=dev)
-        if self._tiles_total is None:
-            self._tiles_total = torch.zeros(3, dtype=torch.int64, device=dev)
-        slot = {(True, 128): 0, (True, 64): 1, (False, 64): 2}.get(key, None)
-        total_ptr = None if slot is None else ctypes.c_void_p(self._tiles_total.data_ptr() + 8 * slot)
-        qh, kh = self._hash_ptrs()
-        ws = torch.empty((self.BH * (max(n_rb, 1) + stride) * 16,), dtype=torch.uint8, device=dev)
-        _lib.call(
-            "scfa_build_tile_lists",
-            _lib.ptr(self.q_idx), qh, _lib.ptr(self.k_idx), kh,
-            self.BH, self.T_q, self.T_kv, self.Tq_pad, self.Tkv_pad,
-            1 if rows_are_queries else 0, 128, int(col_block), self.flags,
-            _lib.ptr(lst), _lib.ptr(cnt), stride, total_ptr, _lib.ptr(ws), ws.numel(), _lib.stream_ptr(),
-        )
-        self._lists[key] = (lst, cnt, stride)
-        return self._lists[key]
+    # list name -> (rows are queries, streamed tile width, tiles_total slot)
+    LISTS = {"fwd": (True, 128, 0), "dq": (True, 64, 1), "dkdv": (False, 64, 2)}
+
+    def schedule(self, *which):
+        """Visibility runs + exact tile lists (scfa_build_schedule), built once per Problem.
+
+        Returns {name: (list, count, stride)} for the requested lists plus the
+        runs under "q_runs" / "k_runs".
+        """
+        which = which or tuple(self.LISTS)
+        want = [w for w in which if w not in self._lists]
+        if want:
+            dev = self.q_idx.device
+            if self._tiles_total is None:
+                self._tiles_total = torch.zeros(3, dtype=torch.int64, device=dev)
+            ready = (1 if "q_runs" in self._lists else 0) | (2 if "k_runs" in self._lists else 0)
+            if any(self.LISTS[w][0] for w in want) and "q_runs" not in self._lists:
+                self._lists["q_runs"] = torch.empty((self.BH, self.Tq_pad, 2), dtype=torch.int32, device=dev)
+            if any(not self.LISTS[w][0] for w in want) and "k_runs" not in self._lists:
+                self._lists["k_runs"] = torch.empty((self.BH, self.Tkv_pad, 2), dtype=torch.int32, device=dev)
+            args = []
+            for name in ("fwd", "dq", "dkdv"):
+                rq, cb, _ = self.LISTS[name]
+                if name in want:
+                    T_rows = self.T_q if rq else self.T_kv
+                    T_cols = self.T_kv if rq else self.T_q
+                    n_rb = max(-(-T_rows // 128), 1)
+                    stride = max(-(-T_cols // cb), 1)
+                    lst = torch.empty((self.BH, n_rb, stride), dtype=torch.int16, device=dev)
+                    cnt = torch.zeros((self.BH, n_rb), dtype=torch.int32, device=dev)
+                    self._lists[name] = (lst, cnt, stride)
+                    args += [_lib.ptr(lst), _lib.ptr(cnt), stride]
+                else:
+                    args += [None, None, 0]
+            qh, kh = self._hash_ptrs()
+            _lib.call(
+                "scfa_build_schedule",
+                _lib.ptr(self.q_idx), qh, _lib.ptr(self.k_idx), kh,
+                self.BH, self.T_q, self.T_kv, self.Tq_pad, self.Tkv_pad, self.flags,
+                _lib.ptr(self._lists.get("q_runs")), _lib.ptr(self._lists.get("k_runs")), ready,
+                *args, _lib.ptr(self._tiles_total), _lib.stream_ptr(),
+            )
+        return self._lists
 
     def executed_tiles(self):
         """128x128 tiles run by the forward kernel (non-empty tiles only)."""
-        self.tile_list(True, 128)
+        self.schedule("fwd")
         return int(self._tiles_total[0].item())
 
     def ref_schedule(self, blocks=BlockSpec()):
@@ -220,14 +236,13 @@ def attention_forward(problem, q, k, v, scale=None, blocks=None, boundary=None):
     L = torch.empty((B, H, T_q), dtype=torch.float32, device=dev)
     lse2 = torch.empty((B * H, pad128(T_q)), dtype=torch.float32, device=dev)
     if B * H > 0 and T_q > 0:
-        lst, cnt, stride = problem.tile_list(True, 128)
-        qh, kh = problem._hash_ptrs()
+        sched = problem.schedule("fwd")
+        lst, cnt, stride = sched["fwd"]
         _lib.call(
             "scfa_attn_fwd",
             _lib.ptr(q), _lib.ptr(k), _lib.ptr(v), B * H, T_q, T_kv, D,
-            _lib.ptr(problem.q_idx), qh, _lib.ptr(problem.k_idx), kh,
-            problem.Tq_pad, problem.Tkv_pad, _lib.ptr(lst), _lib.ptr(cnt), stride,
-            _scale(scale, D), problem.flags, H, T_out, out_b,
+            _lib.ptr(problem.q_idx), _lib.ptr(sched["q_runs"]), problem.Tq_pad, problem.Tkv_pad,
+            _lib.ptr(lst), _lib.ptr(cnt), stride, _scale(scale, D), H, T_out, out_b,
             _lib.ptr(O), _lib.ptr(M), _lib.ptr(L), _lib.ptr(lse2), _lib.stream_ptr(),
         )
     out = FlashOutputs(O, M, L, problem=problem, blocks=blocks, lse2=lse2)
@@ -279,24 +294,24 @@ def attention_backward(problem, q, k, v, outputs, d_out, scale=None, boundary=No
     _lib.call("scfa_bwd_prep", _lib.ptr(O), _lib.ptr(d_out), _lib.ptr(lse_in), _lib.ptr(M), _lib.ptr(Lv),
               BH, T_q, D, Tq_pad, _lib.ptr(problem.q_idx) if out_b else None, H, Tq_out,
               _lib.ptr(d_sorted) if out_b else None, _lib.ptr(delta), _lib.ptr(lse2), _lib.stream_ptr())
-    qh, kh = problem._hash_ptrs()
+    sched = problem.schedule("dq", "dkdv")
     if T_q > 0:
-        lst, cnt, stride = problem.tile_list(True, 64)
+        lst, cnt, stride = sched["dq"]
         _lib.call(
             "scfa_attn_bwd_dq",
             _lib.ptr(q), _lib.ptr(k), _lib.ptr(v), _lib.ptr(d_sorted), BH, T_q, T_kv, D,
-            _lib.ptr(problem.q_idx), qh, _lib.ptr(problem.k_idx), kh, problem.Tq_pad, problem.Tkv_pad,
+            _lib.ptr(problem.q_idx), _lib.ptr(sched["q_runs"]), problem.Tq_pad, problem.Tkv_pad,
             _lib.ptr(lse2), _lib.ptr(delta), _lib.ptr(lst), _lib.ptr(cnt), stride,
-            _scale(scale, D), problem.flags, H, Tq_out, out_b, _lib.ptr(dq), _lib.stream_ptr(),
+            _scale(scale, D), H, Tq_out, out_b, _lib.ptr(dq), _lib.stream_ptr(),
         )
     if T_kv > 0:
-        lst, cnt, stride = problem.tile_list(False, 64)
+        lst, cnt, stride = sched["dkdv"]
         _lib.call(
             "scfa_attn_bwd_dkdv",
             _lib.ptr(q), _lib.ptr(k), _lib.ptr(v), _lib.ptr(d_sorted), BH, T_q, T_kv, D,
-            _lib.ptr(problem.q_idx), qh, _lib.ptr(problem.k_idx), kh, problem.Tq_pad, problem.Tkv_pad,
+            _lib.ptr(problem.k_idx), _lib.ptr(sched["k_runs"]), problem.Tq_pad, problem.Tkv_pad,
             _lib.ptr(lse2), _lib.ptr(delta), _lib.ptr(lst), _lib.ptr(cnt), stride,
-            _scale(scale, D), problem.flags, H, Tkv_out, out_b, _lib.ptr(dk), _lib.ptr(dv), _lib.stream_ptr(),
+            _scale(scale, D), H, Tkv_out, out_b, _lib.ptr(dk), _lib.ptr(dv), _lib.stream_ptr(),
         )
     return dq, dk, dv
 

@@ -49,16 +49,18 @@ _SIGS = {
     "scfa_pack_index": [_P, _I, _L, _L, _L, _L, _L, ctypes.c_int32, _P, _P],
     "scfa_validate_qk": [_P, _P, _L, _L, _L, _L, _L, _P, _P],
     "scfa_validate_sorted": [_P, _P, _L, _L, _L, _P, _P],
-    "scfa_build_tile_lists": [_P, _P, _P, _P, _L, _L, _L, _L, _L, _I, _I, _I, _I, _P, _P, _L, _P, _P, _L, _P],
+    "scfa_build_schedule": [_P, _P, _P, _P, _L, _L, _L, _L, _L, _I, _P, _P, _I, _P, _P, _L, _P, _P, _L, _P, _P,
+                            _L, _P, _P],
     "scfa_ref_schedule": [_P, _P, _P, _P, _L, _L, _L, _L, _L, _L, _L, _I, _P, _P, _P, _P],
-    "scfa_attn_fwd": [_P, _P, _P, _L, _L, _L, _L, _P, _P, _P, _P, _L, _L, _P, _P, _L, _F, _I, _L, _L, _I,
-                      _P, _P, _P, _P, _P],
+    "scfa_attn_fwd": [_P, _P, _P, _L, _L, _L, _L, _P, _P, _L, _L, _P, _P, _L, _F, _L, _L, _I, _P, _P, _P, _P,
+                      _P],
     "scfa_bwd_prep": [_P, _P, _P, _P, _P, _L, _L, _L, _L, _P, _L, _L, _P, _P, _P, _P],
-    "scfa_attn_bwd_dq": [_P, _P, _P, _P, _L, _L, _L, _L, _P, _P, _P, _P, _L, _L, _P, _P, _P, _P, _L, _F, _I,
-                         _L, _L, _I, _P, _P],
+    "scfa_attn_bwd_dq": [_P, _P, _P, _P, _L, _L, _L, _L, _P, _P, _L, _L, _P, _P, _P, _P, _L, _F, _L, _L, _I,
+                         _P, _P],
     "scfa_debug_timing": [_P, _L],
-    "scfa_attn_bwd_dkdv": [_P, _P, _P, _P, _L, _L, _L, _L, _P, _P, _P, _P, _L, _L, _P, _P, _P, _P, _L, _F,
-                           _I, _L, _L, _I, _P, _P, _P],
+    "scfa_debug_ctas_per_sm": [_I, _L],
+    "scfa_attn_bwd_dkdv": [_P, _P, _P, _P, _L, _L, _L, _L, _P, _P, _L, _L, _P, _P, _P, _P, _L, _F, _L, _L,
+                           _I, _P, _P, _P],
 }
 
 _lib = None
@@ -102,7 +104,7 @@ def raise_for(code, what=""):
 
 
 # kernels launched per successful call (for launch accounting in bench.py)
-KERNELS_PER_CALL = {"scfa_build_tile_lists": 3, "scfa_invert_index": 2}
+KERNELS_PER_CALL = {"scfa_build_schedule": 2, "scfa_invert_index": 2}
 launches = 0
 EVENT_HOOK = None  # optional callable(name, phase) used by bench.py to time each entry point
 

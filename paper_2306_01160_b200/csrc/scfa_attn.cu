@@ -7,25 +7,30 @@
 //   BWD_DQ   rows = queries, streamed cols = keys.   S, dP = dO V^T ; dS ; dQ += dS K
 //   BWD_DKDV rows = keys,    streamed cols = queries. S^T, dP^T ; dV += P^T dO ; dK += dS^T Q
 //
-// Each CTA owns one 128-row stationary block of one (b, h) slice and walks a
-// per-block tile list built by scfa_sched.cu.  The list holds only tiles
-// that contain at least one visible (query, key) pair — fully masked tiles
-// are skipped, not masked — and flags the tiles whose pairs are all visible
-// so that the per-element causal/bucket mask runs only in boundary tiles.
+// Each CTA owns one 128-row stationary block of one (b, h) slice at a time
+// (persistent, items handed out round-robin) and walks that block's tile list
+// (scfa_sched.cu): only tiles holding at least one visible (query, key) pair are
+// listed, so fully masked tiles are skipped, not masked, and tiles whose pairs
+// are all visible carry a flag that removes the per-element mask.  Inside a
+// boundary tile a row's visible columns are one contiguous run [lo, hi) of slots
+// (its bucket run cut at the causal boundary), precomputed per row, so the mask
+// costs two subtractions per tile.
 //
 // Roles (192 threads):
-//   warps 0-3  : one thread per stationary row == TMEM lane.  Online softmax
-//                (fwd) or P / dS recompute (bwd), epilogue.
-//   warp 4     : TMA producer (stationary tiles once, streamed tiles in an
-//                NS-stage mbarrier ring, plus the per-column index/bucket
-//                (and lse/delta) vectors via cp.async.bulk).
+//   warps 0-3  : one thread per stationary row == TMEM lane.  Online softmax (fwd)
+//                or P / dS recompute (bwd) with packed fp32x2 math, and the epilogue.
+//   warp 4     : TMA producers.  Lane 0: stationary tiles + the y0 ring (K | K | Q
+//                with the per-column lse/delta of dK/dV); lane 1: the y1 ring (V | V | dO).
 //   warp 5     : TMEM allocator + single-thread tcgen05.mma issuer.
 //
-// TMEM (per CTA, 256 columns for D=64 so that two CTAs share an SM):
-//   FWD      S fp32 [0,128) (P bf16 aliases [0,64)), O fp32 [128,128+D)
-//   BWD_DQ   S [0,64) (dS bf16 aliases [0,32)), dP [64,128), dQ [128,128+D)
-//   BWD_DKDV S^T [0,64) (P^T aliases [0,32)), dP^T [64,128) (dS^T aliases
-//            [64,96)), dV [128,128+D), dK [128+D,128+2D)
+// TMEM per CTA (256 columns at D = 64, two CTAs per SM; 512 at D = 128):
+//   FWD   S fp32 [0,128)  O [128,128+D)  P bf16 [128+D, 192+D)
+//   DQ    S [0,64)  dP [64,128)  dQ [128,128+D)  dS bf16 [128+D, 160+D)
+//   DKDV  S^T [0,64)  dP^T [64,128)  dV [128,128+D)  dK [128+D,128+2D)
+//         P^T / dS^T bf16: own columns at D = 128, aliased onto S^T / dP^T at D = 64.
+// With P (dS) in its own columns the S buffer is free as soon as the row threads
+// have loaded it, so the MMA warp issues the next tile's S while they work on
+// this one ("overlap"); aliased, S(t+1) waits for the accumulate MMAs of tile t.
 #include "scfa_common.cuh"
 #include "scfa_internal.h"
 
@@ -37,44 +42,53 @@ template <int kMode, int kD>
 struct Cfg {
   static constexpr int BM = 128;                             // stationary rows per work item
   static constexpr int BN = (kMode == MODE_FWD) ? 128 : 64;  // streamed rows per tile
-  static constexpr int NS = 2;                               // streamed-tile pipeline stages
-  static constexpr int NXS = 2;                              // stationary-tile slots (next item prefetch)
   static constexpr int DCH = kD / 64;                        // 128-byte column chunks
   static constexpr int NX = (kMode == MODE_FWD) ? 1 : 2;     // stationary tensors
-  static constexpr int NAUX = (kMode == MODE_DKDV) ? 4 : 2;  // per-column vectors
+  static constexpr int NXS = 2;                              // stationary slots (next item prefetch)
+  static constexpr bool AUX = (kMode == MODE_DKDV);          // per-column lse2 / delta with y0
   static constexpr int X_BYTES = BM * kD * 2;
   static constexpr int XSLOT_BYTES = NX * X_BYTES;
   static constexpr int Y_BYTES = BN * kD * 2;
-  static constexpr int AUX_BYTES = BN * 4;
-  static constexpr int STAGE_BYTES = 2 * Y_BYTES + NAUX * AUX_BYTES;
-  // TMEM columns: S (and dP) then accumulators; two accumulator buffers when they fit
+  static constexpr int AUX_BYTES = AUX ? 2 * BN * 4 : 0;
+  // y0 / y1 ring slots are released after the S-phase MMAs ("early") or after the
+  // accumulate MMAs: K feeds only S in the forward, V feeds only dP in dQ.
+  static constexpr bool Y0_EARLY = (kMode == MODE_FWD);
+  static constexpr bool Y1_EARLY = (kMode == MODE_DQ);
+  static constexpr int NS0 = (kMode == MODE_FWD && kD == 64) ? 2 : 3;  // keeps two CTAs per SM
+  static constexpr int NS1 = (kMode == MODE_FWD && kD == 64) ? 3 : 2;  // V has the shorter lead
+  // TMEM
+  static constexpr int TM_COLS = (kD == 64) ? 256 : 512;
   static constexpr int TM_S = 0;
   static constexpr int TM_DP = (kMode == MODE_FWD) ? 0 : BN;
   static constexpr int TM_ACC = 128;
-  static constexpr int ACC_COLS = (kMode == MODE_DKDV) ? 2 * kD : kD;  // one buffer (dK/dV: dV then dK)
-  static constexpr int NACC = (kMode == MODE_DKDV) ? 1 : 2;
-  static constexpr int TM_USED = TM_ACC + NACC * ACC_COLS;
-  static constexpr uint32_t TM_COLS = TM_USED <= 256 ? 256 : 512;
-  // shared memory carve-up (offsets from a 1024-aligned base)
+  static constexpr int ACC_COLS = (kMode == MODE_DKDV) ? 2 * kD : kD;
+  static constexpr int P_COLS = (kMode == MODE_DKDV) ? BN : BN / 2;
+  static constexpr bool OVERLAP = TM_ACC + ACC_COLS + P_COLS <= TM_COLS;
+  static constexpr int TM_P = OVERLAP ? TM_ACC + ACC_COLS : TM_S;                 // P | dS | P^T
+  static constexpr int TM_P2 = OVERLAP ? TM_ACC + ACC_COLS + BN / 2 : TM_DP;      // dS^T (DKDV)
+  // shared memory (all TMA destinations 1024-aligned)
   static constexpr int OFF_X = 0;
-  static constexpr int OFF_STAGE = OFF_X + NXS * XSLOT_BYTES;
-  static constexpr int OFF_BAR = OFF_STAGE + NS * STAGE_BYTES;
-  static constexpr int N_BARS = 2 + 2 * NXS + 2 * NS + 2 * NACC;
-  static constexpr int SMEM_BYTES = OFF_BAR + 8 * N_BARS + 16 + 1024 /*align slack*/;
+  static constexpr int OFF_Y0 = OFF_X + NXS * XSLOT_BYTES;
+  static constexpr int OFF_Y1 = OFF_Y0 + NS0 * Y_BYTES;
+  static constexpr int OFF_AUX = OFF_Y1 + NS1 * Y_BYTES;
+  static constexpr int OFF_BAR = OFF_AUX + NS0 * AUX_BYTES;
+  // s_full, s_free, p_full, p_free, acc_full, x_full/empty[NXS], y0_full/empty[NS0], y1_full/empty[NS1]
+  static constexpr int N_BARS = 5 + 2 * NXS + 2 * NS0 + 2 * NS1;
+  static constexpr int SMEM_BYTES = OFF_BAR + 8 * N_BARS + 16;
+  static_assert(X_BYTES % 1024 == 0 && Y_BYTES % 1024 == 0, "TMA tiles must stay 1024-aligned");
+  static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
 };
 
 struct AttnArgs {
   int BH, H;
   int T_rows, T_cols;          // true lengths of the stationary / streamed side
-  int T_rows_pad, T_cols_pad;  // padded lengths of the aux vectors
+  int T_rows_pad, T_cols_pad;  // padded lengths of the per-slot vectors
   int T_out;                   // boundary-layout output length (out_boundary)
   int out_boundary;            // 1: write rows to (B, T_out, H, D) at their original position
-  const int* row_idx;
-  const int* row_hash;
-  const int* col_idx;
-  const int* col_hash;
-  const float* lse2;   // (BH, Tq_pad), log2-domain; +inf where no key is visible
-  const float* delta;  // (BH, Tq_pad)
+  const int* row_idx;          // original position of each stationary row (output routing)
+  const int2* row_runs;        // visible streamed-slot run [lo, hi) of each stationary row
+  const float* lse2;           // (BH, Tq_pad), log2 domain; +inf where no key is visible
+  const float* delta;          // (BH, Tq_pad)
   const uint16_t* list;
   const int* list_count;
   int list_stride;
@@ -86,20 +100,17 @@ struct AttnArgs {
   float* out_lse2;       // FWD
   float scale_log2;
   float scale;
-  int exclude_self;
-  int use_hash;
-  long long* dbg;   // optional per-tile timestamps (diagnostics)
+  long long* dbg;  // optional per-tile timestamps (diagnostics)
   int dbg_tiles;
 };
 
-// Diagnostics: per-CTA, per-tile clock64 stamps (row thread 0: slots 0-2, MMA lane: 3-7).
-#define SCFA_STAMP(k)                                                                         \
-  if (args.dbg && threadIdx.x == 0 && tg < args.dbg_tiles)                                   \
-    args.dbg[(static_cast<size_t>(blockIdx.x) * args.dbg_tiles + tg) * 8 + (k)] = clock64();
-#define SCFA_MSTAMP(k) SCFA_STAMP_MMA(k)
-#define SCFA_STAMP_MMA(k)                                                                     \
-  if (args.dbg && tg < args.dbg_tiles)                                                       \
-    args.dbg[(static_cast<size_t>(blockIdx.x) * args.dbg_tiles + tg) * 8 + (k)] = clock64();
+// Diagnostics: per-CTA, per-tile clock64 stamps, 16 slots per tile (see scripts/timing.py).
+#define SCFA_STAMP_AT(i, k)                                                                   \
+  if (args.dbg && (i) >= 0 && (i) < args.dbg_tiles)                                          \
+    args.dbg[(static_cast<size_t>(blockIdx.x) * args.dbg_tiles + (i)) * 16 + (k)] = clock64();
+#define SCFA_STAMP(k) \
+  if (threadIdx.x == 0) { SCFA_STAMP_AT(tg, k) }
+#define SCFA_MSTAMP(k) SCFA_STAMP_AT(tg, k)
 
 // Work item -> (bh, row block).  Items run heaviest row block first (largest causal
 // reach), cycling over heads, and CTAs take items round-robin.
@@ -122,74 +133,54 @@ SCFA_DEVICE bool out_row(const AttnArgs& a, int bh, int row, int pos, size_t& of
   return true;
 }
 
-// ---- per-row visibility interval -------------------------------------------------
-// Inside one tile the streamed columns are sorted by (bucket, position) (hash) or by
-// position (QK / dense), with pads and out-of-range slots at the tail.  The columns a
-// stationary row can see therefore form ONE contiguous run [lo, hi): the row's bucket
-// run, cut at the causal boundary.  It is found with a few binary searches in shared
-// memory per row and tile, and applied as a 32-bit mask per 32 columns (R2P + FSEL).
-
-// first i in [0, n) with a[i] >= x  (a ascending on [0, n))
-SCFA_DEVICE int lower_bound(const int* a, int n, int x) {
-  int lo = 0;
-  while (n > 0) {
-    const int h = n >> 1;
-    if (a[lo + h] < x) { lo += h + 1; n -= h + 1; } else { n = h; }
-  }
-  return lo;
-}
-// first i in [0, n) with a[i] > x
-SCFA_DEVICE int upper_bound(const int* a, int n, int x) {
-  int lo = 0;
-  while (n > 0) {
-    const int h = n >> 1;
-    if (a[lo + h] <= x) { lo += h + 1; n -= h + 1; } else { n = h; }
-  }
-  return lo;
-}
-
-// rows are queries (fwd, dQ): columns are keys.  visible <=> k_idx <(=) q_idx [and same bucket]
-template <int BN>
-SCFA_DEVICE void interval_q_rows(const int* kidx, const int* khash, int nv, int qi, int qh, bool excl, bool use_hash,
-                                 int& lo, int& hi) {
-  if (!use_hash) {  // keys ascending over all BN slots (pads 10^9, out-of-range INT_MAX)
-    lo = 0;
-    hi = excl ? lower_bound(kidx, BN, qi) : upper_bound(kidx, BN, qi);
-  } else {          // valid slots [0, nv) sorted by (bucket, position)
-    const int a = lower_bound(khash, nv, qh);
-    const int e = a + upper_bound(khash + a, nv - a, qh);
-    lo = a;
-    hi = a + (excl ? lower_bound(kidx + a, e - a, qi) : upper_bound(kidx + a, e - a, qi));
-  }
-}
-
-// rows are keys (dK/dV): columns are queries.  visible <=> q_idx >(=) k_idx [and same bucket]
-template <int BN>
-SCFA_DEVICE void interval_k_rows(const int* qidx, const int* qhash, int nv, int ki, int kh, bool excl, bool use_hash,
-                                 int& lo, int& hi) {
-  if (!use_hash) {  // real queries ascending, then pads / out-of-range (-1) at the tail
-    int nreal = 0, n = BN;
-    while (n > 0) {
-      const int h = n >> 1;
-      if (qidx[nreal + h] >= 0) { nreal += h + 1; n -= h + 1; } else { n = h; }
-    }
-    lo = excl ? upper_bound(qidx, nreal, ki) : lower_bound(qidx, nreal, ki);
-    hi = nreal;
-  } else {
-    const int a = lower_bound(qhash, nv, kh);
-    const int e = a + upper_bound(qhash + a, nv - a, kh);
-    lo = a + (excl ? upper_bound(qidx + a, e - a, ki) : lower_bound(qidx + a, e - a, ki));
-    hi = e;
-  }
-}
-
 SCFA_DEVICE uint32_t bits_below(int n) { return n <= 0 ? 0u : (n >= 32 ? 0xffffffffu : ((1u << n) - 1u)); }
 
-// 32-column visibility words of the run [lo, hi)
+// 32-column visibility words of the run [lo, hi) (tile-local columns)
 template <int NW>
 SCFA_DEVICE void run_mask(int lo, int hi, uint32_t (&w)[NW]) {
 #pragma unroll
   for (int i = 0; i < NW; ++i) w[i] = bits_below(hi - 32 * i) & ~bits_below(lo - 32 * i);
+}
+
+// ---- coalesced epilogue ------------------------------------------------------------
+// Each row thread holds one output row; written directly, every 16-byte piece of a
+// warp store lands in a different row (32 partial-line writes per instruction).  The
+// rows are instead staged in the item's stationary smem slot — free once the last
+// S MMA has run — and copied out so that each warp store covers whole rows.
+// Staging layout: row r at r * RB bytes, 16-byte chunk c at position c ^ (r & 7).
+template <int RB>
+SCFA_DEVICE void stage_put(uint8_t* stage, int r, int c, uint32_t a, uint32_t b, uint32_t cc, uint32_t d) {
+  const uint32_t addr = smem_u32(stage + r * RB + ((c ^ (r & 7)) << 4));
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(cc), "r"(d) : "memory");
+}
+
+// Copy this warp's 32 staged rows to global: row (warp*32 + i) goes to gbase +
+// off[i] bytes where off/live are held by lane i.
+template <int RB>
+SCFA_DEVICE void stage_copy_out(const uint8_t* stage, int warp, int lane, uint8_t* gbase, long long my_off,
+                                bool my_live) {
+  constexpr int CPR = RB / 16;  // 16-byte chunks per row
+  constexpr int R = 32 / CPR;   // rows per warp instruction
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < CPR; ++j) {
+    const int i = j * R + lane / CPR;
+    const int c = lane % CPR;
+    const long long off = __shfl_sync(0xffffffffu, my_off, i);
+    const int lv = __shfl_sync(0xffffffffu, my_live ? 1 : 0, i);
+    const int row = warp * 32 + i;
+    const uint32_t addr = smem_u32(stage + row * RB + ((c ^ (row & 7)) << 4));
+    uint4 v;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    if (lv) *reinterpret_cast<uint4*>(gbase + off + c * 16) = v;
+  }
+  __syncwarp();
+}
+
+template <int N>
+SCFA_DEVICE void tmem_ld_cols(uint32_t taddr, uint32_t* r) {
+#pragma unroll
+  for (int c = 0; c < N; c += 32) tmem_ld32(taddr + c, *reinterpret_cast<uint32_t(*)[32]>(r + c));
 }
 
 template <int kMode, int kD>
@@ -198,37 +189,43 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
                      const __grid_constant__ CUtensorMap tm_y0, const __grid_constant__ CUtensorMap tm_y1,
                      const AttnArgs args) {
   using C = Cfg<kMode, kD>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem[];
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* bar_s_full = bars + 0;
-  uint64_t* bar_p_full = bars + 1;
-  uint64_t* bar_x_full = bars + 2;
+  uint64_t* bar_s_free = bars + 1;
+  uint64_t* bar_p_full = bars + 2;
+  uint64_t* bar_p_free = bars + 3;
+  uint64_t* bar_acc_full = bars + 4;
+  uint64_t* bar_x_full = bars + 5;
   uint64_t* bar_x_empty = bar_x_full + C::NXS;
-  uint64_t* bar_y_full = bar_x_empty + C::NXS;
-  uint64_t* bar_y_empty = bar_y_full + C::NS;
-  uint64_t* bar_acc_full = bar_y_empty + C::NS;
-  uint64_t* bar_acc_free = bar_acc_full + C::NACC;
+  uint64_t* bar_y0_full = bar_x_empty + C::NXS;
+  uint64_t* bar_y0_empty = bar_y0_full + C::NS0;
+  uint64_t* bar_y1_full = bar_y0_empty + C::NS0;
+  uint64_t* bar_y1_empty = bar_y1_full + C::NS1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_BAR + 8 * C::N_BARS);
 
   if (threadIdx.x == 0) {
+    if (smem_u32(smem) & 1023) __trap();  // TMA SWIZZLE_128B destinations need 1024-byte alignment
     mbar_init(bar_s_full, 1);
+    mbar_init(bar_s_free, 128);
     mbar_init(bar_p_full, 128);
+    mbar_init(bar_p_free, 1);
+    mbar_init(bar_acc_full, 1);
     for (int i = 0; i < C::NXS; ++i) {
       mbar_init(bar_x_full + i, 1);
-      mbar_init(bar_x_empty + i, 1);
+      mbar_init(bar_x_empty + i, 128);  // released by the row threads after the epilogue
     }
-    for (int i = 0; i < C::NS; ++i) {
-      mbar_init(bar_y_full + i, 1);
-      mbar_init(bar_y_empty + i, 1);
+    for (int i = 0; i < C::NS0; ++i) {
+      mbar_init(bar_y0_full + i, 1);
+      mbar_init(bar_y0_empty + i, 1);
     }
-    for (int i = 0; i < C::NACC; ++i) {
-      mbar_init(bar_acc_full + i, 1);
-      mbar_init(bar_acc_free + i, 128);
+    for (int i = 0; i < C::NS1; ++i) {
+      mbar_init(bar_y1_full + i, 1);
+      mbar_init(bar_y1_empty + i, 1);
     }
     fence_barrier_init();
   }
@@ -239,13 +236,13 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 4) {
-    // ------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------ TMA producers
     if (lane == 0) {
+      // stationary tiles + y0 ring (+ per-column lse2/delta for dK/dV)
       tma_prefetch_desc(&tm_x0);
       tma_prefetch_desc(&tm_y0);
-      tma_prefetch_desc(&tm_y1);
       if (C::NX == 2) tma_prefetch_desc(&tm_x1);
-      int tg = 0, ia = 0;  // global tile counter, non-empty item counter
+      int tg = 0, ia = 0;
       for (int w = blockIdx.x; w < args.n_items; w += gridDim.x) {
         int bh, rb;
         decode_item(args, w, bh, rb);
@@ -256,31 +253,46 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
         const int xs = ia % C::NXS;
         if (ia >= C::NXS) mbar_wait(bar_x_empty + xs, ((ia / C::NXS) - 1) & 1);
         uint8_t* xb = smem + C::OFF_X + xs * C::XSLOT_BYTES;
+        SCFA_STAMP_AT(tg, 10);
         mbar_arrive_expect_tx(bar_x_full + xs, C::XSLOT_BYTES);
         for (int c = 0; c < C::DCH; ++c) {
           tma_load_3d(xb + c * C::BM * 128, &tm_x0, bar_x_full + xs, c * 64, rb * C::BM, bh);
           if (C::NX == 2) tma_load_3d(xb + C::X_BYTES + c * C::BM * 128, &tm_x1, bar_x_full + xs, c * 64, rb * C::BM, bh);
         }
         for (int t = 0; t < n; ++t, ++tg) {
-          const int st = tg % C::NS;
-          if (tg >= C::NS) mbar_wait(bar_y_empty + st, ((tg / C::NS) - 1) & 1);
+          const int st = tg % C::NS0;
+          if (tg >= C::NS0) mbar_wait(bar_y0_empty + st, ((tg / C::NS0) - 1) & 1);
           const int col0 = (lst[t] & 0x7fff) * C::BN;
-          uint8_t* stage = smem + C::OFF_STAGE + st * C::STAGE_BYTES;
-          mbar_arrive_expect_tx(bar_y_full + st, C::STAGE_BYTES);
-          for (int c = 0; c < C::DCH; ++c) {
-            tma_load_3d(stage + c * C::BN * 128, &tm_y0, bar_y_full + st, c * 64, col0, bh);
-            tma_load_3d(stage + C::Y_BYTES + c * C::BN * 128, &tm_y1, bar_y_full + st, c * 64, col0, bh);
-          }
-          uint8_t* aux = stage + 2 * C::Y_BYTES;
-          const size_t coff = static_cast<size_t>(bh) * args.T_cols_pad + col0;
-          bulk_load(aux, args.col_idx + coff, C::AUX_BYTES, bar_y_full + st);
-          bulk_load(aux + C::AUX_BYTES, args.col_hash + coff, C::AUX_BYTES, bar_y_full + st);
-          if (kMode == MODE_DKDV) {
-            bulk_load(aux + 2 * C::AUX_BYTES, args.lse2 + coff, C::AUX_BYTES, bar_y_full + st);
-            bulk_load(aux + 3 * C::AUX_BYTES, args.delta + coff, C::AUX_BYTES, bar_y_full + st);
+          uint8_t* yb = smem + C::OFF_Y0 + st * C::Y_BYTES;
+          mbar_arrive_expect_tx(bar_y0_full + st, C::Y_BYTES + C::AUX_BYTES);
+          for (int c = 0; c < C::DCH; ++c) tma_load_3d(yb + c * C::BN * 128, &tm_y0, bar_y0_full + st, c * 64, col0, bh);
+          if (C::AUX) {
+            uint8_t* aux = smem + C::OFF_AUX + st * C::AUX_BYTES;
+            const size_t coff = static_cast<size_t>(bh) * args.T_cols_pad + col0;
+            bulk_load(aux, args.lse2 + coff, C::BN * 4, bar_y0_full + st);
+            bulk_load(aux + C::BN * 4, args.delta + coff, C::BN * 4, bar_y0_full + st);
           }
         }
         ++ia;
+      }
+    } else if (lane == 1) {
+      // y1 ring
+      tma_prefetch_desc(&tm_y1);
+      int tg = 0;
+      for (int w = blockIdx.x; w < args.n_items; w += gridDim.x) {
+        int bh, rb;
+        decode_item(args, w, bh, rb);
+        const int lb = bh * args.n_row_blocks + rb;
+        const int n = args.list_count[lb];
+        const uint16_t* lst = args.list + static_cast<size_t>(lb) * args.list_stride;
+        for (int t = 0; t < n; ++t, ++tg) {
+          const int st = tg % C::NS1;
+          if (tg >= C::NS1) mbar_wait(bar_y1_empty + st, ((tg / C::NS1) - 1) & 1);
+          const int col0 = (lst[t] & 0x7fff) * C::BN;
+          uint8_t* yb = smem + C::OFF_Y1 + st * C::Y_BYTES;
+          mbar_arrive_expect_tx(bar_y1_full + st, C::Y_BYTES);
+          for (int c = 0; c < C::DCH; ++c) tma_load_3d(yb + c * C::BN * 128, &tm_y1, bar_y1_full + st, c * 64, col0, bh);
+        }
       }
     }
   } else if (warp == 5) {
@@ -288,27 +300,64 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
     if (lane == 0) {
       constexpr uint32_t idesc_s = make_idesc_bf16(128, C::BN, false, false);
       constexpr uint32_t idesc_acc = make_idesc_bf16(128, kD, false, true);
+      // the accumulate MMAs of tile `p` (P V | dS K | P^T dO + dS^T Q)
+      auto flush = [&](int ptg, bool first, bool last) {
+        const int s0 = ptg % C::NS0, s1 = ptg % C::NS1;
+        if (kMode == MODE_FWD) mbar_wait(bar_y1_full + s1, (ptg / C::NS1) & 1);  // V not needed before
+        mbar_wait(bar_p_full, ptg & 1);
+        tc_fence_after();
+        const uint32_t y0_addr = smem_u32(smem + C::OFF_Y0 + s0 * C::Y_BYTES);
+        const uint32_t y1_addr = smem_u32(smem + C::OFF_Y1 + s1 * C::Y_BYTES);
+        const uint32_t acc = tmem + C::TM_ACC;
+#pragma unroll
+        for (int k = 0; k < C::BN / 16; ++k) {
+          const uint32_t on = (!first || k > 0);
+          if (kMode == MODE_FWD) {  // O += P V
+            umma_ts(acc, tmem + C::TM_P + k * 8, make_sdesc_sw128(y1_addr + k * 2048, C::BN * 128, 1024), idesc_acc,
+                    on);
+          } else if (kMode == MODE_DQ) {  // dQ += dS K
+            umma_ts(acc, tmem + C::TM_P + k * 8, make_sdesc_sw128(y0_addr + k * 2048, C::BN * 128, 1024), idesc_acc,
+                    on);
+          } else {  // dV += P^T dO ; dK += dS^T Q
+            umma_ts(acc, tmem + C::TM_P + k * 8, make_sdesc_sw128(y1_addr + k * 2048, C::BN * 128, 1024), idesc_acc,
+                    on);
+            umma_ts(acc + kD, tmem + C::TM_P2 + k * 8, make_sdesc_sw128(y0_addr + k * 2048, C::BN * 128, 1024),
+                    idesc_acc, on);
+          }
+        }
+        if (!C::Y0_EARLY) umma_commit(bar_y0_empty + s0);
+        if (!C::Y1_EARLY) umma_commit(bar_y1_empty + s1);
+        umma_commit(bar_p_free);
+        if (last) umma_commit(bar_acc_full);
+      };
       int tg = 0, ia = 0;
+      int p_tg = -1;
+      bool p_first = false, p_last = false;
       for (int w = blockIdx.x; w < args.n_items; w += gridDim.x) {
         int bh, rb;
         decode_item(args, w, bh, rb);
         const int n = args.list_count[bh * args.n_row_blocks + rb];
         if (n == 0) continue;
         const int xs = ia % C::NXS;
-        const int ab = ia % C::NACC;
-        const uint32_t acc = tmem + C::TM_ACC + ab * C::ACC_COLS;
         const uint32_t x0_addr = smem_u32(smem + C::OFF_X + xs * C::XSLOT_BYTES);
         const uint32_t x1_addr = x0_addr + C::X_BYTES;
         mbar_wait(bar_x_full + xs, (ia / C::NXS) & 1);
-        tc_fence_after();
+        SCFA_STAMP_AT(tg, 9);
         for (int t = 0; t < n; ++t, ++tg) {
-          const int st = tg % C::NS;
+          const int s0 = tg % C::NS0, s1 = tg % C::NS1;
           SCFA_MSTAMP(6);
-          mbar_wait(bar_y_full + st, (tg / C::NS) & 1);
+          mbar_wait(bar_y0_full + s0, (tg / C::NS0) & 1);
+          if (kMode != MODE_FWD) mbar_wait(bar_y1_full + s1, (tg / C::NS1) & 1);
+          if (C::OVERLAP) {
+            if (tg > 0) mbar_wait(bar_s_free, (tg - 1) & 1);
+          } else if (p_tg >= 0) {
+            flush(p_tg, p_first, p_last);  // aliased P: the accumulate MMAs must read it first
+            p_tg = -1;
+          }
           SCFA_MSTAMP(7);
           tc_fence_after();
-          const uint32_t y0_addr = smem_u32(smem + C::OFF_STAGE + st * C::STAGE_BYTES);
-          const uint32_t y1_addr = y0_addr + C::Y_BYTES;
+          const uint32_t y0_addr = smem_u32(smem + C::OFF_Y0 + s0 * C::Y_BYTES);
+          const uint32_t y1_addr = smem_u32(smem + C::OFF_Y1 + s1 * C::Y_BYTES);
           // S = X0 . Y0^T  (and dP = X1 . Y1^T), K = head dim, both operands K-major.
 #pragma unroll
           for (int k = 0; k < kD / 16; ++k) {
@@ -327,33 +376,20 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
             }
           }
           umma_commit(bar_s_full);
-          if (t == n - 1) umma_commit(bar_x_empty + xs);  // last read of this stationary slot issued
+          if (C::Y0_EARLY) umma_commit(bar_y0_empty + s0);
+          if (C::Y1_EARLY) umma_commit(bar_y1_empty + s1);
           SCFA_MSTAMP(3);
-          mbar_wait(bar_p_full, tg & 1);
-          SCFA_MSTAMP(4);
-          if (t == 0 && ia >= C::NACC) mbar_wait(bar_acc_free + ab, ((ia / C::NACC) - 1) & 1);
-          tc_fence_after();
-          // Accumulate: A (bf16) from TMEM, B = streamed tile read MN-major, K = BN streamed rows.
-#pragma unroll
-          for (int k = 0; k < C::BN / 16; ++k) {
-            const uint32_t on = (t > 0 || k > 0);
-            if (kMode == MODE_FWD) {  // O += P V
-              umma_ts(acc, tmem + C::TM_S + k * 8, make_sdesc_sw128(y1_addr + k * 2048, C::BN * 128, 1024),
-                      idesc_acc, on);
-            } else if (kMode == MODE_DQ) {  // dQ += dS K
-              umma_ts(acc, tmem + C::TM_S + k * 8, make_sdesc_sw128(y0_addr + k * 2048, C::BN * 128, 1024),
-                      idesc_acc, on);
-            } else {  // dV += P^T dO ; dK += dS^T Q
-              umma_ts(acc, tmem + C::TM_S + k * 8, make_sdesc_sw128(y1_addr + k * 2048, C::BN * 128, 1024),
-                      idesc_acc, on);
-              umma_ts(acc + kD, tmem + C::TM_DP + k * 8, make_sdesc_sw128(y0_addr + k * 2048, C::BN * 128, 1024),
-                      idesc_acc, on);
-            }
-          }
-          umma_commit(bar_y_empty + st);
+          if (p_tg >= 0) flush(p_tg, p_first, p_last);  // overlap: tile t-1 accumulates behind S(t)
+          p_tg = tg;
+          p_first = (t == 0);
+          p_last = (t == n - 1);
           SCFA_MSTAMP(5);
         }
-        umma_commit(bar_acc_full + ab);
+        // The item's last tile accumulates now, not behind the next item's first S: the
+        // row threads' epilogue waits for it, and the next item may not be ready yet.
+        if (p_tg >= 0) flush(p_tg, p_first, p_last);
+        SCFA_STAMP_AT(p_tg, 11);
+        p_tg = -1;
         ++ia;
       }
     }
@@ -363,69 +399,88 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
     const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
     const uint32_t t_s = tmem + lane_off + C::TM_S;
     const uint32_t t_dp = tmem + lane_off + C::TM_DP;
+    const uint32_t t_p = tmem + lane_off + C::TM_P;
+    const uint32_t t_p2 = tmem + lane_off + C::TM_P2;
+    const uint32_t t_acc = tmem + lane_off + C::TM_ACC;
     const float sl = args.scale_log2;
-    const bool excl = args.exclude_self != 0;
-    const bool use_hash = args.use_hash != 0;
     const float NEG_INF = -INFINITY;
+    constexpr int NW = C::BN / 32;
     int tg = 0, ia = 0;
+    // per-item metadata is fetched one item ahead (its global-load latency hides behind
+    // the current item), and each tile's list entry one tile ahead
+    int nx_n = 0, nx_idx = 0, nx_e0 = 0;
+    int2 nx_run = make_int2(0, 0);
+    auto fetch = [&](int w) {
+      if (w >= args.n_items) return;
+      int fbh, frb;
+      decode_item(args, w, fbh, frb);
+      const int flb = fbh * args.n_row_blocks + frb;
+      const size_t foff = static_cast<size_t>(fbh) * args.T_rows_pad + frb * C::BM + r;
+      nx_n = args.list_count[flb];
+      nx_e0 = args.list[static_cast<size_t>(flb) * args.list_stride];
+      nx_idx = args.row_idx[foff];
+      nx_run = args.row_runs[foff];
+    };
+    fetch(blockIdx.x);
     for (int w = blockIdx.x; w < args.n_items; w += gridDim.x) {
       int bh, rb;
       decode_item(args, w, bh, rb);
       const int lb = bh * args.n_row_blocks + rb;
-      const int n = args.list_count[lb];
+      const int n = nx_n;
+      const int my_idx = nx_idx;
+      const int2 run = nx_run;
+      int entry_next = nx_e0;
+      fetch(w + gridDim.x);
       const uint16_t* lst = args.list + static_cast<size_t>(lb) * args.list_stride;
       const int row = rb * C::BM + r;
       const size_t roff = static_cast<size_t>(bh) * args.T_rows_pad + row;
-      const int my_idx = args.row_idx[roff];
-      const int my_hash = args.row_hash[roff];
-      const int ab = ia % C::NACC;
-      const uint32_t t_acc = tmem + lane_off + C::TM_ACC + ab * C::ACC_COLS;
       size_t orow = 0;
       const bool live = out_row(args, bh, row, my_idx, orow);
 
       if (kMode == MODE_FWD) {
-        const float mask_val = sl >= 0.f ? NEG_INF : INFINITY;
+        const bool neg = sl < 0.f;  // a negative scale turns the row max into a row min
+        const float mask_val = neg ? INFINITY : NEG_INF;
         float m_run = NEG_INF;   // log2-domain max used for exponentiation (lags by < 8)
         float m_true = NEG_INF;  // exact running max of scaled logits (log2 domain)
         float l_run = 0.f;
         for (int t = 0; t < n; ++t, ++tg) {
-          const int entry = lst[t];
+          const int entry = entry_next;
+          if (t + 1 < n) entry_next = lst[t + 1];
           const bool full = (entry & 0x8000) != 0;
-          const int st = tg % C::NS;
-          const int* kidx = reinterpret_cast<const int*>(smem + C::OFF_STAGE + st * C::STAGE_BYTES + 2 * C::Y_BYTES);
-          const int* khash = kidx + C::BN;
-          constexpr int NW = C::BN / 32;
-          uint32_t vis[NW];
+          const int col0 = (entry & 0x7fff) * C::BN;
           SCFA_STAMP(0);
           mbar_wait(bar_s_full, tg & 1);
           SCFA_STAMP(1);
           tc_fence_after();
-          uint32_t raw[C::BN];
+          // S is consumed in two 64-column halves to bound register pressure: both halves
+          // are read for the row max, half 1 is exponentiated from registers, half 0 is
+          // re-read (S stays valid until s_free) and exponentiated last.
+          constexpr int HB = C::BN / 2;
+          uint32_t vis[NW];
+          if (!full) run_mask<NW>(run.x - col0, run.y - col0, vis);
+          float x[HB];
+          float ext[2];
 #pragma unroll
-          for (int c = 0; c < C::BN; c += 32) tmem_ld32(t_s + c, *reinterpret_cast<uint32_t(*)[32]>(&raw[c]));
-          if (full) {
+          for (int hf = 0; hf < 2; ++hf) {
+            tmem_ld_cols<HB>(t_s + hf * HB, reinterpret_cast<uint32_t*>(x));
+            tmem_wait_ld();
+            if (!full) {
 #pragma unroll
-            for (int i = 0; i < NW; ++i) vis[i] = 0xffffffffu;
-          } else {
-            const int nv = min(C::BN, args.T_cols - (entry & 0x7fff) * C::BN);
-            int lo, hi;
-            interval_q_rows<C::BN>(kidx, khash, nv, my_idx, my_hash, excl, use_hash, lo, hi);
-            run_mask<NW>(lo, hi, vis);
+              for (int c = 0; c < HB; ++c) x[c] = ((vis[2 * hf + (c >> 5)] >> (c & 31)) & 1u) ? x[c] : mask_val;
+            }
+            float mq[4] = {mask_val, mask_val, mask_val, mask_val};
+            if (!neg) {
+#pragma unroll
+              for (int c = 0; c < HB; c += 2) mq[(c >> 1) & 3] = max3(mq[(c >> 1) & 3], x[c], x[c + 1]);
+              ext[hf] = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
+            } else {
+#pragma unroll
+              for (int c = 0; c < HB; c += 2) mq[(c >> 1) & 3] = min3(mq[(c >> 1) & 3], x[c], x[c + 1]);
+              ext[hf] = fminf(fminf(mq[0], mq[1]), fminf(mq[2], mq[3]));
+            }
+            asm volatile("" ::"f"(ext[hf]));  // pin: this half's max is done before the next tcgen05.ld
           }
-          tmem_wait_ld();
-          float s[C::BN];
-#pragma unroll
-          for (int c = 0; c < C::BN; ++c) s[c] = ((vis[c >> 5] >> (c & 31)) & 1u) ? __uint_as_float(raw[c]) : mask_val;
-          float mq[4] = {mask_val, mask_val, mask_val, mask_val};
-          if (sl >= 0.f) {
-#pragma unroll
-            for (int c = 0; c < C::BN; ++c) mq[c & 3] = fmaxf(mq[c & 3], s[c]);
-          } else {
-#pragma unroll
-            for (int c = 0; c < C::BN; ++c) mq[c & 3] = fminf(mq[c & 3], s[c]);
-          }
-          const float mx = (sl >= 0.f) ? fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]))
-                                       : fminf(fminf(mq[0], mq[1]), fminf(mq[2], mq[3]));
+          const float mx = neg ? fminf(ext[0], ext[1]) : fmaxf(ext[0], ext[1]);
           const float m_tile = mx * sl;  // -inf when the whole row is masked in this tile
           m_true = fmaxf(m_true, m_tile);
           // Rebase to a new max (log2 units) only when the max grows by >= 2^8: P stays
@@ -437,36 +492,62 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
             l_run *= alpha;
             m_run = m_tile;
           }
-          const float m_use = (m_run == NEG_INF) ? 0.f : m_run;
-          float ls[4] = {0.f, 0.f, 0.f, 0.f};
+          const float nm = (m_run == NEG_INF) ? 0.f : -m_run;
+          float la[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-          for (int c = 0; c < C::BN; c += 32) {
-            uint32_t pk[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const float p0 = ex2(fmaf(s[c + 2 * i], sl, -m_use));
-              const float p1 = ex2(fmaf(s[c + 2 * i + 1], sl, -m_use));
-              ls[(2 * i) & 3] += p0;
-              ls[(2 * i + 1) & 3] += p1;
-              pk[i] = pack_bf16(p0, p1);
-            }
-            tmem_st16(t_s + c / 2, pk);
-          }
-          l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
-          // tcgen05.ld/st are warp-collective: the whole warp rescales when any row must
-          // (alpha == 1 for the others, an exact no-op).  The previous P.V into this
-          // accumulator has completed: s_full of this tile was committed after it.
-          if (__any_sync(0xffffffffu, rebase && t > 0)) {
-#pragma unroll 1
-            for (int c = 0; c < kD; c += 32) {
-              uint32_t v[32];
-              tmem_ld32(t_acc + c, v);
+          for (int step = 0; step < 2; ++step) {
+            const int hf = 1 - step;  // half 1 is still in registers
+            if (step == 1) {
+              tmem_ld_cols<HB>(t_s + hf * HB, reinterpret_cast<uint32_t*>(x));
               tmem_wait_ld();
+              if (C::OVERLAP) {
+                tc_fence_before();
+                mbar_arrive(bar_s_free);  // S fully read: the next tile's S may overwrite it
+              }
+              if (!full) {
 #pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
-              tmem_st32(t_acc + c, v);
+                for (int c = 0; c < HB; ++c) x[c] = ((vis[2 * hf + (c >> 5)] >> (c & 31)) & 1u) ? x[c] : mask_val;
+              }
             }
+            uint32_t pk[HB / 2];
+#pragma unroll
+            for (int c = 0; c < HB; c += 2) {
+              float a0, a1;
+              fma2(a0, a1, x[c], x[c + 1], sl, sl, nm, nm);
+              a0 = ex2(a0);
+              a1 = ex2(a1);
+              const int q = (c >> 1) & 1;
+              add2(la[2 * q], la[2 * q + 1], la[2 * q], la[2 * q + 1], a0, a1);
+              pk[c >> 1] = pack_bf16(a0, a1);
+            }
+            if (step == 0) {
+              // P's columns and O are read by the previous tile's accumulate MMAs.
+              if (tg > 0) mbar_wait(bar_p_free, (tg - 1) & 1);
+              tc_fence_after();
+              // tcgen05.ld/st are warp-collective: the whole warp rescales when any row
+              // must (alpha == 1 for the others, an exact no-op).
+              if (__any_sync(0xffffffffu, rebase && t > 0)) {
+#pragma unroll 1
+                for (int c = 0; c < kD; c += 32) {
+                  uint32_t v[32];
+                  tmem_ld32(t_acc + c, v);
+                  tmem_wait_ld();
+#pragma unroll
+                  for (int i = 0; i < 32; i += 2) {
+                    float o0, o1;
+                    mul2(o0, o1, __uint_as_float(v[i]), __uint_as_float(v[i + 1]), alpha, alpha);
+                    v[i] = __float_as_uint(o0);
+                    v[i + 1] = __float_as_uint(o1);
+                  }
+                  tmem_st32(t_acc + c, v);
+                }
+              }
+            }
+#pragma unroll
+            for (int c = 0; c < HB / 2; c += 16)
+              tmem_st16(t_p + hf * (HB / 2) + c, *reinterpret_cast<uint32_t(*)[16]>(&pk[c]));
           }
+          l_run += (la[0] + la[1]) + (la[2] + la[3]);
           tmem_wait_st();
           tc_fence_before();
           mbar_arrive(bar_p_full);
@@ -474,117 +555,129 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
         }
         // ---------------- epilogue: O / l (fused scatter), M, L, lse2
         if (n > 0) {
-          mbar_wait(bar_acc_full + ab, (ia / C::NACC) & 1);
+          mbar_wait(bar_acc_full, ia & 1);
           tc_fence_after();
+          if (threadIdx.x == 0) { SCFA_STAMP_AT(tg - 1, 4) }
         }
         const float inv_l = (l_run > 0.f) ? 1.f / l_run : 0.f;
-        __nv_bfloat16* op = args.out_o + orow * kD;
+        if (n > 0) {
+          constexpr int RB = kD * 2;  // bf16 output row
+          uint8_t* stage = smem + C::OFF_X + (ia % C::NXS) * C::XSLOT_BYTES;
 #pragma unroll
-        for (int c = 0; c < kD; c += 32) {
-          uint32_t v[32];
-          if (n > 0) {  // warp-uniform; every thread of the warp loads (warp-collective)
+          for (int c = 0; c < kD; c += 32) {
+            uint32_t v[32];
             tmem_ld32(t_acc + c, v);
             tmem_wait_ld();
-          } else {
+            uint32_t w[16];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = 0u;
+            for (int i = 0; i < 16; ++i)
+              w[i] = pack_bf16(__uint_as_float(v[2 * i]) * inv_l, __uint_as_float(v[2 * i + 1]) * inv_l);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) stage_put<RB>(stage, r, c / 8 + i, w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
           }
-          uint4 o4[4];
-          uint32_t* ow = reinterpret_cast<uint32_t*>(o4);
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            ow[i] = pack_bf16(__uint_as_float(v[2 * i]) * inv_l, __uint_as_float(v[2 * i + 1]) * inv_l);
-          if (live) {
-            uint4* dst = reinterpret_cast<uint4*>(op + c);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) dst[i] = o4[i];
-          }
-        }
-        if (n > 0) {
-          tc_fence_before();
-          mbar_arrive(bar_acc_free + ab);
+          stage_copy_out<RB>(stage, warp, lane, reinterpret_cast<uint8_t*>(args.out_o),
+                             static_cast<long long>(orow) * RB, live);
+          fence_proxy_async_smem();  // the next TMA load into this slot comes after these accesses
+          mbar_arrive(bar_x_empty + (ia % C::NXS));
+          tc_fence_before();  // O read before the next item's first accumulate (ordered by p_full)
           ++ia;
+        } else if (live) {
+          uint4* dst = reinterpret_cast<uint4*>(args.out_o + orow * kD);
+#pragma unroll
+          for (int i = 0; i < kD / 8; ++i) dst[i] = make_uint4(0u, 0u, 0u, 0u);
         }
         if (row < args.T_rows) {
           const size_t so = static_cast<size_t>(bh) * args.T_rows + row;
           const float LN2 = 0.6931471805599453f;
           const bool dead = !(l_run > 0.f);
           const float m_use = (m_run == NEG_INF) ? 0.f : m_run;
-          args.out0[so] = dead ? NEG_INF : m_true * LN2;           // M
+          args.out0[so] = dead ? NEG_INF : m_true * LN2;             // M
           args.out1[so] = dead ? 0.f : l_run * ex2(m_use - m_true);  // L relative to M
           args.out_lse2[roff] = dead ? INFINITY : (m_use + __log2f(l_run));
         }
+        if (threadIdx.x == 0) { SCFA_STAMP_AT(tg - 1, 8) }
       } else {
         // ---------------- backward passes: P and dS recomputed from (lse2, delta)
-        float my_lse = 0.f, my_delta = 0.f;
+        float my_nlse = 0.f, my_ndelta = 0.f;
         if (kMode == MODE_DQ) {
-          my_lse = args.lse2[roff];
-          my_delta = args.delta[roff];
+          my_nlse = -args.lse2[roff];
+          my_ndelta = -args.delta[roff];
         }
         for (int t = 0; t < n; ++t, ++tg) {
-          const int entry = lst[t];
+          const int entry = entry_next;
+          if (t + 1 < n) entry_next = lst[t + 1];
           const bool full = (entry & 0x8000) != 0;
-          const int st = tg % C::NS;
-          const int* cidx = reinterpret_cast<const int*>(smem + C::OFF_STAGE + st * C::STAGE_BYTES + 2 * C::Y_BYTES);
-          const int* chash = cidx + C::BN;
-          const float* clse = reinterpret_cast<const float*>(chash + C::BN);
-          const float* cdelta = clse + C::BN;
-          constexpr int NW = C::BN / 32;
-          uint32_t vis[NW];
+          const int col0 = (entry & 0x7fff) * C::BN;
           SCFA_STAMP(0);
           mbar_wait(bar_s_full, tg & 1);
           SCFA_STAMP(1);
           tc_fence_after();
+          const float* clse = nullptr;
+          const float* cdelta = nullptr;
+          if (kMode == MODE_DKDV) {
+            const int s0 = tg % C::NS0;
+            mbar_wait(bar_y0_full + s0, (tg / C::NS0) & 1);  // acquire the per-column lse/delta
+            clse = reinterpret_cast<const float*>(smem + C::OFF_AUX + s0 * C::AUX_BYTES);
+            cdelta = clse + C::BN;
+          }
+          uint32_t vis[NW];
           if (full) {
 #pragma unroll
             for (int i = 0; i < NW; ++i) vis[i] = 0xffffffffu;
           } else {
-            const int nv = min(C::BN, args.T_cols - (entry & 0x7fff) * C::BN);
-            int lo, hi;
-            if (kMode == MODE_DQ)
-              interval_q_rows<C::BN>(cidx, chash, nv, my_idx, my_hash, excl, use_hash, lo, hi);
-            else
-              interval_k_rows<C::BN>(cidx, chash, nv, my_idx, my_hash, excl, use_hash, lo, hi);
-            run_mask<NW>(lo, hi, vis);
+            run_mask<NW>(run.x - col0, run.y - col0, vis);
           }
+          // 32-column chunks (bounded register pressure): read S and dP, compute P (and
+          // dS), store; the first store waits for the previous tile's accumulate MMAs,
+          // which read these columns.  (Aliased layout: chunk k's P/dS land in columns
+          // [16k, 16k+16) of S/dP, below the chunks still to be read.)
 #pragma unroll
-          for (int c = 0; c < C::BN; c += 32) {
-            uint32_t sv[32], dv[32];
-            tmem_ld32(t_s + c, sv);
-            tmem_ld32(t_dp + c, dv);
+          for (int cc = 0; cc < C::BN; cc += 32) {
+            float sv[32], dv[32];
+            tmem_ld32(t_s + cc, *reinterpret_cast<uint32_t(*)[32]>(sv));
+            tmem_ld32(t_dp + cc, *reinterpret_cast<uint32_t(*)[32]>(dv));
             tmem_wait_ld();
-            const uint32_t wv = vis[c >> 5];
+            if (C::OVERLAP && cc + 32 == C::BN) {
+              tc_fence_before();
+              mbar_arrive(bar_s_free);
+            }
             uint32_t pk_p[16], pk_ds[16];
 #pragma unroll
-            for (int i = 0; i < 32; i += 4) {
-              float lse4[4], del4[4];
+            for (int c = cc; c < cc + 32; c += 4) {
+              float nl[4], nd[4];
               if (kMode == MODE_DQ) {
 #pragma unroll
-                for (int e = 0; e < 4; ++e) { lse4[e] = my_lse; del4[e] = my_delta; }
+                for (int e = 0; e < 4; ++e) { nl[e] = my_nlse; nd[e] = my_ndelta; }
               } else {
-                const float4 a = *reinterpret_cast<const float4*>(clse + c + i);
-                const float4 b = *reinterpret_cast<const float4*>(cdelta + c + i);
-                lse4[0] = a.x; lse4[1] = a.y; lse4[2] = a.z; lse4[3] = a.w;
-                del4[0] = b.x; del4[1] = b.y; del4[2] = b.z; del4[3] = b.w;
+                const float4 a = *reinterpret_cast<const float4*>(clse + c);
+                const float4 b = *reinterpret_cast<const float4*>(cdelta + c);
+                nl[0] = -a.x; nl[1] = -a.y; nl[2] = -a.z; nl[3] = -a.w;
+                nd[0] = -b.x; nd[1] = -b.y; nd[2] = -b.z; nd[3] = -b.w;
               }
-              float pp[4], dd[4];
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                float p = ex2(fmaf(__uint_as_float(sv[i + e]), sl, -lse4[e]));
-                p = ((wv >> (i + e)) & 1u) ? p : 0.f;
-                pp[e] = p;
-                dd[e] = p * (__uint_as_float(dv[i + e]) - del4[e]);
+              for (int e = 0; e < 4; e += 2) {
+                float p0, p1, d0, d1;
+                fma2(p0, p1, sv[c - cc + e], sv[c - cc + e + 1], sl, sl, nl[e], nl[e + 1]);
+                p0 = ex2(p0);
+                p1 = ex2(p1);
+                const uint32_t wv = vis[(c + e) >> 5];
+                p0 = ((wv >> ((c + e) & 31)) & 1u) ? p0 : 0.f;
+                p1 = ((wv >> ((c + e + 1) & 31)) & 1u) ? p1 : 0.f;
+                add2(d0, d1, dv[c - cc + e], dv[c - cc + e + 1], nd[e], nd[e + 1]);
+                mul2(d0, d1, d0, d1, p0, p1);
+                pk_p[(c - cc + e) >> 1] = pack_bf16(p0, p1);
+                pk_ds[(c - cc + e) >> 1] = pack_bf16(d0, d1);
               }
-              pk_p[i / 2] = pack_bf16(pp[0], pp[1]);
-              pk_p[i / 2 + 1] = pack_bf16(pp[2], pp[3]);
-              pk_ds[i / 2] = pack_bf16(dd[0], dd[1]);
-              pk_ds[i / 2 + 1] = pack_bf16(dd[2], dd[3]);
+            }
+            if (cc == 0) {
+              if (tg > 0) mbar_wait(bar_p_free, (tg - 1) & 1);
+              tc_fence_after();
             }
             if (kMode == MODE_DQ) {
-              tmem_st16(t_s + c / 2, pk_ds);
+              tmem_st16(t_p + cc / 2, pk_ds);
             } else {
-              tmem_st16(t_s + c / 2, pk_p);
-              tmem_st16(t_dp + c / 2, pk_ds);
+              tmem_st16(t_p + cc / 2, pk_p);
+              tmem_st16(t_p2 + cc / 2, pk_ds);
             }
           }
           tmem_wait_st();
@@ -593,38 +686,45 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
           SCFA_STAMP(2);
         }
         if (n > 0) {
-          mbar_wait(bar_acc_full + ab, (ia / C::NACC) & 1);
+          mbar_wait(bar_acc_full, ia & 1);
           tc_fence_after();
+          if (threadIdx.x == 0) { SCFA_STAMP_AT(tg - 1, 4) }
         }
         const int n_out = (kMode == MODE_DKDV) ? 2 : 1;
+        constexpr int RB = kD * 4;  // fp32 gradient row
+        uint8_t* stage = smem + C::OFF_X + (ia % C::NXS) * C::XSLOT_BYTES;
 #pragma unroll
         for (int o = 0; o < n_out; ++o) {
           // DQ: out0 = scale * dQ.  DKDV: out0 = scale * dK (acc + D), out1 = dV (acc).
           const int col = (kMode == MODE_DKDV && o == 0) ? kD : 0;
           const float mul = (o == 0) ? args.scale : 1.f;
-          float* dst = ((o == 0) ? args.out0 : args.out1) + orow * kD;
+          float* dst = (o == 0) ? args.out0 : args.out1;
+          if (n > 0) {
 #pragma unroll
-          for (int c = 0; c < kD; c += 32) {
-            uint32_t v[32];
-            if (n > 0) {
+            for (int c = 0; c < kD; c += 32) {
+              uint32_t v[32];
               tmem_ld32(t_acc + col + c, v);
               tmem_wait_ld();
-            } else {
 #pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] = 0u;
-            }
-            if (live) {
-              float4* d4 = reinterpret_cast<float4*>(dst + c);
+              for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * mul);
 #pragma unroll
-              for (int i = 0; i < 8; ++i)
-                d4[i] = make_float4(__uint_as_float(v[4 * i]) * mul, __uint_as_float(v[4 * i + 1]) * mul,
-                                    __uint_as_float(v[4 * i + 2]) * mul, __uint_as_float(v[4 * i + 3]) * mul);
+              for (int i = 0; i < 8; ++i) stage_put<RB>(stage, r, c / 4 + i, v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
             }
+            stage_copy_out<RB>(stage, warp, lane, reinterpret_cast<uint8_t*>(dst), static_cast<long long>(orow) * RB,
+                               live);
+          } else if (live) {
+            float4* d4 = reinterpret_cast<float4*>(dst + orow * kD);
+#pragma unroll
+            for (int i = 0; i < kD / 4; ++i) d4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
           }
         }
         if (n > 0) {
+          fence_proxy_async_smem();
+          mbar_arrive(bar_x_empty + (ia % C::NXS));
+        }
+        if (threadIdx.x == 0) { SCFA_STAMP_AT(tg - 1, 8) }
+        if (n > 0) {
           tc_fence_before();
-          mbar_arrive(bar_acc_free + ab);
           ++ia;
         }
       }
@@ -651,12 +751,17 @@ static int make_map(CUtensorMap* map, const void* base, int BH, int T, int D, in
 
 static long long* g_dbg_buf = nullptr;
 static int g_dbg_tiles = 0;
+static int g_per_sm[3][2] = {};  // resident CTAs per SM chosen per (mode, D); 0 = not launched yet
 
 static int sm_count() {
-  int dev = 0, n = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  return n > 0 ? n : 148;
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
 }
 
 template <int kMode, int kD>
@@ -679,9 +784,7 @@ static int launch_mode(const AttnLaunch& L, cudaStream_t stream) {
   a.T_out = L.T_out;
   a.out_boundary = L.out_boundary;
   a.row_idx = L.row_idx;
-  a.row_hash = L.row_hash;
-  a.col_idx = L.col_idx;
-  a.col_hash = L.col_hash;
+  a.row_runs = reinterpret_cast<const int2*>(L.row_runs);
   a.lse2 = L.lse2;
   a.delta = L.delta;
   a.list = L.list;
@@ -695,16 +798,21 @@ static int launch_mode(const AttnLaunch& L, cudaStream_t stream) {
   a.out_lse2 = L.out_lse2;
   a.scale_log2 = L.scale * 1.4426950408889634f;
   a.scale = L.scale;
-  a.exclude_self = L.exclude_self;
-  a.use_hash = L.use_hash;
   a.dbg = g_dbg_buf;
   a.dbg_tiles = g_dbg_tiles;
   auto kern = scfa_attn_kernel<kMode, kD>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES) != cudaSuccess)
-    return SCFA_ERR_CUDA;
+  static int per_sm = 0;  // resident CTAs per SM: 2 at D = 64 (TMEM 256 cols each) when shared memory allows
+  if (per_sm == 0) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES) != cudaSuccess)
+      return SCFA_ERR_CUDA;
+    int dev = 0, sm_smem = 0, reserved = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+    per_sm = (C::TM_COLS <= 256 && 2 * (C::SMEM_BYTES + reserved) <= sm_smem) ? 2 : 1;
+    g_per_sm[kMode][kD == 64 ? 0 : 1] = per_sm;
+  }
   if (a.n_items == 0) return SCFA_OK;
-  // persistent: as many CTAs as fit (2 per SM when smem and TMEM allow)
-  const int per_sm = (2 * C::SMEM_BYTES <= 227 * 1024 && C::TM_COLS <= 256) ? 2 : 1;
   int grid = sm_count() * per_sm;
   if (grid > a.n_items) grid = a.n_items;
   kern<<<grid, 192, C::SMEM_BYTES, stream>>>(mx0, mx1, my0, my1, a);
@@ -734,4 +842,9 @@ void set_debug_buffer(long long* p, int tiles) {
 extern "C" int scfa_debug_timing(void* buf, int64_t tiles_per_cta) {
   scfa::set_debug_buffer(static_cast<long long*>(buf), static_cast<int>(tiles_per_cta));
   return 0;
+}
+
+extern "C" int scfa_debug_ctas_per_sm(int mode, int64_t D) {
+  if (mode < 0 || mode > 2 || (D != 64 && D != 128)) return -1;
+  return scfa::g_per_sm[mode][D == 64 ? 0 : 1];
 }

@@ -74,15 +74,14 @@ static int check_attn_args(int64_t BH, int64_t T_q, int64_t T_kv, int64_t D, int
 
 using namespace scfa;
 
-extern "C" int scfa_abi_version(void) { return 1; }
+extern "C" int scfa_abi_version(void) { return 2; }
 
 extern "C" const char* scfa_last_error(void) { return g_err; }
 
 extern "C" int scfa_attn_fwd(const void* q, const void* k, const void* v, int64_t BH, int64_t T_q, int64_t T_kv,
-                             int64_t D, const int32_t* q_idx, const int32_t* q_hash, const int32_t* k_idx,
-                             const int32_t* k_hash, int64_t Tq_pad, int64_t Tkv_pad, const uint16_t* list,
-                             const int32_t* list_count, int64_t list_stride, float scale, int flags, int64_t H,
-                             int64_t T_out, int out_boundary, void* o, float* m, float* l, float* lse2,
+                             int64_t D, const int32_t* q_idx, const int32_t* q_runs, int64_t Tq_pad, int64_t Tkv_pad,
+                             const uint16_t* list, const int32_t* list_count, int64_t list_stride, float scale,
+                             int64_t H, int64_t T_out, int out_boundary, void* o, float* m, float* l, float* lse2,
                              void* stream) {
   int rc = check_attn_args(BH, T_q, T_kv, D, Tq_pad, Tkv_pad, q, k, v);
   if (rc) return rc;
@@ -106,9 +105,7 @@ extern "C" int scfa_attn_fwd(const void* q, const void* k, const void* v, int64_
   L.y1 = T_kv > 0 ? v : q;
   if (T_kv == 0) L.T_cols = static_cast<int>(T_q);
   L.row_idx = q_idx;
-  L.row_hash = (flags & SCFA_FLAG_HASH) ? q_hash : q_idx;
-  L.col_idx = k_idx;
-  L.col_hash = (flags & SCFA_FLAG_HASH) ? k_hash : k_idx;
+  L.row_runs = q_runs;
   L.list = list;
   L.list_count = list_count;
   L.list_stride = static_cast<int>(list_stride);
@@ -118,92 +115,86 @@ extern "C" int scfa_attn_fwd(const void* q, const void* k, const void* v, int64_
   L.out1 = l;
   L.out_lse2 = lse2;
   L.scale = scale;
-  L.exclude_self = (flags & SCFA_FLAG_EXCLUDE_SELF) ? 1 : 0;
-  L.use_hash = (flags & SCFA_FLAG_HASH) ? 1 : 0;
   rc = launch_attention(L, static_cast<cudaStream_t>(stream));
   if (rc && !g_err[0]) set_error("attention forward launch failed: %s", cudaGetErrorString(cudaGetLastError()));
   return rc;
 }
 
-static int bwd_common(int mode, const void* q, const void* k, const void* v, const void* d_out, int64_t BH,
-                      int64_t T_q, int64_t T_kv, int64_t D, const int32_t* q_idx, const int32_t* q_hash,
-                      const int32_t* k_idx, const int32_t* k_hash, int64_t Tq_pad, int64_t Tkv_pad, const float* lse2,
-                      const float* delta, const uint16_t* list, const int32_t* list_count, int64_t list_stride,
-                      float scale, int flags, int64_t H, int64_t T_out, int out_boundary, float* out0,
-                      float* out1, void* stream) {
+extern "C" int scfa_attn_bwd_dq(const void* q, const void* k, const void* v, const void* d_out, int64_t BH,
+                                int64_t T_q, int64_t T_kv, int64_t D, const int32_t* q_idx, const int32_t* q_runs,
+                                int64_t Tq_pad, int64_t Tkv_pad, const float* lse2, const float* delta,
+                                const uint16_t* list, const int32_t* list_count, int64_t list_stride, float scale,
+                                int64_t H, int64_t T_out, int out_boundary, float* dq, void* stream) {
   int rc = check_attn_args(BH, T_q, T_kv, D, Tq_pad, Tkv_pad, q, k, v);
   if (rc) return rc;
-  const bool hash = (flags & SCFA_FLAG_HASH) != 0;
+  if (BH == 0 || T_q == 0) return SCFA_OK;
   AttnLaunch L{};
-  L.mode = mode;
+  L.mode = 1;  // rows = queries
   L.D = static_cast<int>(D);
   L.BH = static_cast<int>(BH);
   L.H = static_cast<int>(H);
   L.T_out = static_cast<int>(T_out);
   L.out_boundary = out_boundary;
   L.scale = scale;
-  L.exclude_self = (flags & SCFA_FLAG_EXCLUDE_SELF) ? 1 : 0;
-  L.use_hash = hash ? 1 : 0;
   L.lse2 = lse2;
   L.delta = delta;
   L.list = list;
   L.list_count = list_count;
   L.list_stride = static_cast<int>(list_stride);
-  L.out0 = out0;
-  L.out1 = out1;
-  if (mode == 1) {  // dQ: rows = queries
-    if (BH == 0 || T_q == 0) return SCFA_OK;
-    L.T_rows = static_cast<int>(T_q);
-    L.T_cols = static_cast<int>(T_kv > 0 ? T_kv : 1);
-    L.T_rows_pad = static_cast<int>(Tq_pad);
-    L.T_cols_pad = static_cast<int>(Tkv_pad);
-    L.x0 = q;
-    L.x1 = d_out;
-    L.y0 = T_kv > 0 ? k : q;
-    L.y1 = T_kv > 0 ? v : q;
-    if (T_kv == 0) L.T_cols = static_cast<int>(T_q);
-    L.row_idx = q_idx;
-    L.row_hash = hash ? q_hash : q_idx;
-    L.col_idx = k_idx;
-    L.col_hash = hash ? k_hash : k_idx;
-  } else {  // dK/dV: rows = keys
-    if (BH == 0 || T_kv == 0) return SCFA_OK;
-    L.T_rows = static_cast<int>(T_kv);
-    L.T_cols = static_cast<int>(T_q > 0 ? T_q : 1);
-    L.T_rows_pad = static_cast<int>(Tkv_pad);
-    L.T_cols_pad = static_cast<int>(Tq_pad);
-    L.x0 = k;
-    L.x1 = v;
-    L.y0 = T_q > 0 ? q : k;
-    L.y1 = T_q > 0 ? d_out : k;
-    if (T_q == 0) L.T_cols = static_cast<int>(T_kv);
-    L.row_idx = k_idx;
-    L.row_hash = hash ? k_hash : k_idx;
-    L.col_idx = q_idx;
-    L.col_hash = hash ? q_hash : q_idx;
-  }
+  L.out0 = dq;
+  L.T_rows = static_cast<int>(T_q);
+  L.T_cols = static_cast<int>(T_kv > 0 ? T_kv : 1);
+  L.T_rows_pad = static_cast<int>(Tq_pad);
+  L.T_cols_pad = static_cast<int>(Tkv_pad);
+  L.x0 = q;
+  L.x1 = d_out;
+  L.y0 = T_kv > 0 ? k : q;
+  L.y1 = T_kv > 0 ? v : q;
+  if (T_kv == 0) L.T_cols = static_cast<int>(T_q);
+  L.row_idx = q_idx;
+  L.row_runs = q_runs;
   L.n_row_blocks = (L.T_rows + 127) / 128;
   rc = launch_attention(L, static_cast<cudaStream_t>(stream));
-  if (rc && !g_err[0]) set_error("attention backward launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+  if (rc && !g_err[0]) set_error("attention backward (dQ) launch failed: %s", cudaGetErrorString(cudaGetLastError()));
   return rc;
 }
 
-extern "C" int scfa_attn_bwd_dq(const void* q, const void* k, const void* v, const void* d_out, int64_t BH,
-                                int64_t T_q, int64_t T_kv, int64_t D, const int32_t* q_idx, const int32_t* q_hash,
-                                const int32_t* k_idx, const int32_t* k_hash, int64_t Tq_pad, int64_t Tkv_pad,
-                                const float* lse2, const float* delta, const uint16_t* list,
-                                const int32_t* list_count, int64_t list_stride, float scale, int flags, int64_t H,
-                                int64_t T_out, int out_boundary, float* dq, void* stream) {
-  return bwd_common(1, q, k, v, d_out, BH, T_q, T_kv, D, q_idx, q_hash, k_idx, k_hash, Tq_pad, Tkv_pad, lse2, delta,
-                    list, list_count, list_stride, scale, flags, H, T_out, out_boundary, dq, nullptr, stream);
-}
-
 extern "C" int scfa_attn_bwd_dkdv(const void* q, const void* k, const void* v, const void* d_out, int64_t BH,
-                                  int64_t T_q, int64_t T_kv, int64_t D, const int32_t* q_idx, const int32_t* q_hash,
-                                  const int32_t* k_idx, const int32_t* k_hash, int64_t Tq_pad, int64_t Tkv_pad,
-                                  const float* lse2, const float* delta, const uint16_t* list,
-                                  const int32_t* list_count, int64_t list_stride, float scale, int flags, int64_t H,
-                                  int64_t T_out, int out_boundary, float* dk, float* dv, void* stream) {
-  return bwd_common(2, q, k, v, d_out, BH, T_q, T_kv, D, q_idx, q_hash, k_idx, k_hash, Tq_pad, Tkv_pad, lse2, delta,
-                    list, list_count, list_stride, scale, flags, H, T_out, out_boundary, dk, dv, stream);
+                                  int64_t T_q, int64_t T_kv, int64_t D, const int32_t* k_idx, const int32_t* k_runs,
+                                  int64_t Tq_pad, int64_t Tkv_pad, const float* lse2, const float* delta,
+                                  const uint16_t* list, const int32_t* list_count, int64_t list_stride, float scale,
+                                  int64_t H, int64_t T_out, int out_boundary, float* dk, float* dv, void* stream) {
+  int rc = check_attn_args(BH, T_q, T_kv, D, Tq_pad, Tkv_pad, q, k, v);
+  if (rc) return rc;
+  if (BH == 0 || T_kv == 0) return SCFA_OK;
+  AttnLaunch L{};
+  L.mode = 2;  // rows = keys
+  L.D = static_cast<int>(D);
+  L.BH = static_cast<int>(BH);
+  L.H = static_cast<int>(H);
+  L.T_out = static_cast<int>(T_out);
+  L.out_boundary = out_boundary;
+  L.scale = scale;
+  L.lse2 = lse2;
+  L.delta = delta;
+  L.list = list;
+  L.list_count = list_count;
+  L.list_stride = static_cast<int>(list_stride);
+  L.out0 = dk;
+  L.out1 = dv;
+  L.T_rows = static_cast<int>(T_kv);
+  L.T_cols = static_cast<int>(T_q > 0 ? T_q : 1);
+  L.T_rows_pad = static_cast<int>(Tkv_pad);
+  L.T_cols_pad = static_cast<int>(Tq_pad);
+  L.x0 = k;
+  L.x1 = v;
+  L.y0 = T_q > 0 ? q : k;
+  L.y1 = T_q > 0 ? d_out : k;
+  if (T_q == 0) L.T_cols = static_cast<int>(T_kv);
+  L.row_idx = k_idx;
+  L.row_runs = k_runs;
+  L.n_row_blocks = (L.T_rows + 127) / 128;
+  rc = launch_attention(L, static_cast<cudaStream_t>(stream));
+  if (rc && !g_err[0]) set_error("attention backward (dK/dV) launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+  return rc;
 }

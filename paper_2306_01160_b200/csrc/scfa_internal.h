@@ -28,10 +28,8 @@ struct AttnLaunch {
   const void* x1;
   const void* y0;
   const void* y1;
-  const int* row_idx;
-  const int* row_hash;
-  const int* col_idx;
-  const int* col_hash;
+  const int* row_idx;   // original position per stationary row slot (output routing)
+  const int* row_runs;  // (BH, T_rows_pad) int2: visible streamed-slot run [lo, hi)
   const float* lse2;
   const float* delta;
   const uint16_t* list;
@@ -43,8 +41,6 @@ struct AttnLaunch {
   float* out1;
   float* out_lse2;
   float scale;
-  int exclude_self;
-  int use_hash;
 };
 
 int launch_attention(const AttnLaunch& L, cudaStream_t stream);

@@ -1,152 +1,197 @@
-// scfa_sched.cu — tile schedules.
+// scfa_sched.cu — visibility runs and tile schedules.
 //
-// 1. Exact tile lists for the tcgen05 kernels.  The reference schedules a
-//    contiguous key-block range per query block — [0, j_stop) for the QK and
-//    dense kernels (causal_j_stops, _kernel.py:45-53) and a causally refined
-//    bucket band [j_start, j_stop) for hash (hash_tile_ranges, _kernel.py:56-79)
-//    — and then masks.  Here a tile is listed only if it contains at least one
-//    visible pair; that is decided exactly per tile from the sorted index /
-//    bucket vectors, and tiles whose pairs are all visible are flagged so the
-//    kernel skips the per-element mask there.
-// 2. The reference's own schedule at any BlockSpec, used to report
+// 1. Visibility runs.  Both sides of every (b, h) slice are sorted — keys by
+//    position (QK / dense, pads at the tail) or by (bucket, position) (hash,
+//    sort_by_bucket hash_sparse.py:89-133).  The keys a query sees,
+//    {k : k_hash == q_hash and k_idx <(=) q_idx} (_tile_mask, _kernel.py:82-89),
+//    are therefore ONE contiguous run of key slots: the prefix of the query's
+//    bucket run cut at the causal boundary.  Likewise the queries a key is seen
+//    by form one run of query slots.  scfa_build_schedule stores that run,
+//    [lo, hi), per row slot; the attention kernels turn it into their
+//    per-element mask with two subtractions per tile, with no binary search and no
+//    per-column index traffic.
+// 2. Exact tile lists.  The reference schedules a contiguous key-block range per
+//    query block — [0, j_stop) for QK / dense (causal_j_stops, _kernel.py:45-53)
+//    and a causally refined bucket band for hash (hash_tile_ranges,
+//    _kernel.py:56-79) — and masks inside it.  Here a (row block, column block)
+//    tile is listed iff some row's run intersects it, and flagged "full" (bit 15)
+//    iff every row's run covers it, so the kernel skips the mask there.
+// 3. The reference's own schedule at any BlockSpec, used to report
 //    FlashOutputs.tiles_computed with the reference's meaning.
 #include "scfa_common.cuh"
 #include "scfa_internal.h"
 
 namespace scfa {
 
-constexpr int kMaxBlockRows = 128;
-constexpr int kMaxColBlocks = 4096;
+constexpr int kRowBlock = 128;
+constexpr int kMaxColBlocks = 2048;  // 131072 streamed slots at 64-slot tiles
 
-struct Summary {
-  int min_i, max_i, min_h, max_h;
-};
+// first i in [0, n) with a[i] >= x / > x  (a ascending on [0, n))
+SCFA_DEVICE int g_lower(const int32_t* __restrict__ a, int n, int x) {
+  int lo = 0;
+  while (n > 0) {
+    const int h = n >> 1;
+    if (__ldg(a + lo + h) < x) { lo += h + 1; n -= h + 1; } else { n = h; }
+  }
+  return lo;
+}
+SCFA_DEVICE int g_upper(const int32_t* __restrict__ a, int n, int x) {
+  int lo = 0;
+  while (n > 0) {
+    const int h = n >> 1;
+    if (__ldg(a + lo + h) <= x) { lo += h + 1; n -= h + 1; } else { n = h; }
+  }
+  return lo;
+}
 
-// one warp per (bh, block): min/max of index and bucket over all slots of the block
-__global__ void block_summary_kernel(const int32_t* __restrict__ idx, const int32_t* __restrict__ hash, int64_t T_pad,
-                                     int block, int64_t n_blk, int64_t total, Summary* __restrict__ out) {
-  const int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (w >= total) return;
-  const int64_t bh = w / n_blk, blk = w - bh * n_blk;
-  const int32_t* ip = idx + bh * T_pad + blk * block;
-  const int32_t* hp = hash ? hash + bh * T_pad + blk * block : nullptr;
-  int mn = 0x7fffffff, mx = -0x7fffffff - 1, hmn = 0x7fffffff, hmx = -0x7fffffff - 1;
-  for (int i = lane; i < block; i += 32) {
-    const int v = ip[i];
-    mn = min(mn, v);
-    mx = max(mx, v);
-    if (hp) {
-      const int hv = hp[i];
-      hmn = min(hmn, hv);
-      hmx = max(hmx, hv);
+// One thread per row slot.  dir 0: rows = queries, run in key-slot space;
+// dir 1: rows = keys, run in query-slot space.  Row slots past the true
+// length get the empty run.
+__global__ void __launch_bounds__(256) runs_kernel(const int32_t* __restrict__ q_idx, const int32_t* __restrict__ q_hash,
+                                                   const int32_t* __restrict__ k_idx, const int32_t* __restrict__ k_hash,
+                                                   int T_q, int T_kv, int Tq_pad, int Tkv_pad, int flags,
+                                                   int2* __restrict__ q_runs, int2* __restrict__ k_runs) {
+  const int dir = blockIdx.y;
+  const int64_t bh = blockIdx.z;
+  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool excl = (flags & SCFA_FLAG_EXCLUDE_SELF) != 0;
+  const bool use_hash = (flags & SCFA_FLAG_HASH) != 0;
+  const int32_t* qi = q_idx + bh * Tq_pad;
+  const int32_t* ki = k_idx + bh * Tkv_pad;
+  const int32_t* qh = use_hash ? q_hash + bh * Tq_pad : nullptr;
+  const int32_t* kh = use_hash ? k_hash + bh * Tkv_pad : nullptr;
+  if (dir == 0) {
+    if (q_runs == nullptr || slot >= Tq_pad) return;
+    int2 r = make_int2(0, 0);
+    if (slot < T_q && T_kv > 0) {
+      const int x = qi[slot];
+      if (!use_hash) {  // keys ascending, pads (10^9) at the tail
+        r.y = excl ? g_lower(ki, T_kv, x) : g_upper(ki, T_kv, x);
+      } else {          // bucket run [a, e), sorted by position inside
+        const int g = qh[slot];
+        const int a = g_lower(kh, T_kv, g);
+        const int e = a + g_upper(kh + a, T_kv - a, g);
+        r.x = a;
+        r.y = a + (excl ? g_lower(ki + a, e - a, x) : g_upper(ki + a, e - a, x));
+      }
     }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    hmn = min(hmn, __shfl_xor_sync(0xffffffffu, hmn, o));
-    hmx = max(hmx, __shfl_xor_sync(0xffffffffu, hmx, o));
-  }
-  if (lane == 0) {
-    Summary r;
-    r.min_i = mn;
-    r.max_i = mx;
-    r.min_h = hp ? hmn : 0;
-    r.max_h = hp ? hmx : 0;
-    out[w] = r;
+    q_runs[bh * Tq_pad + slot] = r;
+  } else {
+    if (k_runs == nullptr || slot >= Tkv_pad) return;
+    int2 r = make_int2(0, 0);
+    if (slot < T_kv && T_q > 0) {
+      const int x = ki[slot];
+      if (!use_hash) {  // real queries ascending, then pads (-1) at the tail
+        int n_real = 0, n = T_q;
+        while (n > 0) {
+          const int h = n >> 1;
+          if (__ldg(qi + n_real + h) >= 0) { n_real += h + 1; n -= h + 1; } else { n = h; }
+        }
+        r.x = excl ? g_upper(qi, n_real, x) : g_lower(qi, n_real, x);
+        r.y = n_real;
+      } else {
+        const int g = kh[slot];
+        const int a = g_lower(qh, T_q, g);
+        const int e = a + g_upper(qh + a, T_q - a, g);
+        r.x = a + (excl ? g_upper(qi + a, e - a, x) : g_lower(qi + a, e - a, x));
+        r.y = e;
+      }
+    }
+    k_runs[bh * Tkv_pad + slot] = r;
   }
 }
 
-SCFA_DEVICE bool causal_ok(int qi, int ki, bool excl) { return excl ? (qi > ki) : (qi >= ki); }
+struct ListJob {
+  const int2* runs;  // row runs (BH, T_rows_pad)
+  uint16_t* list;    // (BH, n_rb, stride)
+  int32_t* count;    // (BH, n_rb)
+  int64_t stride;
+  int T_rows, T_rows_pad, n_rb, n_cb, col_block;
+};
 
-// Tile classification: 0 empty, 1 partial (mask needed), 2 full.
-// rows = stationary side (queries if rows_are_queries), cols = streamed side.
-__global__ void __launch_bounds__(128) tile_list_kernel(
-    const int32_t* __restrict__ q_idx, const int32_t* __restrict__ q_hash, const int32_t* __restrict__ k_idx,
-    const int32_t* __restrict__ k_hash, int64_t T_q, int64_t T_kv, int64_t Tq_pad, int64_t Tkv_pad,
-    int rows_are_queries, int row_block, int col_block, int flags, const Summary* __restrict__ row_sum,
-    const Summary* __restrict__ col_sum, int n_row_blocks, int n_col_blocks, uint16_t* __restrict__ list,
-    int32_t* __restrict__ list_count, int64_t list_stride, unsigned long long* tiles_total) {
-  __shared__ int r_idx[kMaxBlockRows];
-  __shared__ int r_hash[kMaxBlockRows];
-  __shared__ uint8_t cls[kMaxColBlocks];
+struct ListJobs {
+  ListJob job[3];
+  unsigned long long* tiles;  // [3] accumulated, may be null
+};
+
+// One CTA (128 threads = 128 rows) per (row block, slice, list).  Each row adds its
+// run's column-block range to a difference array; a block scan turns it into the
+// set of non-empty tiles, listed in ascending order.  The full-tile range is the
+// intersection of every row's fully covered blocks.
+__global__ void __launch_bounds__(128) tile_list_kernel(const __grid_constant__ ListJobs jobs) {
+  __shared__ int diff[kMaxColBlocks + 8];
+  __shared__ int warp_tot[4];
+  __shared__ int full_lo, full_hi;
+  const int z = blockIdx.z;
+  const ListJob& J = jobs.job[z];
   const int rb = blockIdx.x;
   const int64_t bh = blockIdx.y;
-  const bool excl = (flags & SCFA_FLAG_EXCLUDE_SELF) != 0;
-  const bool use_hash = (flags & SCFA_FLAG_HASH) != 0;
-  const bool rq = rows_are_queries != 0;
-  const int32_t* ri = rq ? q_idx + bh * Tq_pad : k_idx + bh * Tkv_pad;
-  const int32_t* rh = rq ? q_hash + bh * Tq_pad : k_hash + bh * Tkv_pad;
-  const int32_t* ci = rq ? k_idx + bh * Tkv_pad : q_idx + bh * Tq_pad;
-  const int32_t* ch = rq ? k_hash + bh * Tkv_pad : q_hash + bh * Tq_pad;
-  const int64_t T_rows = rq ? T_q : T_kv, T_cols = rq ? T_kv : T_q;
-  const int row0 = rb * row_block;
-  const int n_r = static_cast<int>((T_rows - row0) < row_block ? (T_rows - row0) : row_block);
-  for (int i = threadIdx.x; i < row_block; i += blockDim.x) {
-    r_idx[i] = ri[row0 + i];
-    if (use_hash) r_hash[i] = rh[row0 + i];
+  if (J.list == nullptr || rb >= J.n_rb) return;
+  const int n_cb = J.n_cb, B = J.col_block;
+  for (int i = threadIdx.x; i <= n_cb; i += blockDim.x) diff[i] = 0;
+  if (threadIdx.x == 0) {
+    full_lo = 0;
+    full_hi = n_cb;
   }
   __syncthreads();
-  const Summary rs = row_sum[bh * n_row_blocks + rb];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nw = blockDim.x >> 5;
-  for (int cb = warp; cb < n_col_blocks; cb += nw) {
-    const Summary cs = col_sum[bh * n_col_blocks + cb];
-    // query/key views of the two summaries
-    const Summary& qs = rq ? rs : cs;
-    const Summary& ks = rq ? cs : rs;
-    int c = 0;
-    bool maybe = causal_ok(qs.max_i, ks.min_i, excl);
-    if (use_hash) maybe = maybe && max(qs.min_h, ks.min_h) <= min(qs.max_h, ks.max_h);
-    if (maybe) {
-      const bool all_vis = causal_ok(qs.min_i, ks.max_i, excl) &&
-                           (!use_hash || (qs.min_h == qs.max_h && ks.min_h == ks.max_h && qs.min_h == ks.min_h));
-      if (all_vis) {
-        c = 2;
-      } else if (!use_hash) {
-        c = 1;  // sorted indices: max_q vs min_k decides non-emptiness exactly
-      } else {
-        // exact bucket test: per column bucket g, the row run of g is contiguous and
-        // sorted by index, so one binary search finds the extreme row of the run.
-        const int col0 = cb * col_block;
-        bool hit = false;
-        for (int j = lane; j < col_block && !hit; j += 32) {
-          const int64_t col = col0 + j;
-          if (col >= T_cols) break;
-          const int g = ch[col], cidx = ci[col];
-          int lo = 0, hi = n_r;
-          if (rq) {  // last query row with bucket g (largest index in the run)
-            while (lo < hi) { const int mid = (lo + hi) >> 1; if (r_hash[mid] <= g) lo = mid + 1; else hi = mid; }
-            const int r = lo - 1;
-            hit = (r >= 0 && r_hash[r] == g && causal_ok(r_idx[r], cidx, excl));
-          } else {   // first key row with bucket g (smallest index in the run)
-            while (lo < hi) { const int mid = (lo + hi) >> 1; if (r_hash[mid] < g) lo = mid + 1; else hi = mid; }
-            hit = (lo < n_r && r_hash[lo] == g && causal_ok(cidx, r_idx[lo], excl));
-          }
-        }
-        c = __any_sync(0xffffffffu, hit) ? 1 : 0;
-      }
-    }
-    if (lane == 0) cls[cb] = static_cast<uint8_t>(c);
+  const int row = rb * kRowBlock + threadIdx.x;
+  const int2 r = (row < J.T_rows_pad) ? J.runs[bh * J.T_rows_pad + row] : make_int2(0, 0);
+  if (r.y > r.x) {
+    atomicAdd(&diff[r.x / B], 1);
+    atomicAdd(&diff[(r.y - 1) / B + 1], -1);
+    atomicMax(&full_lo, (r.x + B - 1) / B);
+    atomicMin(&full_hi, r.y / B);
+  } else {
+    atomicMin(&full_hi, 0);  // a row that sees nothing: no tile of this block is full
   }
   __syncthreads();
-  if (warp == 0) {
-    uint16_t* out = list + (bh * n_row_blocks + rb) * list_stride;
-    int n = 0;
-    for (int c0 = 0; c0 < n_col_blocks; c0 += 32) {
-      const int cb = c0 + lane;
-      const int c = cb < n_col_blocks ? cls[cb] : 0;
-      const uint32_t bal = __ballot_sync(0xffffffffu, c != 0);
-      const int pos = n + __popc(bal & ((1u << lane) - 1u));
-      if (c) out[pos] = static_cast<uint16_t>(cb | (c == 2 ? 0x8000 : 0));
-      n += __popc(bal);
+  // ---- ascending compaction of {cb : prefix(diff)[cb] > 0}; thread i owns a chunk
+  const int per = (n_cb + blockDim.x - 1) / blockDim.x;
+  const int c0 = threadIdx.x * per, c1 = min(n_cb, c0 + per);
+  int run = 0, mine = 0;
+  for (int c = c0; c < c1; ++c) run += diff[c];
+  // exclusive scan of the chunk sums -> running coverage at c0
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  int cover = incl - run;
+  for (int w = 0; w < warp; ++w) cover += warp_tot[w];
+  {
+    int c = cover;
+    for (int i = c0; i < c1; ++i) {
+      c += diff[i];
+      mine += (c > 0);
     }
-    if (lane == 0) {
-      list_count[bh * n_row_blocks + rb] = n;
-      if (tiles_total) atomicAdd(tiles_total, static_cast<unsigned long long>(n));
+  }
+  __syncthreads();  // warp_tot reused below
+  int pos = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, pos, o);
+    if (lane >= o) pos += v;
+  }
+  if (lane == 31) warp_tot[warp] = pos;
+  __syncthreads();
+  pos -= mine;
+  for (int w = 0; w < warp; ++w) pos += warp_tot[w];
+  uint16_t* out = J.list + (bh * J.n_rb + rb) * J.stride;
+  const int flo = full_lo, fhi = full_hi;
+  {
+    int c = cover;
+    for (int i = c0; i < c1; ++i) {
+      c += diff[i];
+      if (c > 0) out[pos++] = static_cast<uint16_t>(i | ((i >= flo && i < fhi) ? 0x8000 : 0));
     }
+  }
+  if (threadIdx.x == blockDim.x - 1) {
+    J.count[bh * J.n_rb + rb] = pos;
+    if (jobs.tiles) atomicAdd(jobs.tiles + z, static_cast<unsigned long long>(pos));
   }
 }
 
@@ -228,58 +273,72 @@ __global__ void ref_schedule_kernel(const int32_t* __restrict__ q_idx, const int
 
 using namespace scfa;
 
-extern "C" int scfa_build_tile_lists(const int32_t* q_idx, const int32_t* q_hash, const int32_t* k_idx,
-                                     const int32_t* k_hash, int64_t BH, int64_t T_q, int64_t T_kv, int64_t Tq_pad,
-                                     int64_t Tkv_pad, int rows_are_queries, int row_block, int col_block, int flags,
-                                     uint16_t* list, int32_t* list_count, int64_t list_stride,
-                                     unsigned long long* tiles_total, void* workspace, int64_t workspace_bytes,
-                                     void* stream) {
+extern "C" int scfa_build_schedule(const int32_t* q_idx, const int32_t* q_hash, const int32_t* k_idx,
+                                   const int32_t* k_hash, int64_t BH, int64_t T_q, int64_t T_kv, int64_t Tq_pad,
+                                   int64_t Tkv_pad, int flags, int32_t* q_runs, int32_t* k_runs, int runs_ready,
+                                   uint16_t* list_fwd,
+                                   int32_t* count_fwd, int64_t stride_fwd, uint16_t* list_dq, int32_t* count_dq,
+                                   int64_t stride_dq, uint16_t* list_dkdv, int32_t* count_dkdv, int64_t stride_dkdv,
+                                   unsigned long long* tiles, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const bool rq = rows_are_queries != 0;
-  const int64_t T_rows = rq ? T_q : T_kv, T_cols = rq ? T_kv : T_q;
-  const int64_t n_rb = (T_rows + row_block - 1) / row_block;
-  const int64_t n_cb = (T_cols + col_block - 1) / col_block;
-  if (row_block > kMaxBlockRows || n_cb > kMaxColBlocks || n_cb > list_stride || n_cb > 32767) {
-    set_error("tile list: sequence too long for the schedule builder");
+  if (Tq_pad < ((T_q + 127) / 128) * 128 || Tkv_pad < ((T_kv + 127) / 128) * 128 || BH > 65535) {
+    set_error("schedule: padded vectors shorter than the block grid (or too many slices)");
     return SCFA_ERR_SHAPE;
   }
-  const int64_t Tr_pad = rq ? Tq_pad : Tkv_pad, Tc_pad = rq ? Tkv_pad : Tq_pad;
-  if (n_rb * row_block > Tr_pad || n_cb * col_block > Tc_pad) {
-    set_error("tile list: padded vectors shorter than the block grid");
-    return SCFA_ERR_SHAPE;
+  if ((list_fwd || list_dq) && q_runs == nullptr) {
+    set_error("schedule: query-row lists need q_runs");
+    return SCFA_ERR_PARAM;
   }
-  if (BH == 0 || n_rb == 0) return SCFA_OK;
-  const bool use_hash = (flags & SCFA_FLAG_HASH) != 0;
-  const int64_t bytes = BH * (n_rb + n_cb) * static_cast<int64_t>(sizeof(Summary));
-  if (workspace == nullptr || workspace_bytes < bytes || (reinterpret_cast<uintptr_t>(workspace) & 15)) {
-    set_error("tile list: workspace must be >= %lld bytes, 16-byte aligned", static_cast<long long>(bytes));
-    return SCFA_ERR_SHAPE;
+  if (list_dkdv && k_runs == nullptr) {
+    set_error("schedule: key-row lists need k_runs");
+    return SCFA_ERR_PARAM;
   }
-  Summary* sums = static_cast<Summary*>(workspace);
-  Summary* rsum = sums;
-  Summary* csum = sums + BH * n_rb;
-  const int32_t* ri = rq ? q_idx : k_idx;
-  const int32_t* rh = rq ? q_hash : k_hash;
-  const int32_t* ci = rq ? k_idx : q_idx;
-  const int32_t* chh = rq ? k_hash : q_hash;
-  {
-    const int64_t tot = BH * n_rb;
-    block_summary_kernel<<<static_cast<unsigned>((tot * 32 + 255) / 256), 256, 0, s>>>(
-        ri, use_hash ? rh : nullptr, Tr_pad, row_block, n_rb, tot, rsum);
+  if (BH == 0) return SCFA_OK;
+  ListJobs jobs{};
+  const int n_rb_q = static_cast<int>((T_q + 127) / 128), n_rb_k = static_cast<int>((T_kv + 127) / 128);
+  const int64_t n_cb128_k = (T_kv + 127) / 128, n_cb64_k = (T_kv + 63) / 64, n_cb64_q = (T_q + 63) / 64;
+  auto set = [&](int z, const int32_t* runs, uint16_t* list, int32_t* count, int64_t stride, int64_t T_rows,
+                 int64_t T_rows_pad, int64_t n_cb, int B) -> int {
+    if (!list) return SCFA_OK;
+    if (n_cb > kMaxColBlocks || n_cb > 32767 || stride < n_cb || !count) {
+      set_error("schedule: sequence too long for the tile lists (or list stride < column blocks)");
+      return SCFA_ERR_SHAPE;
+    }
+    ListJob& J = jobs.job[z];
+    J.runs = reinterpret_cast<const int2*>(runs);
+    J.list = list;
+    J.count = count;
+    J.stride = stride;
+    J.T_rows = static_cast<int>(T_rows);
+    J.T_rows_pad = static_cast<int>(T_rows_pad);
+    J.n_rb = static_cast<int>((T_rows + 127) / 128);
+    J.n_cb = static_cast<int>(n_cb);
+    J.col_block = B;
+    return SCFA_OK;
+  };
+  int rc = set(0, q_runs, list_fwd, count_fwd, stride_fwd, T_q, Tq_pad, n_cb128_k, 128);
+  rc = rc ? rc : set(1, q_runs, list_dq, count_dq, stride_dq, T_q, Tq_pad, n_cb64_k, 64);
+  rc = rc ? rc : set(2, k_runs, list_dkdv, count_dkdv, stride_dkdv, T_kv, Tkv_pad, n_cb64_q, 64);
+  if (rc) return rc;
+  jobs.tiles = tiles;
+  const int64_t Tmax_pad = Tq_pad > Tkv_pad ? Tq_pad : Tkv_pad;
+  int2* q_out = (runs_ready & 1) ? nullptr : reinterpret_cast<int2*>(q_runs);
+  int2* k_out = (runs_ready & 2) ? nullptr : reinterpret_cast<int2*>(k_runs);
+  if (q_out || k_out) {
+    dim3 grid(static_cast<unsigned>((Tmax_pad + 255) / 256), 2, static_cast<unsigned>(BH));
+    runs_kernel<<<grid, 256, 0, s>>>(q_idx, (flags & SCFA_FLAG_HASH) ? q_hash : nullptr, k_idx,
+                                     (flags & SCFA_FLAG_HASH) ? k_hash : nullptr, static_cast<int>(T_q),
+                                     static_cast<int>(T_kv), static_cast<int>(Tq_pad), static_cast<int>(Tkv_pad), flags,
+                                     q_out, k_out);
   }
-  if (n_cb > 0) {
-    const int64_t tot = BH * n_cb;
-    block_summary_kernel<<<static_cast<unsigned>((tot * 32 + 255) / 256), 256, 0, s>>>(
-        ci, use_hash ? chh : nullptr, Tc_pad, col_block, n_cb, tot, csum);
+  const int n_rb = n_rb_q > n_rb_k ? n_rb_q : n_rb_k;
+  if ((list_fwd || list_dq || list_dkdv) && n_rb > 0) {
+    dim3 grid(static_cast<unsigned>(n_rb), static_cast<unsigned>(BH), 3);
+    tile_list_kernel<<<grid, 128, 0, s>>>(jobs);
   }
-  dim3 grid(static_cast<unsigned>(n_rb), static_cast<unsigned>(BH));
-  tile_list_kernel<<<grid, 128, 0, s>>>(q_idx, use_hash ? q_hash : q_idx, k_idx, use_hash ? k_hash : k_idx, T_q,
-                                        T_kv, Tq_pad, Tkv_pad, rows_are_queries, row_block, col_block, flags, rsum,
-                                        csum, static_cast<int>(n_rb), static_cast<int>(n_cb), list, list_count,
-                                        list_stride, tiles_total);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
-    set_error("tile list: %s", cudaGetErrorString(e));
+    set_error("schedule: %s", cudaGetErrorString(e));
     return SCFA_ERR_CUDA;
   }
   return SCFA_OK;

@@ -1,0 +1,116 @@
+"""GPU schedule parity: the visibility runs and exact tile lists of scfa_build_schedule
+against a brute-force visibility matrix built by the oracle on the same sorted /
+compacted index vectors (_tile_mask semantics, _kernel.py:82-89).
+
+Bars (bit-exact): every row's run [lo, hi) is exactly its set of visible slots; a tile
+is listed iff it holds a visible pair, flagged full iff all its pairs are visible;
+the listed-tile totals match.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import scfa_oracle as orc
+
+import paper_2306_01160_b200 as scfa
+from paper_2306_01160_b200 import hash_sparse as hs
+
+pytestmark = pytest.mark.gpu
+
+
+def _check_problem(prob, vis):
+    """vis: (BH, T_q, T_kv) bool in kernel slot order."""
+    sched = prob.schedule("fwd", "dq", "dkdv")
+    BH, Tq, Tk = vis.shape
+    qr = sched["q_runs"].cpu().numpy()
+    kr = sched["k_runs"].cpu().numpy()
+    for bh in range(BH):
+        for s in range(prob.Tq_pad):
+            want = np.zeros(Tk, bool) if s >= Tq else vis[bh, s]
+            got = np.zeros(Tk, bool)
+            got[qr[bh, s, 0]:qr[bh, s, 1]] = True
+            assert np.array_equal(got, want), f"q run bh={bh} slot={s}: {qr[bh, s]}"
+        for s in range(prob.Tkv_pad):
+            want = np.zeros(Tq, bool) if s >= Tk else vis[bh, :, s]
+            got = np.zeros(Tq, bool)
+            got[kr[bh, s, 0]:kr[bh, s, 1]] = True
+            assert np.array_equal(got, want), f"k run bh={bh} slot={s}: {kr[bh, s]}"
+    totals = prob._tiles_total.cpu().numpy()
+    for slot, (name, rows_q, cb) in enumerate((("fwd", True, 128), ("dq", True, 64), ("dkdv", False, 64))):
+        lst, cnt, _ = sched[name]
+        lst = lst.cpu().numpy().view(np.uint16)
+        cnt = cnt.cpu().numpy()
+        v = vis if rows_q else np.swapaxes(vis, 1, 2)
+        n_rb = -(-v.shape[1] // 128)
+        n_cb = -(-v.shape[2] // cb)
+        total = 0
+        for bh in range(BH):
+            for rb in range(n_rb):
+                rows = np.zeros((128, n_cb * cb), bool)
+                blk = v[bh, rb * 128:(rb + 1) * 128]
+                rows[:blk.shape[0], :blk.shape[1]] = blk
+                tiles = rows.reshape(128, n_cb, cb)
+                any_ = tiles.any(axis=(0, 2))
+                all_ = tiles.all(axis=(0, 2))
+                want = [c | (0x8000 if all_[c] else 0) for c in range(n_cb) if any_[c]]
+                got = list(lst[bh, rb, :cnt[bh, rb]])
+                assert got == want, f"{name} bh={bh} rb={rb}: {got[:8]} vs {want[:8]}"
+                total += len(want)
+        assert totals[slot] == total
+
+
+@pytest.mark.parametrize("T,nb,excl,seed", [(300, 4, True, 0), (1024, 16, True, 1), (512, 1, False, 2),
+                                            (700, 64, True, 3)])
+def test_hash_runs_and_lists(T, nb, excl, seed):
+    B, H, D = 1, 2, 64
+    dev = torch.device("cuda")
+    x = torch.zeros((B, T, H, D), dtype=torch.bfloat16, device=dev)
+    h = torch.from_numpy(scfa.random_buckets(B, T, H, nb, seed)).to(dev)
+    sb = hs._sort_batch(x, x, x, h, h, "bthd")
+    prob = hs._problem_of(sb, excl)
+    qi = sb.q_idx.cpu().numpy().reshape(B * H, T)
+    qh = sb.q_hash.cpu().numpy().reshape(B * H, T)
+    vis = orc.visibility(qi, qi, qh, qh, exclude_self=excl)
+    _check_problem(prob, vis)
+
+
+def test_hash_rect_runs_and_lists():
+    B, H, D, Tq, Tk = 1, 2, 64, 200, 333
+    dev = torch.device("cuda")
+    xq = torch.zeros((B, Tq, H, D), dtype=torch.bfloat16, device=dev)
+    xk = torch.zeros((B, Tk, H, D), dtype=torch.bfloat16, device=dev)
+    qh = torch.from_numpy(scfa.random_buckets(B, Tq, H, 8, 5)).to(dev)
+    kh = torch.from_numpy(scfa.random_buckets(B, Tk, H, 8, 6)).to(dev)
+    sb = hs._sort_batch(xq, xk, xk, qh, kh, "bthd")
+    prob = hs._problem_of(sb, True)
+    qi = sb.q_idx.cpu().numpy().reshape(B * H, Tq)
+    ki = sb.k_idx.cpu().numpy().reshape(B * H, Tk)
+    vis = orc.visibility(qi, ki, sb.q_hash.cpu().numpy().reshape(B * H, Tq),
+                         sb.k_hash.cpu().numpy().reshape(B * H, Tk), exclude_self=True)
+    _check_problem(prob, vis)
+
+
+@pytest.mark.parametrize("T,drop,seed", [(300, 0.5, 0), (1024, 0.3, 1), (256, 0.0, 2), (400, 0.95, 3)])
+def test_qk_runs_and_lists(T, drop, seed):
+    B, H, D = 2, 2, 64
+    dev = torch.device("cuda")
+    x = torch.zeros((B, T, H, D), dtype=torch.bfloat16, device=dev)
+    qk = torch.from_numpy(scfa.random_keep(B, T, H, drop, seed)).to(dev)
+    kk = torch.from_numpy(scfa.random_keep(B, T, H, drop, seed + 100)).to(dev)
+    prep = scfa.qk_preprocess(x, x, x, qk, kk)
+    prob = prep.problem
+    qi = prep.q_idx.cpu().numpy().reshape(B * H, -1).astype(np.int64)
+    ki = prep.k_idx.cpu().numpy().reshape(B * H, -1).astype(np.int64)
+    vis = orc.visibility(qi, ki)
+    vis &= (qi >= 0)[..., :, None] & (ki < orc.KEY_PAD)[..., None, :]
+    _check_problem(prob, vis)
+
+
+def test_dense_runs_and_lists():
+    from paper_2306_01160_b200.dense import causal_problem
+
+    T = 513
+    prob = causal_problem(1, 1, T, 64, torch.device("cuda"))
+    vis = orc.visibility(np.arange(T), np.arange(T))[None]
+    _check_problem(prob, vis)
