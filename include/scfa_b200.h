@@ -80,6 +80,20 @@ int scfa_hash_sort(const void* hash, int hash_dtype, int64_t B, int64_t T, int64
                    int64_t ps_t, int32_t* perm, int32_t* rank, int32_t* scratch, int32_t* err_flag,
                    void* stream);
 
+/* Fused hash preparation for SHARED bucket ids (q_hash is k_hash, T_Q == T_KV,
+ * positions = arange: the reference's bench / LM setting, cli.py:481-487).
+ * One launch replaces scfa_hash_sort + 2 x scfa_build_aux + the run pass of
+ * scfa_build_schedule: the stable sort of _bucket_order (hash_sparse.py:89-94),
+ * the sorted idx / hash vectors of sort_by_bucket (hash_sparse.py:127-133) and
+ * the visibility runs for `flags` (SCFA_FLAG_EXCLUDE_SELF).  T <= 16384.
+ * perm/rank (B*H, T); scratch (B*H, T + 257); q_idx/k_idx/q_hash/k_hash (B*H, T_pad) with the
+ * same sentinels as scfa_build_aux; q_runs/k_runs (B*H, T_pad) int32 pairs as
+ * scfa_build_schedule (pass runs_ready = 3 there).                           */
+int scfa_hash_prepare(const void* hash, int hash_dtype, int64_t B, int64_t T, int64_t H, int64_t sb,
+                      int64_t st, int64_t sh, int flags, int32_t* perm, int32_t* rank, int32_t* scratch,
+                      int32_t* q_idx, int32_t* k_idx, int32_t* q_hash, int32_t* k_hash, int32_t* q_runs,
+                      int32_t* k_runs, int32_t* err_flag, void* stream);
+
 /* ---------------------------------------------------------------- gather / scatter
  * Row gather into engine layout (compact(...) take_along_axis, qk_sparse.py:68-70;
  * sort_by_bucket gather_rows, hash_sparse.py:122-125) fused with the
@@ -90,6 +104,13 @@ int scfa_hash_sort(const void* hash, int hash_dtype, int64_t B, int64_t T, int64
 int scfa_gather_rows(const void* src, int elem_bytes, int64_t B, int64_t H, int64_t D, int64_t sb,
                      int64_t st, int64_t sh, const int32_t* perm, int64_t T_perm, int64_t n_slots,
                      void* dst, void* stream);
+
+/* n (1..3) scfa_gather_rows in one launch (Q | K | V of one batch).  Host arrays:
+ * srcs/dsts/perms[n]; strides[3n] = (sb, st, sh) per source; T_perm[n], n_slots[n].
+ * All sources share elem_bytes, B, H, D.                                      */
+int scfa_gather_rows3(int n, const void* const* srcs, void* const* dsts, const int32_t* const* perms,
+                      const int64_t* strides, int elem_bytes, int64_t B, int64_t H, int64_t D,
+                      const int64_t* T_perm, const int64_t* n_slots, void* stream);
 
 /* Inverse: dst row (b,t,h) = src[bh, rank[bh,t]] if rank < n_slots else 0.
  * Replaces qk_postprocess (qk_sparse.py:214-225) and hash_scatter +

@@ -83,6 +83,11 @@ class Problem:
     def Tkv_pad(self):
         return pad128(self.T_kv)
 
+    def set_runs(self, q_runs, k_runs):
+        """Adopt visibility runs computed elsewhere (scfa_hash_prepare) for this problem's flags."""
+        self._lists["q_runs"] = q_runs
+        self._lists["k_runs"] = k_runs
+
     def _hash_ptrs(self):
         if self.flags & _lib.FLAG_HASH:
             return _lib.ptr(self.q_hash), _lib.ptr(self.k_hash)

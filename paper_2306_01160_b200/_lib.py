@@ -42,6 +42,8 @@ _SIGS = {
     "scfa_qk_compact": [_P, _I, _L, _L, _L, _L, _L, _L, _P, _P, _P, _P, _P],
     "scfa_hash_sort": [_P, _I, _L, _L, _L, _L, _L, _L, _P, _I, _L, _L, _P, _P, _P, _P, _P],
     "scfa_gather_rows": [_P, _I, _L, _L, _L, _L, _L, _L, _P, _L, _L, _P, _P],
+    "scfa_gather_rows3": [_I, _P, _P, _P, _P, _I, _L, _L, _L, _P, _P, _P],
+    "scfa_hash_prepare": [_P, _I, _L, _L, _L, _L, _L, _L, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "scfa_scatter_rows": [_P, _I, _L, _L, _L, _L, _P, _L, _P, _I, _L, _L, _L, _P],
     "scfa_build_aux": [_P, _P, _L, _L, _L, _L, _L, ctypes.c_int32, ctypes.c_int32, _P, _I, _L, _L, _L,
                        ctypes.c_int32, _P, _I, _L, _L, _P, _P, _P],
@@ -118,6 +120,15 @@ def call(name, *args):
         EVENT_HOOK(name, 1)
     raise_for(rc, name)
     launches += KERNELS_PER_CALL.get(name, 1)
+
+
+def ptr_array(tensors):
+    """Host array of device pointers (void*[n]) for the multi-tensor entry points."""
+    return (ctypes.c_void_p * len(tensors))(*[t.data_ptr() for t in tensors])
+
+
+def i64_array(values):
+    return (ctypes.c_int64 * len(values))(*[int(v) for v in values])
 
 
 def ptr(t):

@@ -217,7 +217,262 @@ __global__ void __launch_bounds__(kSortThreads) hash_sort_kernel(
   for (int64_t s = threadIdx.x; s < T; s += blockDim.x) rank[bh * T + perm[bh * T + s]] = static_cast<int32_t>(s);
 }
 
+// ------------------------------------------------------------------ fused hash preparation
+//
+// Shared bucket ids (q_hash is k_hash, T_Q == T_KV, positions = arange — the
+// reference's own bench / LM setting, cli.py:481-487): one CTA per (b, h) slice
+// does, with the slice's keys cached in shared memory,
+//   sort_by_bucket's stable argsort (hash_sparse.py:89-94)        -> perm, rank
+//   the sorted idx / hash vectors (hash_sparse.py:127-133, padded) -> idx_*, hash_*
+//   the visibility runs (scfa_sched.cu runs_kernel), which for shared ids are
+//   O(1) per slot: a query slot s in bucket run [a, e) sees key slots [a, s)
+//   ([a, s] without exclude_self) and key slot s is seen by query slots (s, e).
+// That replaces hash_sort + 2 x build_aux + runs_kernel (four launches, three
+// re-reads of the ids from HBM) by one launch.
+
+constexpr int kPrepMaxT = 16384;
+
+struct PrepSmem {
+  int cnt[256][32];  // per (digit, warp) counts, then exclusive offsets (digit-major)
+  int red[33];
+  long long mx;
+};
+
+SCFA_DEVICE int lower_bound_s(const int32_t* a, int n, int x) {
+  int lo = 0;
+  while (n > 0) {
+    const int h = n >> 1;
+    if (a[lo + h] < x) { lo += h + 1; n -= h + 1; } else { n = h; }
+  }
+  return lo;
+}
+
+// Stable LSD radix pass (8-bit digit) of the slice: warp w owns the contiguous slot
+// segment [w * seg, (w + 1) * seg) of `src` and walks it in order, so
+//   slot = sum of counts of smaller digits (all warps) + counts of this digit in
+//          earlier warps + this warp's running count + rank among equal lanes,
+// which is exactly argsort(kind="stable").  Two walks, three __syncthreads.
+SCFA_DEVICE void radix_pass(PrepSmem& S, const int32_t* key, int T, int shift, const int32_t* src, int32_t* dst,
+                           int32_t* sorted_key) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int seg = (((T + 31) / 32) + 31) & ~31;
+  const int s0 = warp * seg, s1 = min(T, s0 + seg);
+  for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) (&S.cnt[0][0])[i] = 0;
+  __syncthreads();
+  for (int base = s0; base < s1; base += 32) {
+    const int s = base + lane;
+    const bool act = s < s1;
+    const int d = act ? ((key[src ? src[s] : s] >> shift) & 255) : 256 + lane;
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    if (act && (peers & lanemask_lt()) == 0) S.cnt[d][warp] += __popc(peers);
+  }
+  __syncthreads();
+  {  // exclusive scan of cnt in (digit, warp) order: 8 entries per thread
+    int* flat = &S.cnt[0][0];
+    const int i0 = threadIdx.x * 8;
+    int loc[8], sum = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { loc[i] = flat[i0 + i]; sum += loc[i]; }
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += n;
+    }
+    if (lane == 31) S.red[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const int v = S.red[lane];
+      int w = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int n = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += n;
+      }
+      S.red[lane] = w - v;
+    }
+    __syncthreads();
+    int acc = S.red[warp] + incl - sum;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { flat[i0 + i] = acc; acc += loc[i]; }
+  }
+  __syncthreads();
+  for (int base = s0; base < s1; base += 32) {
+    const int s = base + lane;
+    const bool act = s < s1;
+    const int32_t val = act ? (src ? src[s] : s) : 0;
+    const int d = act ? ((key[val] >> shift) & 255) : 256 + lane;
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const int below = __popc(peers & lanemask_lt());
+    int off = 0;
+    if (act) off = S.cnt[d][warp];
+    __syncwarp();
+    if (act) {
+      dst[off + below] = val;
+      if (sorted_key) sorted_key[off + below] = key[val];
+      if (below == 0) S.cnt[d][warp] = off + __popc(peers);
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+}
+
+// Kernel 1 (one CTA per slice): keys cached in shared memory, stable LSD radix
+// passes -> perm; the final pass also writes the sorted ids.  With one pass (ids <
+// 256, every bench / LM bucket count) the pass's digit offsets ARE the bucket runs:
+// bounds[bh][g] = first slot of bucket g, bounds[bh][256] = T.  bounds[bh][0] = -1
+// flags a multi-pass sort (the finishing kernel then searches the sorted ids).
+__global__ void __launch_bounds__(kSortThreads) hash_prepare_sort_kernel(
+    const void* hash, int hdt, int T, int T_pad, int64_t H, int64_t sb, int64_t st, int64_t sh, int32_t* perm,
+    int32_t* scratch, int32_t* sorted_hash, int32_t* err) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  PrepSmem& S = *reinterpret_cast<PrepSmem*>(dsm);
+  int32_t* key = reinterpret_cast<int32_t*>(dsm + sizeof(PrepSmem));
+  const int64_t bh = blockIdx.x;
+  const int64_t b = bh / H, h = bh % H;
+  const int64_t hbase = b * sb + h * sh;
+
+  constexpr int kMaxPer = kPrepMaxT / kSortThreads;
+  long long v[kMaxPer];
+#pragma unroll
+  for (int i = 0; i < kMaxPer; ++i) {  // all loads in flight before any use
+    const int t = threadIdx.x + i * kSortThreads;
+    v[i] = t < T ? load_int(hash, hdt, hbase + t * st) : 0;
+  }
+  long long mh = 0;
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < kMaxPer; ++i) {
+    const int t = threadIdx.x + i * kSortThreads;
+    if (t < T) {
+      bad |= (v[i] < 0 || v[i] > 0x7fffffffLL);
+      const long long c = v[i] < 0 ? 0 : (v[i] > 0x7fffffffLL ? 0x7fffffffLL : v[i]);
+      key[t] = static_cast<int32_t>(c);
+      mh = max(mh, c);
+    }
+  }
+  if (bad) flag_error(err, SCFA_ERR_SHAPE);
+  if (threadIdx.x == 0) S.mx = 0;
+  __syncthreads();
+  atomicMax(reinterpret_cast<unsigned long long*>(&S.mx), static_cast<unsigned long long>(mh));
+  __syncthreads();
+  int passes = 0;
+  for (long long m = S.mx; m > 0; m >>= 8) ++passes;
+
+  int32_t* P = perm + bh * T;
+  int32_t* X = scratch + bh * (T + 257);  // radix ping-pong, then the slice's bucket bounds
+  int32_t* bounds = X + T;
+  int32_t* SH = sorted_hash + bh * T_pad;
+  if (passes == 0) {
+    for (int s = threadIdx.x; s < T; s += blockDim.x) { P[s] = s; SH[s] = 0; }
+    if (threadIdx.x <= 256) bounds[threadIdx.x] = (threadIdx.x == 0) ? 0 : T;
+    return;
+  }
+  for (int p = 0; p < passes; ++p) {  // the final pass lands in perm; pass 0 reads the identity
+    const bool last = p == passes - 1;
+    const bool to_perm = ((passes - 1 - p) & 1) == 0;
+    radix_pass(S, key, T, 8 * p, p == 0 ? nullptr : (to_perm ? X : P), to_perm ? P : X, last ? SH : nullptr);
+  }
+  // radix_pass leaves each digit's end offset in S.cnt[d][31] (after the last walk)
+  if (threadIdx.x < 256) {
+    const int start = threadIdx.x == 0 ? 0 : S.cnt[threadIdx.x - 1][31];
+    bounds[threadIdx.x] = (passes == 1) ? start : -1;
+  }
+  if (threadIdx.x == 0) bounds[256] = T;
+}
+
+// Kernel 2 (one thread per slot, all slices): sorted vectors, rank and visibility runs.
+// With shared ids and positions = arange a query slot s in bucket run [a, e) sees key
+// slots [a, s) ([a, s] without exclude_self); key slot s is seen by query slots (s, e).
+__global__ void __launch_bounds__(256) hash_prepare_finish_kernel(int T, int T_pad, int excl, const int32_t* perm,
+                                                                  const int32_t* scratch, int32_t* rank,
+                                                                  int32_t* q_idx, int32_t* k_idx, int32_t* q_hash,
+                                                                  int32_t* k_hash, int2* q_runs, int2* k_runs) {
+  const int64_t bh = blockIdx.y;
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= T_pad) return;
+  const size_t o = static_cast<size_t>(bh) * T_pad + s;
+  if (s >= T) {
+    q_idx[o] = kQueryPad;
+    k_idx[o] = kColOob;
+    q_hash[o] = kQHashOob;
+    k_hash[o] = kKHashOob;
+    q_runs[o] = make_int2(0, 0);
+    k_runs[o] = make_int2(0, 0);
+    return;
+  }
+  const int32_t t = perm[bh * T + s];
+  const int32_t g = q_hash[o];  // written sorted by kernel 1
+  int a, e;
+  const int32_t* bd = scratch + bh * (T + 257) + T;
+  if (bd[0] >= 0) {
+    a = bd[g];
+    e = bd[g + 1];
+  } else {  // multi-pass ids: search the sorted ids
+    const int32_t* sh = q_hash + static_cast<size_t>(bh) * T_pad;
+    int lo = 0, n = s;
+    while (n > 0) { const int hh = n >> 1; if (sh[lo + hh] < g) { lo += hh + 1; n -= hh + 1; } else n = hh; }
+    a = lo;
+    lo = s + 1; n = T - s - 1;
+    while (n > 0) { const int hh = n >> 1; if (sh[lo + hh] <= g) { lo += hh + 1; n -= hh + 1; } else n = hh; }
+    e = lo;
+  }
+  rank[bh * T + t] = s;
+  q_idx[o] = t;
+  k_idx[o] = t;
+  k_hash[o] = g;
+  q_runs[o] = make_int2(a, excl ? s : s + 1);
+  k_runs[o] = make_int2(excl ? s + 1 : s, e);
+}
+
 // ------------------------------------------------------------------ gather / scatter
+
+// Up to three row gathers sharing one permutation in one launch (Q | K | V).
+// Each 8-thread group moves one 128-byte row piece; a warp keeps 4 rows x 4
+// iterations of 16-byte loads in flight.
+struct GatherJobs {
+  const uint8_t* src[3];
+  uint8_t* dst[3];
+  const int32_t* perm[3];
+  int64_t sb[3], st[3], sh[3];
+  int64_t n_slots[3], T_perm[3];
+};
+
+__global__ void __launch_bounds__(256) gather_rows3_kernel(const __grid_constant__ GatherJobs J, int n_jobs, int eb,
+                                                           int64_t H, int64_t D, int64_t BH) {
+  const int64_t row_bytes = D * eb;
+  const int vecs = static_cast<int>(row_bytes / 16);
+  const int j = blockIdx.y;
+  const int64_t n_rows = BH * J.n_slots[j];
+  const int64_t total = n_rows * vecs;
+  const uint8_t* __restrict__ src = J.src[j];
+  uint8_t* __restrict__ dst = J.dst[j];
+  const int32_t* __restrict__ perm = J.perm[j];
+  const int64_t n_slots = J.n_slots[j], T_perm = J.T_perm[j], sb = J.sb[j], st = J.st[j], sh = J.sh[j];
+  constexpr int U = 4;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t g0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g0 < total; g0 += stride * U) {
+    uint4 v[U];
+    int64_t doff[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t g = g0 + u * stride;
+      doff[u] = -1;
+      if (g < total) {
+        const int64_t r = g / vecs;
+        const int c = static_cast<int>(g - r * vecs);
+        const int64_t bh = r / n_slots, s = r - bh * n_slots;
+        const int64_t b = bh / H, h = bh - b * H;
+        const int64_t t = __ldg(perm + bh * T_perm + s);
+        v[u] = __ldg(reinterpret_cast<const uint4*>(src + (b * sb + t * st + h * sh) * eb) + c);
+        doff[u] = r * row_bytes + c * 16;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (doff[u] >= 0) *reinterpret_cast<uint4*>(dst + doff[u]) = v[u];
+  }
+}
 
 __global__ void gather_rows_kernel(const uint8_t* __restrict__ src, int eb, int64_t H, int64_t D, int64_t sb,
                                    int64_t st, int64_t sh, const int32_t* __restrict__ perm, int64_t T_perm,
@@ -486,6 +741,66 @@ extern "C" int scfa_hash_sort(const void* hash, int hash_dtype, int64_t B, int64
   hash_sort_kernel<<<static_cast<unsigned>(B * H), kSortThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       hash, hash_dtype, T, H, sb, st, sh, pos, pos_dtype, ps_bh, ps_t, perm, rank, scratch, err_flag);
   return check_launch("hash_sort");
+}
+
+extern "C" int scfa_hash_prepare(const void* hash, int hash_dtype, int64_t B, int64_t T, int64_t H, int64_t sb,
+                                 int64_t st, int64_t sh, int flags, int32_t* perm, int32_t* rank, int32_t* scratch,
+                                 int32_t* q_idx, int32_t* k_idx, int32_t* q_hash, int32_t* k_hash, int32_t* q_runs,
+                                 int32_t* k_runs, int32_t* err_flag, void* stream) {
+  if (T > kPrepMaxT) { set_error("hash_prepare: T > %d (use scfa_hash_sort)", kPrepMaxT); return SCFA_ERR_SHAPE; }
+  if (B * H == 0 || T == 0) return SCFA_OK;
+  if (B * H > 65535) { set_error("hash_prepare: too many (b, h) slices"); return SCFA_ERR_SHAPE; }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int T_pad = static_cast<int>((T + 127) / 128) * 128;
+  const size_t smem = sizeof(PrepSmem) + static_cast<size_t>(T) * 4;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(hash_prepare_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(sizeof(PrepSmem) + kPrepMaxT * 4)) != cudaSuccess)
+      return check_launch("hash_prepare attribute");
+    attr = true;
+  }
+  hash_prepare_sort_kernel<<<static_cast<unsigned>(B * H), kSortThreads, smem, s>>>(
+      hash, hash_dtype, static_cast<int>(T), T_pad, H, sb, st, sh, perm, scratch, q_hash, err_flag);
+  int rc = check_launch("hash_prepare_sort");
+  if (rc) return rc;
+  dim3 grid(static_cast<unsigned>((T_pad + 255) / 256), static_cast<unsigned>(B * H));
+  hash_prepare_finish_kernel<<<grid, 256, 0, s>>>(static_cast<int>(T), T_pad, (flags & SCFA_FLAG_EXCLUDE_SELF) ? 1 : 0,
+                                                  perm, scratch, rank, q_idx, k_idx, q_hash, k_hash,
+                                                  reinterpret_cast<int2*>(q_runs), reinterpret_cast<int2*>(k_runs));
+  return check_launch("hash_prepare_finish");
+}
+
+extern "C" int scfa_gather_rows3(int n, const void* const* srcs, void* const* dsts, const int32_t* const* perms,
+                                 const int64_t* strides, int elem_bytes, int64_t B, int64_t H, int64_t D,
+                                 const int64_t* T_perm, const int64_t* n_slots, void* stream) {
+  if (n < 1 || n > 3) { set_error("gather_rows3: 1 to 3 tensors"); return SCFA_ERR_PARAM; }
+  if ((D * elem_bytes) % 16 != 0) { set_error("row bytes must be a multiple of 16"); return SCFA_ERR_SHAPE; }
+  GatherJobs J{};
+  int64_t most = 0;
+  for (int i = 0; i < n; ++i) {
+    J.src[i] = static_cast<const uint8_t*>(srcs[i]);
+    J.dst[i] = static_cast<uint8_t*>(dsts[i]);
+    J.perm[i] = perms[i];
+    J.sb[i] = strides[3 * i];
+    J.st[i] = strides[3 * i + 1];
+    J.sh[i] = strides[3 * i + 2];
+    J.T_perm[i] = T_perm[i];
+    J.n_slots[i] = n_slots[i];
+    if (((J.sb[i] | J.st[i] | J.sh[i]) * elem_bytes) % 16 != 0 || (reinterpret_cast<uintptr_t>(srcs[i]) & 15) ||
+        (reinterpret_cast<uintptr_t>(dsts[i]) & 15)) {
+      set_error("gather rows must be 16-byte aligned");
+      return SCFA_ERR_SHAPE;
+    }
+    most = n_slots[i] > most ? n_slots[i] : most;
+  }
+  const int64_t work = B * H * most * (D * elem_bytes / 16);
+  if (work == 0) return SCFA_OK;
+  int64_t g = (work + 256 * 4 - 1) / (256 * 4);
+  if (g > 148 * 16) g = 148 * 16;
+  dim3 grid(static_cast<unsigned>(g), static_cast<unsigned>(n));
+  gather_rows3_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(J, n, elem_bytes, H, D, B * H);
+  return check_launch("gather_rows3");
 }
 
 extern "C" int scfa_gather_rows(const void* src, int elem_bytes, int64_t B, int64_t H, int64_t D, int64_t sb,

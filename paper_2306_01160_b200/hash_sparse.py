@@ -158,7 +158,48 @@ def _scatter(src, rank, layout, out_dtype=None):
     return out
 
 
-def _sort_batch(q, k, v, q_hash, k_hash, layout, q_pos=None, k_pos=None, check=True):
+def _gather3(xs, perms, layout):
+    """Rows of up to three tensors ('bthd' or 'bhtd') in their perm order, one launch."""
+    outs, strides = [], []
+    for x, perm in zip(xs, perms):
+        if layout == "bthd":
+            B, T, H, D = x.shape
+            strides += [x.stride(0), x.stride(1), x.stride(2)]
+        else:
+            B, H, T, D = x.shape
+            strides += [x.stride(0), x.stride(2), x.stride(1)]
+        outs.append(torch.empty((B, H, perm.shape[1], D), dtype=x.dtype, device=x.device))
+    n = len(xs)
+    _lib.call("scfa_gather_rows3", n, _lib.ptr_array(xs), _lib.ptr_array(outs), _lib.ptr_array(perms),
+              _lib.i64_array(strides), xs[0].element_size(), B, H, D,
+              _lib.i64_array([p.shape[1] for p in perms]), _lib.i64_array([p.shape[1] for p in perms]),
+              _lib.stream_ptr())
+    return outs
+
+
+_PREP_MAX_T = 16384
+
+
+def _prepare_shared(hash_t, sb, st, sh, B, H, T, D, err, exclude_self):
+    """Fused sort + sorted vectors + visibility runs for shared bucket ids (scfa_hash_prepare)."""
+    dev = hash_t.device
+    BH, T_pad = B * H, pad128(T)
+    perm = torch.empty((BH, T), dtype=torch.int32, device=dev)
+    rank = torch.empty((BH, T), dtype=torch.int32, device=dev)
+    scratch = torch.empty((BH, T + 257), dtype=torch.int32, device=dev)
+    vec = torch.empty((4, BH, T_pad), dtype=torch.int32, device=dev)
+    runs = torch.empty((2, BH, T_pad, 2), dtype=torch.int32, device=dev)
+    flags = _lib.FLAG_HASH | (_lib.FLAG_EXCLUDE_SELF if exclude_self else 0)
+    _lib.call("scfa_hash_prepare", _lib.ptr(hash_t), _lib.dtype_code(hash_t), B, T, H, sb, st, sh, flags,
+              _lib.ptr(perm), _lib.ptr(rank), _lib.ptr(scratch), _lib.ptr(vec[0]), _lib.ptr(vec[1]),
+              _lib.ptr(vec[2]), _lib.ptr(vec[3]), _lib.ptr(runs[0]), _lib.ptr(runs[1]), _lib.ptr(err),
+              _lib.stream_ptr())
+    problem = Problem(B, H, T, T, D, vec[0], vec[1], vec[2], vec[3], flags=flags)
+    problem.set_runs(runs[0], runs[1])
+    return perm, rank, problem
+
+
+def _sort_batch(q, k, v, q_hash, k_hash, layout, q_pos=None, k_pos=None, check=True, exclude_self=True):
     """Shared by sort_by_bucket (engine layout) and hash_sparse_attention (boundary layout)."""
     if layout == "bhtd":
         check_forward_operands(q, k, v)
@@ -180,19 +221,25 @@ def _sort_batch(q, k, v, q_hash, k_hash, layout, q_pos=None, k_pos=None, check=T
     else:
         kh, ksb, kst, ksh = _hash_view(torch.as_tensor(k_hash, device=dev), B, H, T_KV, hl)
     err = torch.zeros(1, dtype=torch.int32, device=dev)
-    q_perm, q_rank = _sort(qh, qsb, qst, qsh, B, H, T_Q, err, q_pos)
-    if same:
+    if same and 0 < T_Q <= _PREP_MAX_T:
+        q_perm, q_rank, problem = _prepare_shared(qh, qsb, qst, qsh, B, H, T_Q, D, err, exclude_self)
         k_perm, k_rank = q_perm, q_rank
+        if check and int(err.item()):
+            raise ShapeError("bucket ids must be non-negative (and < 2**31)")
+        q_s, k_s, v_s = _gather3([q, k, v], [q_perm, q_perm, q_perm], layout)
+        qi, ki, qhs, khs = problem.q_idx, problem.k_idx, problem.q_hash, problem.k_hash
     else:
-        k_perm, k_rank = _sort(kh, ksb, kst, ksh, B, H, T_KV, err, k_pos)
-    if check and int(err.item()):
-        raise ShapeError("bucket ids must be non-negative (and < 2**31)")
-    q_s = _gather(q, q_perm, layout)
-    k_s = _gather(k, k_perm, layout)
-    v_s = _gather(v, k_perm, layout)
-    qi, qhs = _aux(q_perm, qh, qsb, qst, qsh, B, H, T_Q, _OOB_QI, _OOB_QH, q_pos)
-    ki, khs = _aux(k_perm, kh, ksb, kst, ksh, B, H, T_KV, _OOB_KI, _OOB_KH, k_pos)
-    problem = Problem(B, H, T_Q, T_KV, D, qi, ki, qhs, khs, flags=_lib.FLAG_HASH)
+        q_perm, q_rank = _sort(qh, qsb, qst, qsh, B, H, T_Q, err, q_pos)
+        if same:
+            k_perm, k_rank = q_perm, q_rank
+        else:
+            k_perm, k_rank = _sort(kh, ksb, kst, ksh, B, H, T_KV, err, k_pos)
+        if check and int(err.item()):
+            raise ShapeError("bucket ids must be non-negative (and < 2**31)")
+        q_s, k_s, v_s = _gather3([q, k, v], [q_perm, k_perm, k_perm], layout)
+        qi, qhs = _aux(q_perm, qh, qsb, qst, qsh, B, H, T_Q, _OOB_QI, _OOB_QH, q_pos)
+        ki, khs = _aux(k_perm, kh, ksb, kst, ksh, B, H, T_KV, _OOB_KI, _OOB_KH, k_pos)
+        problem = Problem(B, H, T_Q, T_KV, D, qi, ki, qhs, khs, flags=_lib.FLAG_HASH)
     return SortedBatch(
         q=q_s, k=k_s, v=v_s,
         q_idx=qi[:, :T_Q].view(B, H, T_Q), k_idx=ki[:, :T_KV].view(B, H, T_KV),
@@ -281,7 +328,7 @@ def hash_sparse_attention(q, k, v, q_hash, k_hash, scale=None, blocks=BlockSpec(
     position (hash_scatter + from_heads fused).
     """
     q, k, v = as_operand(q), as_operand(k), as_operand(v)
-    sb = _sort_batch(q, k, v, q_hash, k_hash, "bthd")
+    sb = _sort_batch(q, k, v, q_hash, k_hash, "bthd", exclude_self=exclude_self)
     prob = _problem_of(sb, exclude_self)
     return attention_forward(prob, sb.q, sb.k, sb.v, scale, blocks, boundary=(q.shape[1], False)).O
 
@@ -295,8 +342,9 @@ def hash_sparse_attention_fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, ex
     permutations are fused into the kernels' loads (sorted copies) and epilogues.
     """
     q, k, v = as_operand(q), as_operand(k), as_operand(v)
-    sb = _sort_batch(q, k, v, q_hash, k_hash, "bthd", check=False)
+    sb = _sort_batch(q, k, v, q_hash, k_hash, "bthd", check=False, exclude_self=exclude_self)
     prob = _problem_of(sb, exclude_self)
+    prob.schedule("fwd", "dq", "dkdv")  # runs + all three tile lists in one pass
     T_Q, T_KV = q.shape[1], k.shape[1]
     outputs = attention_forward(prob, sb.q, sb.k, sb.v, scale, boundary=(T_Q, False))
     dq, dk, dv = attention_backward(prob, sb.q, sb.k, sb.v, outputs, as_operand(d_out), scale,

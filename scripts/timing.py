@@ -29,6 +29,7 @@ hb = torch.from_numpy(buckets).to(dev)
 T = cfg["T"]
 sb = hs._sort_batch(q, k, v, hb, hb, "bthd", check=False)
 prob = hs._problem_of(sb, True)
+prob.schedule("fwd", "dq", "dkdv")
 for _ in range(3):
     out = attention_forward(prob, sb.q, sb.k, sb.v, boundary=(T, False))
     g = attention_backward(prob, sb.q, sb.k, sb.v, out, dO, boundary=(T, T, False))

@@ -67,7 +67,7 @@ def test_hash_runs_and_lists(T, nb, excl, seed):
     dev = torch.device("cuda")
     x = torch.zeros((B, T, H, D), dtype=torch.bfloat16, device=dev)
     h = torch.from_numpy(scfa.random_buckets(B, T, H, nb, seed)).to(dev)
-    sb = hs._sort_batch(x, x, x, h, h, "bthd")
+    sb = hs._sort_batch(x, x, x, h, h, "bthd", exclude_self=excl)
     prob = hs._problem_of(sb, excl)
     qi = sb.q_idx.cpu().numpy().reshape(B * H, T)
     qh = sb.q_hash.cpu().numpy().reshape(B * H, T)
@@ -114,3 +114,30 @@ def test_dense_runs_and_lists():
     prob = causal_problem(1, 1, T, 64, torch.device("cuda"))
     vis = orc.visibility(np.arange(T), np.arange(T))[None]
     _check_problem(prob, vis)
+
+
+@pytest.mark.parametrize("T,nb,excl,seed", [(300, 4, True, 0), (2048, 16, False, 1), (4096, 300, True, 2),
+                                            (1000, 1, True, 3)])
+def test_fused_prepare_matches_general_path(T, nb, excl, seed):
+    """scfa_hash_prepare (shared ids) == hash_sort + build_aux + runs_kernel, bit for bit."""
+    from paper_2306_01160_b200._kernel import Problem
+
+    B, H, D = 2, 3, 64
+    dev = torch.device("cuda")
+    x = torch.zeros((B, T, H, D), dtype=torch.bfloat16, device=dev)
+    h = torch.from_numpy(scfa.random_buckets(B, T, H, nb, seed)).to(dev)
+    sb = hs._sort_batch(x, x, x, h, h, "bthd", exclude_self=excl)
+    fused = sb.problem
+    # reference order: stable argsort of the bucket ids per (b, h)
+    want = np.argsort(h.cpu().numpy().transpose(0, 2, 1).reshape(B * H, T), axis=1, kind="stable")
+    assert np.array_equal(sb.q_perm.cpu().numpy(), want)
+    assert np.array_equal(sb.q_rank.cpu().numpy(), np.argsort(want, axis=1))
+    flags = fused.flags
+    general = Problem(B, H, T, T, D, fused.q_idx.clone(), fused.k_idx.clone(), fused.q_hash.clone(),
+                      fused.k_hash.clone(), flags=flags)
+    g = general.schedule("fwd", "dq", "dkdv")
+    f = fused.schedule("fwd", "dq", "dkdv")
+    for key in ("q_runs", "k_runs"):
+        assert torch.equal(g[key], f[key]), key
+    for name in ("fwd", "dq", "dkdv"):
+        assert torch.equal(g[name][1], f[name][1]), name
