@@ -179,11 +179,7 @@ def run_ours(args, cfg):
     flops_step = 14.0 * D * p_live
 
     def step(q, k, v, hb, dO):
-        sb = hs._sort_batch(q, k, v, hb, hb, "bthd", check=False, exclude_self=cfg["exclude_self"])
-        prob = hs._problem_of(sb, cfg["exclude_self"])
-        prob.schedule("fwd", "dq", "dkdv")
-        out = attention_forward(prob, sb.q, sb.k, sb.v, boundary=(T, False))
-        dq, dk, dv = attention_backward(prob, sb.q, sb.k, sb.v, out, dO, boundary=(T, T, False))
+        out, dq, dk, dv, prob = hs._fwd_bwd(q, k, v, hb, hb, dO, exclude_self=cfg["exclude_self"])
         return (out.O, dq, dk, dv), prob
 
     def barrier():

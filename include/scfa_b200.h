@@ -88,11 +88,21 @@ int scfa_hash_sort(const void* hash, int hash_dtype, int64_t B, int64_t T, int64
  * the visibility runs for `flags` (SCFA_FLAG_EXCLUDE_SELF).  T <= 16384.
  * perm/rank (B*H, T); scratch (B*H, T + 257); q_idx/k_idx/q_hash/k_hash (B*H, T_pad) with the
  * same sentinels as scfa_build_aux; q_runs/k_runs (B*H, T_pad) int32 pairs as
- * scfa_build_schedule (pass runs_ready = 3 there).                           */
+ * scfa_build_schedule (pass runs_ready = 3 there); rows (optional, B*H x T_pad) the
+ * scfa_row_map table of the sorted order for gather-mode attention.          */
 int scfa_hash_prepare(const void* hash, int hash_dtype, int64_t B, int64_t T, int64_t H, int64_t sb,
                       int64_t st, int64_t sh, int flags, int32_t* perm, int32_t* rank, int32_t* scratch,
                       int32_t* q_idx, int32_t* k_idx, int32_t* q_hash, int32_t* k_hash, int32_t* q_runs,
-                      int32_t* k_runs, int32_t* err_flag, void* stream);
+                      int32_t* k_runs, int32_t* rows, int32_t* err_flag, void* stream);
+
+/* Row tables for the gather-mode attention kernels: rows[bh, s] = (b * T_src + perm[bh, s])
+ * * H + h, the row of slot s of slice bh = (b, h) in a (B, T_src, H, D) tensor viewed as
+ * [B*T_src*H, D]; slots s >= n_slots (up to T_pad) repeat the row of slot 0.  This is the
+ * gather of compact() / sort_by_bucket (qk_sparse.py:68-70, hash_sparse.py:122-125) and the
+ * inverse scatter of qk_postprocess / hash_scatter as an index table instead of a copy.
+ * perm (B*H, T_perm) int32; rows (B*H, T_pad) int32.                               */
+int scfa_row_map(const int32_t* perm, int64_t B, int64_t H, int64_t T_perm, int64_t n_slots,
+                 int64_t T_pad, int64_t T_src, int32_t* rows, void* stream);
 
 /* ---------------------------------------------------------------- gather / scatter
  * Row gather into engine layout (compact(...) take_along_axis, qk_sparse.py:68-70;
@@ -175,7 +185,8 @@ int scfa_validate_sorted(const int32_t* idx, const int32_t* hash, int64_t BH, in
  *   dq  : query rows in 128-row blocks x 64-key tiles    (scfa_attn_bwd_dq)
  *   dkdv: key rows in 128-row blocks x 64-query tiles    (scfa_attn_bwd_dkdv)
  * list_* (B*H, n_row_blocks, stride_*) with stride >= n_col_blocks; count_*
- * (B*H, n_row_blocks) int32.  A NULL list skips that list.  tiles[3] (may be
+ * (B*H * n_row_blocks + 2) int32: the counts, then a work-counter pair the attention
+ * kernels use to hand out items dynamically (zeroed here, left zero by every launch).  A NULL list skips that list.  tiles[3] (may be
  * NULL) accumulates the listed-tile totals.  flags: SCFA_FLAG_*.            */
 int scfa_build_schedule(const int32_t* q_idx, const int32_t* q_hash, const int32_t* k_idx,
                         const int32_t* k_hash, int64_t BH, int64_t T_q, int64_t T_kv, int64_t Tq_pad,
@@ -207,12 +218,18 @@ int scfa_ref_schedule(const int32_t* q_idx, const int32_t* q_hash, const int32_t
  * Output layout: out_boundary = 0 writes o as (B*H, T_q, D); out_boundary = 1 writes
  * row s of slice (b, h) to o[b, q_idx[bh, s], h, :] of a (B, T_out, H, D) tensor (H
  * heads) — the inverse scatter of qk_postprocess / hash_scatter fused into the
- * epilogue; pad rows (q_idx outside [0, T_out)) are not written.                  */
+ * epilogue; pad rows (q_idx outside [0, T_out)) are not written.
+ * Row tables (gather mode, ABI 3): with q_rows != NULL, q is a [R_q, D] row table (e.g. the
+ * caller's (B, T, H, D) tensor, R_q = B*T*H) and slot s of slice bh is row q_rows[bh, s]
+ * ((B*H, Tq_pad) int32, from scfa_row_map / scfa_hash_prepare); O is written to the same rows
+ * of the [R_q, D] table `o` (this replaces out_boundary).  Likewise k_rows for k / v.  The
+ * operands are then loaded with TMA tile::gather4: no compacted / sorted copies exist.  */
 int scfa_attn_fwd(const void* q, const void* k, const void* v, int64_t BH, int64_t T_q,
                   int64_t T_kv, int64_t D, const int32_t* q_idx, const int32_t* q_runs,
                   int64_t Tq_pad, int64_t Tkv_pad, const uint16_t* list, const int32_t* list_count,
                   int64_t list_stride, float scale, int64_t H, int64_t T_out, int out_boundary,
-                  void* o, float* m, float* l, float* lse2, void* stream);
+                  void* o, float* m, float* l, float* lse2, const int32_t* q_rows,
+                  const int32_t* k_rows, int64_t R_q, int64_t R_kv, void* stream);
 
 /* delta = rowsum(dO * O) (qk_sparse.py:168, hash_sparse.py:194, dense.py:81);
  * lse2 rebuilt from (M, L) when lse2_in is NULL (m_hat/inv_l, _kernel.py:152-154).
@@ -227,23 +244,30 @@ int scfa_bwd_prep(const void* o, const void* d_out, const float* lse2_in, const 
 
 /* Backward pass 1 (dQ, query-block owner, _kernel.py:173-179).  q_runs, list_dq,
  * count_dq from scfa_build_schedule.  dq (B*H, T_q, D) f32, or (B, T_out, H, D)
- * scattered by q_idx when out_boundary (as scfa_attn_fwd).                          */
+ * scattered by q_idx when out_boundary (as scfa_attn_fwd), or the rows q_rows of a
+ * [R_q, D] f32 table in gather mode (q / d_out row tables as in scfa_attn_fwd).
+ * o != NULL fuses the delta pass: delta = rowsum(dO * O) (qk_sparse.py:168) is computed
+ * per query slot from the O rows (addressed like d_out) and written to delta_out
+ * (B*H, Tq_pad) for scfa_attn_bwd_dkdv; `delta` is then ignored.                    */
 int scfa_attn_bwd_dq(const void* q, const void* k, const void* v, const void* d_out, int64_t BH,
                      int64_t T_q, int64_t T_kv, int64_t D, const int32_t* q_idx,
                      const int32_t* q_runs, int64_t Tq_pad, int64_t Tkv_pad, const float* lse2,
                      const float* delta, const uint16_t* list, const int32_t* list_count,
                      int64_t list_stride, float scale, int64_t H, int64_t T_out, int out_boundary,
-                     float* dq, void* stream);
+                     float* dq, const int32_t* q_rows, const int32_t* k_rows, int64_t R_q,
+                     int64_t R_kv, const void* o, float* delta_out, void* stream);
 
 /* Backward pass 2 (dK/dV, key-block owner over the transposed schedule,
  * _kernel.py:181-192).  k_runs, list_dkdv, count_dkdv from scfa_build_schedule.
- * dk, dv (B*H, T_kv, D) f32, or (B, T_out, H, D) scattered by k_idx when out_boundary. */
+ * dk, dv (B*H, T_kv, D) f32, or (B, T_out, H, D) scattered by k_idx when out_boundary,
+ * or the rows k_rows of [R_kv, D] f32 tables in gather mode.                         */
 int scfa_attn_bwd_dkdv(const void* q, const void* k, const void* v, const void* d_out, int64_t BH,
                        int64_t T_q, int64_t T_kv, int64_t D, const int32_t* k_idx,
                        const int32_t* k_runs, int64_t Tq_pad, int64_t Tkv_pad, const float* lse2,
                        const float* delta, const uint16_t* list, const int32_t* list_count,
                        int64_t list_stride, float scale, int64_t H, int64_t T_out, int out_boundary,
-                       float* dk, float* dv, void* stream);
+                       float* dk, float* dv, const int32_t* q_rows, const int32_t* k_rows,
+                       int64_t R_q, int64_t R_kv, void* stream);
 
 /* ---------------------------------------------------------------- diagnostics
  * Route per-tile clock64 stamps of subsequent attention launches into `buf`

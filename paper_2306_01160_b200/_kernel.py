@@ -68,6 +68,7 @@ class Problem:
         self.B, self.H, self.T_q, self.T_kv, self.D = int(B), int(H), int(T_q), int(T_kv), int(D)
         self.q_idx, self.k_idx, self.q_hash, self.k_hash = q_idx, k_idx, q_hash, k_hash
         self.flags = int(flags)
+        self.rows = None  # RowTables for gather-mode kernels, when the operands stay in (B, T, H, D)
         self._lists = {}
         self._tiles_total = None
 
@@ -122,7 +123,9 @@ class Problem:
                     n_rb = max(-(-T_rows // 128), 1)
                     stride = max(-(-T_cols // cb), 1)
                     lst = torch.empty((self.BH, n_rb, stride), dtype=torch.int16, device=dev)
-                    cnt = torch.zeros((self.BH, n_rb), dtype=torch.int32, device=dev)
+                    # counts (BH, n_rb) + the attention kernels' work counter pair
+                    cnt = torch.zeros(self.BH * n_rb + 2, dtype=torch.int32, device=dev)[: self.BH * n_rb].view(
+                        self.BH, n_rb)  # same base address; the pair lives past the view
                     self._lists[name] = (lst, cnt, stride)
                     args += [_lib.ptr(lst), _lib.ptr(cnt), stride]
                 else:
@@ -134,6 +137,7 @@ class Problem:
                 self.BH, self.T_q, self.T_kv, self.Tq_pad, self.Tkv_pad, self.flags,
                 _lib.ptr(self._lists.get("q_runs")), _lib.ptr(self._lists.get("k_runs")), ready,
                 *args, _lib.ptr(self._tiles_total), _lib.stream_ptr(),
+                kernels=(0 if ready == 3 else 1) + 1,
             )
         return self._lists
 
@@ -219,16 +223,36 @@ def _zeros_or_empty(shape, dtype, dev, zero):
     return torch.zeros(shape, dtype=dtype, device=dev) if zero else torch.empty(shape, dtype=dtype, device=dev)
 
 
-def attention_forward(problem, q, k, v, scale=None, blocks=None, boundary=None):
+class RowTables:
+    """Gather-mode addressing (scfa_row_map): slot s of slice bh lives at row q_rows[bh, s]
+    of the caller's (B, T_Q, H, D) tensor viewed as [B*T_Q*H, D] (k_rows likewise)."""
+
+    def __init__(self, q_rows, k_rows, R_q, R_kv):
+        self.q_rows, self.k_rows, self.R_q, self.R_kv = q_rows, k_rows, int(R_q), int(R_kv)
+
+    def args(self):
+        return [_lib.ptr(self.q_rows), _lib.ptr(self.k_rows), self.R_q, self.R_kv]
+
+
+_NO_ROWS = [None, None, 0, 0]
+
+
+def attention_forward(problem, q, k, v, scale=None, blocks=None, boundary=None, rows=None):
     """Launch the forward kernel over the exact tile list; returns FlashOutputs.
 
     boundary=None: O is engine layout (B, H, T_q, D) in kernel (sorted/compacted) order.
     boundary=(T_out, zero_fill): the epilogue writes each row straight to its original
     position of a (B, T_out, H, D) tensor (fused inverse scatter); positions no row maps
     to are zero-filled first when zero_fill (QK drops).  M, L stay in kernel order.
+    rows=RowTables: q, k, v are the caller's (B, T, H, D) tensors, read by TMA gather4
+    through the row tables (no sorted copies); requires boundary.
     """
-    B, H, T_q, D = q.shape
-    T_kv = k.shape[2]
+    if rows is not None:
+        B, T_in, H, D = q.shape
+        T_q, T_kv = problem.T_q, problem.T_kv
+    else:
+        B, H, T_q, D = q.shape
+        T_kv = k.shape[2]
     dev = q.device
     if boundary is None:
         O = torch.empty((B, H, T_q, D), dtype=torch.bfloat16, device=dev)
@@ -248,24 +272,31 @@ def attention_forward(problem, q, k, v, scale=None, blocks=None, boundary=None):
             _lib.ptr(q), _lib.ptr(k), _lib.ptr(v), B * H, T_q, T_kv, D,
             _lib.ptr(problem.q_idx), _lib.ptr(sched["q_runs"]), problem.Tq_pad, problem.Tkv_pad,
             _lib.ptr(lst), _lib.ptr(cnt), stride, _scale(scale, D), H, T_out, out_b,
-            _lib.ptr(O), _lib.ptr(M), _lib.ptr(L), _lib.ptr(lse2), _lib.stream_ptr(),
+            _lib.ptr(O), _lib.ptr(M), _lib.ptr(L), _lib.ptr(lse2),
+            *(rows.args() if rows is not None else _NO_ROWS), _lib.stream_ptr(),
         )
     out = FlashOutputs(O, M, L, problem=problem, blocks=blocks, lse2=lse2)
     out._boundary = boundary
     return out
 
 
-def attention_backward(problem, q, k, v, outputs, d_out, scale=None, boundary=None):
+def attention_backward(problem, q, k, v, outputs, d_out, scale=None, boundary=None, rows=None):
     """dQ, dK, dV (fp32) recomputing P from the saved statistics.
 
     boundary=None: d_out and outputs.O are engine layout in kernel order and the
     gradients come back the same way.  boundary=(T_q_out, T_kv_out, zero_fill):
     outputs.O and d_out are (B, T_q_out, H, D); dO is gathered into kernel order
     inside the delta pass, and dQ / dK / dV are written straight to their original
-    positions of (B, T_*_out, H, D) fp32 tensors.
+    positions of (B, T_*_out, H, D) fp32 tensors.  rows=RowTables: as attention_forward
+    (q, k, v, d_out, outputs.O all (B, T, H, D)); the delta pass is fused into the dQ
+    kernel and nothing is gathered or copied.
     """
-    B, H, T_q, D = q.shape
-    T_kv = k.shape[2]
+    if rows is not None:
+        B, _, H, D = q.shape
+        T_q, T_kv = problem.T_q, problem.T_kv
+    else:
+        B, H, T_q, D = q.shape
+        T_kv = k.shape[2]
     dev = q.device
     BH = B * H
     Tq_pad = pad128(T_q)
@@ -285,20 +316,28 @@ def attention_backward(problem, q, k, v, outputs, d_out, scale=None, boundary=No
         dk = _zeros_or_empty((B, Tkv_out, H, D), torch.float32, dev, zero)
         dv = _zeros_or_empty((B, Tkv_out, H, D), torch.float32, dev, zero)
         out_b = 1
-        d_sorted = torch.empty((B, H, T_q, D), dtype=torch.bfloat16, device=dev)
+        d_sorted = d_out if rows is not None else torch.empty((B, H, T_q, D), dtype=torch.bfloat16, device=dev)
     if BH == 0:
         return dq, dk, dv
     delta = torch.empty((BH, Tq_pad), dtype=torch.float32, device=dev)
-    lse2 = torch.empty((BH, Tq_pad), dtype=torch.float32, device=dev)
     lse_in = getattr(outputs, "_lse2", None)
-    M = outputs.M if lse_in is None else None
-    Lv = outputs.L if lse_in is None else None
-    if M is not None:
-        M = torch.as_tensor(M, device=dev).to(torch.float32).contiguous()
-        Lv = torch.as_tensor(Lv, device=dev).to(torch.float32).contiguous()
-    _lib.call("scfa_bwd_prep", _lib.ptr(O), _lib.ptr(d_out), _lib.ptr(lse_in), _lib.ptr(M), _lib.ptr(Lv),
-              BH, T_q, D, Tq_pad, _lib.ptr(problem.q_idx) if out_b else None, H, Tq_out,
-              _lib.ptr(d_sorted) if out_b else None, _lib.ptr(delta), _lib.ptr(lse2), _lib.stream_ptr())
+    rargs = rows.args() if rows is not None else _NO_ROWS
+    if lse_in is not None and (rows is not None or boundary is None):
+        lse2 = lse_in  # from our forward; delta is fused into the dQ kernel
+        fuse = True
+    else:
+        fuse = False
+        lse2 = torch.empty((BH, Tq_pad), dtype=torch.float32, device=dev)
+        M = outputs.M if lse_in is None else None
+        Lv = outputs.L if lse_in is None else None
+        if M is not None:
+            M = torch.as_tensor(M, device=dev).to(torch.float32).contiguous()
+            Lv = torch.as_tensor(Lv, device=dev).to(torch.float32).contiguous()
+        if rows is not None:
+            raise ShapeError("row-table backward needs the forward's saved log-sum-exp")
+        _lib.call("scfa_bwd_prep", _lib.ptr(O), _lib.ptr(d_out), _lib.ptr(lse_in), _lib.ptr(M), _lib.ptr(Lv),
+                  BH, T_q, D, Tq_pad, _lib.ptr(problem.q_idx) if out_b else None, H, Tq_out,
+                  _lib.ptr(d_sorted) if out_b else None, _lib.ptr(delta), _lib.ptr(lse2), _lib.stream_ptr())
     sched = problem.schedule("dq", "dkdv")
     if T_q > 0:
         lst, cnt, stride = sched["dq"]
@@ -307,7 +346,8 @@ def attention_backward(problem, q, k, v, outputs, d_out, scale=None, boundary=No
             _lib.ptr(q), _lib.ptr(k), _lib.ptr(v), _lib.ptr(d_sorted), BH, T_q, T_kv, D,
             _lib.ptr(problem.q_idx), _lib.ptr(sched["q_runs"]), problem.Tq_pad, problem.Tkv_pad,
             _lib.ptr(lse2), _lib.ptr(delta), _lib.ptr(lst), _lib.ptr(cnt), stride,
-            _scale(scale, D), H, Tq_out, out_b, _lib.ptr(dq), _lib.stream_ptr(),
+            _scale(scale, D), H, Tq_out, out_b, _lib.ptr(dq), *rargs,
+            _lib.ptr(O) if fuse else None, _lib.ptr(delta) if fuse else None, _lib.stream_ptr(),
         )
     if T_kv > 0:
         lst, cnt, stride = sched["dkdv"]
@@ -316,9 +356,25 @@ def attention_backward(problem, q, k, v, outputs, d_out, scale=None, boundary=No
             _lib.ptr(q), _lib.ptr(k), _lib.ptr(v), _lib.ptr(d_sorted), BH, T_q, T_kv, D,
             _lib.ptr(problem.k_idx), _lib.ptr(sched["k_runs"]), problem.Tq_pad, problem.Tkv_pad,
             _lib.ptr(lse2), _lib.ptr(delta), _lib.ptr(lst), _lib.ptr(cnt), stride,
-            _scale(scale, D), H, Tkv_out, out_b, _lib.ptr(dk), _lib.ptr(dv), _lib.stream_ptr(),
+            _scale(scale, D), H, Tkv_out, out_b, _lib.ptr(dk), _lib.ptr(dv), *rargs, _lib.stream_ptr(),
         )
     return dq, dk, dv
+
+
+def make_row_tables(q_perm, k_perm, B, H, T_q_slots, T_kv_slots, T_Q, T_KV, Tq_pad, Tkv_pad, shared=False):
+    """scfa_row_map for both sides (shared=True reuses the query table for keys)."""
+    dev = q_perm.device
+
+    def one(perm, n_slots, T_src, T_pad):
+        rows = torch.empty((B * H, T_pad), dtype=torch.int32, device=dev)
+        if B * H and n_slots:
+            _lib.call("scfa_row_map", _lib.ptr(perm), B, H, perm.shape[1], n_slots, T_pad, T_src, _lib.ptr(rows),
+                      _lib.stream_ptr())
+        return rows
+
+    qr = one(q_perm, T_q_slots, T_Q, Tq_pad)
+    kr = qr if shared else one(k_perm, T_kv_slots, T_KV, Tkv_pad)
+    return RowTables(qr, kr, B * T_Q * H, B * T_KV * H)
 
 
 def causal_j_stops(q_idx, k_idx, blocks=BlockSpec()):

@@ -43,7 +43,8 @@ _SIGS = {
     "scfa_hash_sort": [_P, _I, _L, _L, _L, _L, _L, _L, _P, _I, _L, _L, _P, _P, _P, _P, _P],
     "scfa_gather_rows": [_P, _I, _L, _L, _L, _L, _L, _L, _P, _L, _L, _P, _P],
     "scfa_gather_rows3": [_I, _P, _P, _P, _P, _I, _L, _L, _L, _P, _P, _P],
-    "scfa_hash_prepare": [_P, _I, _L, _L, _L, _L, _L, _L, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "scfa_hash_prepare": [_P, _I, _L, _L, _L, _L, _L, _L, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "scfa_row_map": [_P, _L, _L, _L, _L, _L, _L, _P, _P],
     "scfa_scatter_rows": [_P, _I, _L, _L, _L, _L, _P, _L, _P, _I, _L, _L, _L, _P],
     "scfa_build_aux": [_P, _P, _L, _L, _L, _L, _L, ctypes.c_int32, ctypes.c_int32, _P, _I, _L, _L, _L,
                        ctypes.c_int32, _P, _I, _L, _L, _P, _P, _P],
@@ -55,14 +56,14 @@ _SIGS = {
                             _L, _P, _P],
     "scfa_ref_schedule": [_P, _P, _P, _P, _L, _L, _L, _L, _L, _L, _L, _I, _P, _P, _P, _P],
     "scfa_attn_fwd": [_P, _P, _P, _L, _L, _L, _L, _P, _P, _L, _L, _P, _P, _L, _F, _L, _L, _I, _P, _P, _P, _P,
-                      _P],
+                      _P, _P, _L, _L, _P],
     "scfa_bwd_prep": [_P, _P, _P, _P, _P, _L, _L, _L, _L, _P, _L, _L, _P, _P, _P, _P],
     "scfa_attn_bwd_dq": [_P, _P, _P, _P, _L, _L, _L, _L, _P, _P, _L, _L, _P, _P, _P, _P, _L, _F, _L, _L, _I,
-                         _P, _P],
+                         _P, _P, _P, _L, _L, _P, _P, _P],
     "scfa_debug_timing": [_P, _L],
     "scfa_debug_ctas_per_sm": [_I, _L],
     "scfa_attn_bwd_dkdv": [_P, _P, _P, _P, _L, _L, _L, _L, _P, _P, _L, _L, _P, _P, _P, _P, _L, _F, _L, _L,
-                           _I, _P, _P, _P],
+                           _I, _P, _P, _P, _P, _L, _L, _P],
 }
 
 _lib = None
@@ -106,12 +107,12 @@ def raise_for(code, what=""):
 
 
 # kernels launched per successful call (for launch accounting in bench.py)
-KERNELS_PER_CALL = {"scfa_build_schedule": 2, "scfa_invert_index": 2}
+KERNELS_PER_CALL = {"scfa_build_schedule": 2, "scfa_invert_index": 2, "scfa_hash_prepare": 2}
 launches = 0
 EVENT_HOOK = None  # optional callable(name, phase) used by bench.py to time each entry point
 
 
-def call(name, *args):
+def call(name, *args, kernels=None):
     global launches
     if EVENT_HOOK is not None:
         EVENT_HOOK(name, 0)
@@ -119,7 +120,7 @@ def call(name, *args):
     if EVENT_HOOK is not None:
         EVENT_HOOK(name, 1)
     raise_for(rc, name)
-    launches += KERNELS_PER_CALL.get(name, 1)
+    launches += KERNELS_PER_CALL.get(name, 1) if kernels is None else kernels
 
 
 def ptr_array(tensors):

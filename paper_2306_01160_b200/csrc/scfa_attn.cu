@@ -19,9 +19,16 @@
 // Roles (192 threads):
 //   warps 0-3  : one thread per stationary row == TMEM lane.  Online softmax (fwd)
 //                or P / dS recompute (bwd) with packed fp32x2 math, and the epilogue.
-//   warp 4     : TMA producers.  Lane 0: stationary tiles + the y0 ring (K | K | Q
-//                with the per-column lse/delta of dK/dV); lane 1: the y1 ring (V | V | dO).
+//   warp 4     : TMA producer warp: stationary tiles, the y0 ring (K | K | Q with the
+//                per-column lse/delta of dK/dV) and the y1 ring (V | V | dO).  In
+//                gather mode every lane owns 4 rows of a tile and issues tile::gather4
+//                loads straight from the caller's (B, T, H, D) tensors (row tables), so
+//                no sorted / compacted copy of Q, K, V, dO is ever materialised.
 //   warp 5     : TMEM allocator + single-thread tcgen05.mma issuer.
+//
+// Epilogues stage the output rows in the item's (now idle) stationary slot and copy
+// them out so that each warp store covers whole rows, each row going straight to its
+// original position (the inverse scatter fused in).
 //
 // TMEM per CTA (256 columns at D = 64, two CTAs per SM; 512 at D = 128):
 //   FWD   S fp32 [0,128)  O [128,128+D)  P bf16 [128+D, 192+D)
@@ -72,9 +79,12 @@ struct Cfg {
   static constexpr int OFF_Y1 = OFF_Y0 + NS0 * Y_BYTES;
   static constexpr int OFF_AUX = OFF_Y1 + NS1 * Y_BYTES;
   static constexpr int OFF_BAR = OFF_AUX + NS0 * AUX_BYTES;
-  // s_full, s_free, p_full, p_free, acc_full, x_full/empty[NXS], y0_full/empty[NS0], y1_full/empty[NS1]
-  static constexpr int N_BARS = 5 + 2 * NXS + 2 * NS0 + 2 * NS1;
-  static constexpr int SMEM_BYTES = OFF_BAR + 8 * N_BARS + 16;
+  // s_full, s_free, p_full, p_free, acc_full, x_full/empty[NXS], y0_full/empty[NS0], y1_full/empty[NS1],
+  // q_full/empty[NQ] (work-item ring)
+  static constexpr int NQ = 4;
+  static constexpr int N_BARS = 5 + 2 * NXS + 2 * NS0 + 2 * NS1 + 2 * NQ;
+  static constexpr int OFF_RING = OFF_BAR + 8 * N_BARS;  // int2 {item, tiles} x NQ
+  static constexpr int SMEM_BYTES = OFF_RING + 8 * NQ + 16;
   static_assert(X_BYTES % 1024 == 0 && Y_BYTES % 1024 == 0, "TMA tiles must stay 1024-aligned");
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
 };
@@ -89,6 +99,10 @@ struct AttnArgs {
   const int2* row_runs;        // visible streamed-slot run [lo, hi) of each stationary row
   const float* lse2;           // (BH, Tq_pad), log2 domain; +inf where no key is visible
   const float* delta;          // (BH, Tq_pad)
+  const int* x_rows;  // gather mode: global row per stationary slot (BH, T_rows_pad); null = tiled loads
+  const int* y_rows;  // gather mode: global row per streamed slot (BH, T_cols_pad)
+  const __nv_bfloat16* o_src;  // DQ: O rows (addressed like dO) for the fused delta
+  float* delta_out;            // DQ: delta = rowsum(dO * O) per query slot (BH, T_rows_pad)
   const uint16_t* list;
   const int* list_count;
   int list_stride;
@@ -112,17 +126,23 @@ struct AttnArgs {
   if (threadIdx.x == 0) { SCFA_STAMP_AT(tg, k) }
 #define SCFA_MSTAMP(k) SCFA_STAMP_AT(tg, k)
 
-// Work item -> (bh, row block).  Items run heaviest row block first (largest causal
-// reach), cycling over heads, and CTAs take items round-robin.
-SCFA_DEVICE void decode_item(const AttnArgs& a, int w, int& bh, int& rb) {
-  rb = a.n_row_blocks - 1 - w / a.BH;
-  bh = w - (w / a.BH) * a.BH;
+// Work index -> item (bh * n_row_blocks + rb).  Items are handed out dynamically
+// (one atomic counter per launch, next to the tile counts) in the order: heaviest row
+// block first (largest causal reach), cycling over heads.
+SCFA_DEVICE int item_of(const AttnArgs& a, int w) {
+  const int rb = a.n_row_blocks - 1 - w / a.BH;
+  const int bh = w - (w / a.BH) * a.BH;
+  return bh * a.n_row_blocks + rb;
 }
 
 // Output row of stationary row `row` (original position `pos`): engine layout
 // (bh, row) or boundary layout (b, pos, h) — the fused inverse scatter.
 SCFA_DEVICE bool out_row(const AttnArgs& a, int bh, int row, int pos, size_t& off) {
   if (row >= a.T_rows) return false;
+  if (a.x_rows) {  // row tables: `pos` is the global row the stationary operand came from
+    off = static_cast<size_t>(pos);
+    return true;
+  }
   if (!a.out_boundary) {
     off = static_cast<size_t>(bh) * a.T_rows + row;
     return true;
@@ -206,7 +226,11 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
   uint64_t* bar_y0_empty = bar_y0_full + C::NS0;
   uint64_t* bar_y1_full = bar_y0_empty + C::NS0;
   uint64_t* bar_y1_empty = bar_y1_full + C::NS1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_BAR + 8 * C::N_BARS);
+  uint64_t* bar_q_full = bar_y1_empty + C::NS1;
+  uint64_t* bar_q_empty = bar_q_full + C::NQ;
+  int2* ring = reinterpret_cast<int2*>(smem + C::OFF_RING);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_RING + 8 * C::NQ);
+  int* work_ctr = const_cast<int*>(args.list_count) + args.n_items;  // [0] next item, [1] CTAs done
 
   if (threadIdx.x == 0) {
     if (smem_u32(smem) & 1023) __trap();  // TMA SWIZZLE_128B destinations need 1024-byte alignment
@@ -217,7 +241,7 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
     mbar_init(bar_acc_full, 1);
     for (int i = 0; i < C::NXS; ++i) {
       mbar_init(bar_x_full + i, 1);
-      mbar_init(bar_x_empty + i, 128);  // released by the row threads after the epilogue
+      mbar_init(bar_x_empty + i, 128);  // released by the row threads after the epilogue (staging)
     }
     for (int i = 0; i < C::NS0; ++i) {
       mbar_init(bar_y0_full + i, 1);
@@ -226,6 +250,10 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
     for (int i = 0; i < C::NS1; ++i) {
       mbar_init(bar_y1_full + i, 1);
       mbar_init(bar_y1_empty + i, 1);
+    }
+    for (int i = 0; i < C::NQ; ++i) {
+      mbar_init(bar_q_full + i, 1);
+      mbar_init(bar_q_empty + i, 1 + 128);  // the MMA thread + the row threads
     }
     fence_barrier_init();
   }
@@ -236,64 +264,116 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 4) {
-    // ------------------------------------------------------------ TMA producers
+    // ------------------------------------------------------------ TMA producer warp
     if (lane == 0) {
-      // stationary tiles + y0 ring (+ per-column lse2/delta for dK/dV)
       tma_prefetch_desc(&tm_x0);
       tma_prefetch_desc(&tm_y0);
+      tma_prefetch_desc(&tm_y1);
       if (C::NX == 2) tma_prefetch_desc(&tm_x1);
-      int tg = 0, ia = 0;
-      for (int w = blockIdx.x; w < args.n_items; w += gridDim.x) {
-        int bh, rb;
-        decode_item(args, w, bh, rb);
-        const int lb = bh * args.n_row_blocks + rb;
-        const int n = args.list_count[lb];
-        if (n == 0) continue;
-        const uint16_t* lst = args.list + static_cast<size_t>(lb) * args.list_stride;
-        const int xs = ia % C::NXS;
-        if (ia >= C::NXS) mbar_wait(bar_x_empty + xs, ((ia / C::NXS) - 1) & 1);
-        uint8_t* xb = smem + C::OFF_X + xs * C::XSLOT_BYTES;
+    }
+    const bool gx = args.x_rows != nullptr, gy = args.y_rows != nullptr;
+    int tg = 0, ia = 0;
+    // Work ring: item k+1 is grabbed and published before item k's tiles are loaded, so
+    // the consumers can always look one item ahead without waiting on the loads.
+    auto grab = [&](int k) -> int2 {
+      int2 e = make_int2(-1, 0);
+      if (lane == 0) {
+        const int w = atomicAdd(work_ctr, 1);
+        if (w < args.n_items) {
+          e.x = item_of(args, w);
+          e.y = args.list_count[e.x];
+        }
+        const int qs = k % C::NQ;
+        if (k >= C::NQ) mbar_wait(bar_q_empty + qs, ((k / C::NQ) - 1) & 1);
+        ring[qs] = e;
+        mbar_arrive(bar_q_full + qs);
+      }
+      e.x = __shfl_sync(0xffffffffu, e.x, 0);
+      e.y = __shfl_sync(0xffffffffu, e.y, 0);
+      return e;
+    };
+    int2 cur = grab(0);
+    for (int k = 0; cur.x >= 0; ++k) {
+      const int2 item = cur;
+      cur = grab(k + 1);
+      const int lb = item.x, n = item.y;
+      if (n == 0) continue;
+      const int bh = lb / args.n_row_blocks, rb = lb - bh * args.n_row_blocks;
+      const uint16_t* lst = args.list + static_cast<size_t>(lb) * args.list_stride;
+      const int xs = ia % C::NXS;
+      if (ia >= C::NXS) mbar_wait(bar_x_empty + xs, ((ia / C::NXS) - 1) & 1);
+      uint8_t* xb = smem + C::OFF_X + xs * C::XSLOT_BYTES;
+      if (lane == 0) {
         SCFA_STAMP_AT(tg, 10);
         mbar_arrive_expect_tx(bar_x_full + xs, C::XSLOT_BYTES);
+      }
+      __syncwarp();
+      if (gx) {  // 128 stationary rows: 4 per lane
+        const int4 r4 = __ldg(reinterpret_cast<const int4*>(args.x_rows + static_cast<size_t>(bh) * args.T_rows_pad +
+                                                          rb * C::BM) + lane);
+#pragma unroll
+        for (int c = 0; c < C::DCH; ++c) {
+          tma_gather4(xb + c * C::BM * 128 + lane * 512, &tm_x0, bar_x_full + xs, c * 64, r4.x, r4.y, r4.z, r4.w);
+          if (C::NX == 2)
+            tma_gather4(xb + C::X_BYTES + c * C::BM * 128 + lane * 512, &tm_x1, bar_x_full + xs, c * 64, r4.x, r4.y,
+                        r4.z, r4.w);
+        }
+      } else if (lane == 0) {
         for (int c = 0; c < C::DCH; ++c) {
           tma_load_3d(xb + c * C::BM * 128, &tm_x0, bar_x_full + xs, c * 64, rb * C::BM, bh);
           if (C::NX == 2) tma_load_3d(xb + C::X_BYTES + c * C::BM * 128, &tm_x1, bar_x_full + xs, c * 64, rb * C::BM, bh);
         }
-        for (int t = 0; t < n; ++t, ++tg) {
-          const int st = tg % C::NS0;
-          if (tg >= C::NS0) mbar_wait(bar_y0_empty + st, ((tg / C::NS0) - 1) & 1);
-          const int col0 = (lst[t] & 0x7fff) * C::BN;
-          uint8_t* yb = smem + C::OFF_Y0 + st * C::Y_BYTES;
+      }
+      for (int t = 0; t < n; ++t, ++tg) {
+        const int col0 = (lst[t] & 0x7fff) * C::BN;
+        int4 r4 = make_int4(0, 0, 0, 0);
+        if (gy && lane < C::BN / 4)
+          r4 = __ldg(reinterpret_cast<const int4*>(args.y_rows + static_cast<size_t>(bh) * args.T_cols_pad + col0) + lane);
+        // y0 ring (+ per-column lse2 / delta for dK/dV)
+        const int st = tg % C::NS0;
+        if (tg >= C::NS0) mbar_wait(bar_y0_empty + st, ((tg / C::NS0) - 1) & 1);
+        uint8_t* yb = smem + C::OFF_Y0 + st * C::Y_BYTES;
+        if (lane == 0) {
+          SCFA_STAMP_AT(tg, 14);
           mbar_arrive_expect_tx(bar_y0_full + st, C::Y_BYTES + C::AUX_BYTES);
-          for (int c = 0; c < C::DCH; ++c) tma_load_3d(yb + c * C::BN * 128, &tm_y0, bar_y0_full + st, c * 64, col0, bh);
-          if (C::AUX) {
-            uint8_t* aux = smem + C::OFF_AUX + st * C::AUX_BYTES;
-            const size_t coff = static_cast<size_t>(bh) * args.T_cols_pad + col0;
-            bulk_load(aux, args.lse2 + coff, C::BN * 4, bar_y0_full + st);
-            bulk_load(aux + C::BN * 4, args.delta + coff, C::BN * 4, bar_y0_full + st);
+        }
+        __syncwarp();
+        if (gy) {
+          if (lane < C::BN / 4) {
+#pragma unroll
+            for (int c = 0; c < C::DCH; ++c)
+              tma_gather4(yb + c * C::BN * 128 + lane * 512, &tm_y0, bar_y0_full + st, c * 64, r4.x, r4.y, r4.z, r4.w);
           }
+        } else if (lane == 0) {
+          for (int c = 0; c < C::DCH; ++c) tma_load_3d(yb + c * C::BN * 128, &tm_y0, bar_y0_full + st, c * 64, col0, bh);
         }
-        ++ia;
-      }
-    } else if (lane == 1) {
-      // y1 ring
-      tma_prefetch_desc(&tm_y1);
-      int tg = 0;
-      for (int w = blockIdx.x; w < args.n_items; w += gridDim.x) {
-        int bh, rb;
-        decode_item(args, w, bh, rb);
-        const int lb = bh * args.n_row_blocks + rb;
-        const int n = args.list_count[lb];
-        const uint16_t* lst = args.list + static_cast<size_t>(lb) * args.list_stride;
-        for (int t = 0; t < n; ++t, ++tg) {
-          const int st = tg % C::NS1;
-          if (tg >= C::NS1) mbar_wait(bar_y1_empty + st, ((tg / C::NS1) - 1) & 1);
-          const int col0 = (lst[t] & 0x7fff) * C::BN;
-          uint8_t* yb = smem + C::OFF_Y1 + st * C::Y_BYTES;
-          mbar_arrive_expect_tx(bar_y1_full + st, C::Y_BYTES);
-          for (int c = 0; c < C::DCH; ++c) tma_load_3d(yb + c * C::BN * 128, &tm_y1, bar_y1_full + st, c * 64, col0, bh);
+        if (C::AUX && lane == 0) {
+          uint8_t* aux = smem + C::OFF_AUX + st * C::AUX_BYTES;
+          const size_t coff = static_cast<size_t>(bh) * args.T_cols_pad + col0;
+          bulk_load(aux, args.lse2 + coff, C::BN * 4, bar_y0_full + st);
+          bulk_load(aux + C::BN * 4, args.delta + coff, C::BN * 4, bar_y0_full + st);
+        }
+        // y1 ring
+        const int st1 = tg % C::NS1;
+        if (tg >= C::NS1) mbar_wait(bar_y1_empty + st1, ((tg / C::NS1) - 1) & 1);
+        uint8_t* yb1 = smem + C::OFF_Y1 + st1 * C::Y_BYTES;
+        if (lane == 0) {
+          SCFA_STAMP_AT(tg, 15);
+          mbar_arrive_expect_tx(bar_y1_full + st1, C::Y_BYTES);
+        }
+        __syncwarp();
+        if (gy) {
+          if (lane < C::BN / 4) {
+#pragma unroll
+            for (int c = 0; c < C::DCH; ++c)
+              tma_gather4(yb1 + c * C::BN * 128 + lane * 512, &tm_y1, bar_y1_full + st1, c * 64, r4.x, r4.y, r4.z,
+                          r4.w);
+          }
+        } else if (lane == 0) {
+          for (int c = 0; c < C::DCH; ++c) tma_load_3d(yb1 + c * C::BN * 128, &tm_y1, bar_y1_full + st1, c * 64, col0, bh);
         }
       }
+      ++ia;
     }
   } else if (warp == 5) {
     // ------------------------------------------------------------ MMA issuer
@@ -304,7 +384,9 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
       auto flush = [&](int ptg, bool first, bool last) {
         const int s0 = ptg % C::NS0, s1 = ptg % C::NS1;
         if (kMode == MODE_FWD) mbar_wait(bar_y1_full + s1, (ptg / C::NS1) & 1);  // V not needed before
+        SCFA_STAMP_AT(ptg, 12);
         mbar_wait(bar_p_full, ptg & 1);
+        SCFA_STAMP_AT(ptg, 13);
         tc_fence_after();
         const uint32_t y0_addr = smem_u32(smem + C::OFF_Y0 + s0 * C::Y_BYTES);
         const uint32_t y1_addr = smem_u32(smem + C::OFF_Y1 + s1 * C::Y_BYTES);
@@ -333,10 +415,13 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
       int tg = 0, ia = 0;
       int p_tg = -1;
       bool p_first = false, p_last = false;
-      for (int w = blockIdx.x; w < args.n_items; w += gridDim.x) {
-        int bh, rb;
-        decode_item(args, w, bh, rb);
-        const int n = args.list_count[bh * args.n_row_blocks + rb];
+      for (int k = 0;; ++k) {
+        const int qs = k % C::NQ;
+        mbar_wait(bar_q_full + qs, (k / C::NQ) & 1);
+        const int2 item = ring[qs];
+        mbar_arrive(bar_q_empty + qs);
+        if (item.x < 0) break;
+        const int n = item.y;
         if (n == 0) continue;
         const int xs = ia % C::NXS;
         const uint32_t x0_addr = smem_u32(smem + C::OFF_X + xs * C::XSLOT_BYTES);
@@ -408,29 +493,34 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
     int tg = 0, ia = 0;
     // per-item metadata is fetched one item ahead (its global-load latency hides behind
     // the current item), and each tile's list entry one tile ahead
-    int nx_n = 0, nx_idx = 0, nx_e0 = 0;
+    int nx_idx = 0, nx_e0 = 0;
     int2 nx_run = make_int2(0, 0);
-    auto fetch = [&](int w) {
-      if (w >= args.n_items) return;
-      int fbh, frb;
-      decode_item(args, w, fbh, frb);
-      const int flb = fbh * args.n_row_blocks + frb;
+    int2 nx_item = make_int2(-1, 0);
+    // ring slot k: wait until published, read (the q_empty arrival comes when the item
+    // is consumed), and prefetch its per-row metadata
+    auto peek = [&](int k) {
+      const int qs = k % C::NQ;
+      mbar_wait(bar_q_full + qs, (k / C::NQ) & 1);
+      nx_item = ring[qs];
+      if (nx_item.x < 0) return;
+      const int fbh = nx_item.x / args.n_row_blocks, frb = nx_item.x - fbh * args.n_row_blocks;
       const size_t foff = static_cast<size_t>(fbh) * args.T_rows_pad + frb * C::BM + r;
-      nx_n = args.list_count[flb];
-      nx_e0 = args.list[static_cast<size_t>(flb) * args.list_stride];
-      nx_idx = args.row_idx[foff];
+      nx_e0 = args.list[static_cast<size_t>(nx_item.x) * args.list_stride];
+      nx_idx = args.x_rows ? args.x_rows[foff] : args.row_idx[foff];
       nx_run = args.row_runs[foff];
     };
-    fetch(blockIdx.x);
-    for (int w = blockIdx.x; w < args.n_items; w += gridDim.x) {
-      int bh, rb;
-      decode_item(args, w, bh, rb);
-      const int lb = bh * args.n_row_blocks + rb;
-      const int n = nx_n;
+    peek(0);
+    for (int k = 0;; ++k) {
+      const int2 item = nx_item;
+      mbar_arrive(bar_q_empty + (k % C::NQ));
+      if (item.x < 0) break;
+      const int lb = item.x;
+      const int bh = lb / args.n_row_blocks, rb = lb - bh * args.n_row_blocks;
+      const int n = item.y;
       const int my_idx = nx_idx;
       const int2 run = nx_run;
       int entry_next = nx_e0;
-      fetch(w + gridDim.x);
+      peek(k + 1);
       const uint16_t* lst = args.list + static_cast<size_t>(lb) * args.list_stride;
       const int row = rb * C::BM + r;
       const size_t roff = static_cast<size_t>(bh) * args.T_rows_pad + row;
@@ -438,9 +528,18 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
       const bool live = out_row(args, bh, row, my_idx, orow);
 
       if (kMode == MODE_FWD) {
+        // One pass over S per tile, in 32-column chunks, with a lagging exponent base:
+        // P = 2^(s*scale*log2e - m_run) where m_run is the row max as of the row's first
+        // visible chunk, raised only when a chunk's max exceeds it by more than kLag
+        // (P <= 2^kLag stays far inside fp32 / bf16 range; the final 1/l makes the
+        // result exact).  A raise is free for a row that has seen nothing yet (l = 0,
+        // O = 0) and otherwise rescales l, this tile's stored P chunks and O (rare).
+        // Chunks no row of the warp can see are skipped (P = 0, no exponentials).
+        constexpr float kLag = 64.f;
+        constexpr int NCH = C::BN / 32;
         const bool neg = sl < 0.f;  // a negative scale turns the row max into a row min
         const float mask_val = neg ? INFINITY : NEG_INF;
-        float m_run = NEG_INF;   // log2-domain max used for exponentiation (lags by < 8)
+        float m_run = NEG_INF;   // log2-domain exponent base (lags the max by < kLag)
         float m_true = NEG_INF;  // exact running max of scaled logits (log2 domain)
         float l_run = 0.f;
         for (int t = 0; t < n; ++t, ++tg) {
@@ -452,100 +551,113 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
           mbar_wait(bar_s_full, tg & 1);
           SCFA_STAMP(1);
           tc_fence_after();
-          // S is consumed in two 64-column halves to bound register pressure: both halves
-          // are read for the row max, half 1 is exponentiated from registers, half 0 is
-          // re-read (S stays valid until s_free) and exponentiated last.
-          constexpr int HB = C::BN / 2;
-          uint32_t vis[NW];
-          if (!full) run_mask<NW>(run.x - col0, run.y - col0, vis);
-          float x[HB];
-          float ext[2];
-#pragma unroll
-          for (int hf = 0; hf < 2; ++hf) {
-            tmem_ld_cols<HB>(t_s + hf * HB, reinterpret_cast<uint32_t*>(x));
-            tmem_wait_ld();
-            if (!full) {
-#pragma unroll
-              for (int c = 0; c < HB; ++c) x[c] = ((vis[2 * hf + (c >> 5)] >> (c & 31)) & 1u) ? x[c] : mask_val;
-            }
-            float mq[4] = {mask_val, mask_val, mask_val, mask_val};
-            if (!neg) {
-#pragma unroll
-              for (int c = 0; c < HB; c += 2) mq[(c >> 1) & 3] = max3(mq[(c >> 1) & 3], x[c], x[c + 1]);
-              ext[hf] = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
-            } else {
-#pragma unroll
-              for (int c = 0; c < HB; c += 2) mq[(c >> 1) & 3] = min3(mq[(c >> 1) & 3], x[c], x[c + 1]);
-              ext[hf] = fminf(fminf(mq[0], mq[1]), fminf(mq[2], mq[3]));
-            }
-            asm volatile("" ::"f"(ext[hf]));  // pin: this half's max is done before the next tcgen05.ld
-          }
-          const float mx = neg ? fminf(ext[0], ext[1]) : fmaxf(ext[0], ext[1]);
-          const float m_tile = mx * sl;  // -inf when the whole row is masked in this tile
-          m_true = fmaxf(m_true, m_tile);
-          // Rebase to a new max (log2 units) only when the max grows by >= 2^8: P stays
-          // <= 256 and the final normalisation by l keeps the result exact.
-          float alpha = 1.f;
-          const bool rebase = m_tile > m_run + 8.0f || (m_run == NEG_INF && m_tile != NEG_INF);
-          if (rebase) {
-            alpha = (m_run == NEG_INF) ? 0.f : ex2(m_run - m_tile);
-            l_run *= alpha;
-            m_run = m_tile;
-          }
-          const float nm = (m_run == NEG_INF) ? 0.f : -m_run;
+          const int rlo = run.x - col0, rhi = run.y - col0;
           float la[4] = {0.f, 0.f, 0.f, 0.f};
+          bool p_ready = (tg == 0);  // P columns free: the previous tile's PV has read them
 #pragma unroll
-          for (int step = 0; step < 2; ++step) {
-            const int hf = 1 - step;  // half 1 is still in registers
-            if (step == 1) {
-              tmem_ld_cols<HB>(t_s + hf * HB, reinterpret_cast<uint32_t*>(x));
+          for (int ch = 0; ch < NCH; ++ch) {
+            const uint32_t wv = full ? 0xffffffffu : (bits_below(rhi - 32 * ch) & ~bits_below(rlo - 32 * ch));
+            uint32_t pk[16];
+            if (__any_sync(0xffffffffu, wv != 0u)) {
+              float x[32];
+              tmem_ld32(t_s + 32 * ch, *reinterpret_cast<uint32_t(*)[32]>(x));
               tmem_wait_ld();
-              if (C::OVERLAP) {
+              if (ch == NCH - 1) {
                 tc_fence_before();
                 mbar_arrive(bar_s_free);  // S fully read: the next tile's S may overwrite it
               }
-              if (!full) {
+              if (__any_sync(0xffffffffu, wv != 0xffffffffu)) {
 #pragma unroll
-                for (int c = 0; c < HB; ++c) x[c] = ((vis[2 * hf + (c >> 5)] >> (c & 31)) & 1u) ? x[c] : mask_val;
+                for (int c = 0; c < 32; ++c) x[c] = ((wv >> c) & 1u) ? x[c] : mask_val;
               }
-            }
-            uint32_t pk[HB / 2];
+              float e0 = mask_val, e1 = mask_val;
+              if (!neg) {
 #pragma unroll
-            for (int c = 0; c < HB; c += 2) {
-              float a0, a1;
-              fma2(a0, a1, x[c], x[c + 1], sl, sl, nm, nm);
-              a0 = ex2(a0);
-              a1 = ex2(a1);
-              const int q = (c >> 1) & 1;
-              add2(la[2 * q], la[2 * q + 1], la[2 * q], la[2 * q + 1], a0, a1);
-              pk[c >> 1] = pack_bf16(a0, a1);
-            }
-            if (step == 0) {
-              // P's columns and O are read by the previous tile's accumulate MMAs.
-              if (tg > 0) mbar_wait(bar_p_free, (tg - 1) & 1);
-              tc_fence_after();
-              // tcgen05.ld/st are warp-collective: the whole warp rescales when any row
-              // must (alpha == 1 for the others, an exact no-op).
-              if (__any_sync(0xffffffffu, rebase && t > 0)) {
-#pragma unroll 1
-                for (int c = 0; c < kD; c += 32) {
-                  uint32_t v[32];
-                  tmem_ld32(t_acc + c, v);
-                  tmem_wait_ld();
+                for (int c = 0; c < 32; c += 4) {
+                  e0 = max3(e0, x[c], x[c + 1]);
+                  e1 = max3(e1, x[c + 2], x[c + 3]);
+                }
+              } else {
 #pragma unroll
-                  for (int i = 0; i < 32; i += 2) {
-                    float o0, o1;
-                    mul2(o0, o1, __uint_as_float(v[i]), __uint_as_float(v[i + 1]), alpha, alpha);
-                    v[i] = __float_as_uint(o0);
-                    v[i + 1] = __float_as_uint(o1);
-                  }
-                  tmem_st32(t_acc + c, v);
+                for (int c = 0; c < 32; c += 4) {
+                  e0 = min3(e0, x[c], x[c + 1]);
+                  e1 = min3(e1, x[c + 2], x[c + 3]);
                 }
               }
-            }
+              const float ms = (neg ? fminf(e0, e1) : fmaxf(e0, e1)) * sl;  // -inf: nothing visible
+              m_true = fmaxf(m_true, ms);
+              const bool raise = ms > m_run + kLag;  // includes the row's first visible chunk
+              if (__any_sync(0xffffffffu, raise)) {
+                const bool rescale = raise && (m_run != NEG_INF);
+                float alpha = 1.f;
+                if (raise) {
+                  alpha = rescale ? ex2(m_run - ms) : 0.f;
+                  m_run = ms;
+                }
+                if (__any_sync(0xffffffffu, rescale)) {  // rare: P chunks of this tile, l, O
+                  if (!p_ready) {
+                    mbar_wait(bar_p_free, (tg - 1) & 1);
+                    tc_fence_after();
+                    p_ready = true;
+                  }
+                  tmem_wait_st();
+#pragma unroll 1
+                  for (int j = 0; j < ch; ++j) {
+                    uint32_t q16[16];
+                    tmem_ld16(t_p + 16 * j, q16);
+                    tmem_wait_ld();
 #pragma unroll
-            for (int c = 0; c < HB / 2; c += 16)
-              tmem_st16(t_p + hf * (HB / 2) + c, *reinterpret_cast<uint32_t(*)[16]>(&pk[c]));
+                    for (int i = 0; i < 16; ++i) {
+                      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&q16[i]));
+                      q16[i] = pack_bf16(f.x * alpha, f.y * alpha);
+                    }
+                    tmem_st16(t_p + 16 * j, q16);
+                  }
+#pragma unroll 1
+                  for (int c = 0; c < kD; c += 32) {
+                    uint32_t v[32];
+                    tmem_ld32(t_acc + c, v);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 32; i += 2) {
+                      float o0, o1;
+                      mul2(o0, o1, __uint_as_float(v[i]), __uint_as_float(v[i + 1]), alpha, alpha);
+                      v[i] = __float_as_uint(o0);
+                      v[i + 1] = __float_as_uint(o1);
+                    }
+                    tmem_st32(t_acc + c, v);
+                  }
+                  tmem_wait_st();
+                }
+                l_run *= alpha;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) la[i] *= alpha;
+              }
+              const float nm = (m_run == NEG_INF) ? 0.f : -m_run;
+#pragma unroll
+              for (int c = 0; c < 32; c += 2) {
+                float a0, a1;
+                fma2(a0, a1, x[c], x[c + 1], sl, sl, nm, nm);
+                a0 = ex2(a0);
+                a1 = ex2(a1);
+                const int q = (c >> 1) & 1;
+                add2(la[2 * q], la[2 * q + 1], la[2 * q], la[2 * q + 1], a0, a1);
+                pk[c >> 1] = pack_bf16(a0, a1);
+              }
+            } else {
+              if (ch == NCH - 1) {
+                tc_fence_before();
+                mbar_arrive(bar_s_free);
+              }
+#pragma unroll
+              for (int i = 0; i < 16; ++i) pk[i] = 0u;
+            }
+            if (!p_ready) {  // P's columns are read by the previous tile's accumulate MMAs
+              mbar_wait(bar_p_free, (tg - 1) & 1);
+              tc_fence_after();
+              p_ready = true;
+            }
+            tmem_st16(t_p + 16 * ch, pk);
           }
           l_run += (la[0] + la[1]) + (la[2] + la[3]);
           tmem_wait_st();
@@ -561,7 +673,7 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
         }
         const float inv_l = (l_run > 0.f) ? 1.f / l_run : 0.f;
         if (n > 0) {
-          constexpr int RB = kD * 2;  // bf16 output row
+          constexpr int RB = kD * 2;  // bf16 output row, staged in the freed stationary slot
           uint8_t* stage = smem + C::OFF_X + (ia % C::NXS) * C::XSLOT_BYTES;
 #pragma unroll
           for (int c = 0; c < kD; c += 32) {
@@ -594,6 +706,8 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
           args.out0[so] = dead ? NEG_INF : m_true * LN2;             // M
           args.out1[so] = dead ? 0.f : l_run * ex2(m_use - m_true);  // L relative to M
           args.out_lse2[roff] = dead ? INFINITY : (m_use + __log2f(l_run));
+        } else {
+          args.out_lse2[roff] = INFINITY;  // pad slot: read (never used) by the dK/dV column loads
         }
         if (threadIdx.x == 0) { SCFA_STAMP_AT(tg - 1, 8) }
       } else {
@@ -601,7 +715,43 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
         float my_nlse = 0.f, my_ndelta = 0.f;
         if (kMode == MODE_DQ) {
           my_nlse = -args.lse2[roff];
-          my_ndelta = -args.delta[roff];
+          if (args.delta_out) {
+            // fused delta = rowsum(dO * O) (qk_sparse.py:168): O row from global, dO row
+            // from the stationary tile in shared memory
+            float dl = 0.f;
+            if (n > 0 && row < args.T_rows) {
+              const size_t orow_o = args.x_rows ? static_cast<size_t>(my_idx)
+                                                : static_cast<size_t>(bh) * args.T_rows + row;
+              const uint4* op = reinterpret_cast<const uint4*>(args.o_src + orow_o * kD);
+              uint4 ov[kD / 8];
+#pragma unroll
+              for (int j = 0; j < kD / 8; ++j) ov[j] = __ldg(op + j);
+              mbar_wait(bar_x_full + (ia % C::NXS), (ia / C::NXS) & 1);
+              const uint8_t* dob = smem + C::OFF_X + (ia % C::NXS) * C::XSLOT_BYTES + C::X_BYTES;
+#pragma unroll
+              for (int j = 0; j < kD / 8; ++j) {
+                const uint32_t addr =
+                    smem_u32(dob + (j >> 3) * C::BM * 128 + r * 128 + (((j & 7) ^ (r & 7)) << 4));
+                uint4 dv4;
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(dv4.x), "=r"(dv4.y), "=r"(dv4.z), "=r"(dv4.w)
+                             : "r"(addr));
+                const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&ov[j]);
+                const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&dv4);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 x = __bfloat1622float2(a2[e]);
+                  const float2 y = __bfloat1622float2(b2[e]);
+                  dl = fmaf(x.x, y.x, dl);
+                  dl = fmaf(x.y, y.y, dl);
+                }
+              }
+            }
+            args.delta_out[roff] = dl;
+            my_ndelta = -dl;
+          } else {
+            my_ndelta = -args.delta[roff];
+          }
         }
         for (int t = 0; t < n; ++t, ++tg) {
           const int entry = entry_next;
@@ -691,7 +841,7 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
           if (threadIdx.x == 0) { SCFA_STAMP_AT(tg - 1, 4) }
         }
         const int n_out = (kMode == MODE_DKDV) ? 2 : 1;
-        constexpr int RB = kD * 4;  // fp32 gradient row
+        constexpr int RB = kD * 4;  // fp32 gradient row, staged in the freed stationary slot
         uint8_t* stage = smem + C::OFF_X + (ia % C::NXS) * C::XSLOT_BYTES;
 #pragma unroll
         for (int o = 0; o < n_out; ++o) {
@@ -737,9 +887,26 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
     tc_fence_after();
     tmem_dealloc<C::TM_COLS>(tmem);
   }
+  if (threadIdx.x == 0) {  // the last CTA to finish re-arms the work counter for the next launch
+    __threadfence();
+    if (atomicAdd(work_ctr + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+      work_ctr[0] = 0;
+      work_ctr[1] = 0;
+      __threadfence();
+    }
+  }
 }
 
 // ------------------------------------------------------------------ host side
+
+// Row-table map for tile::gather4 / tile::scatter4: a [nrows, D] matrix of elem_bytes
+// elements, one 128-byte column window (64 bf16 / 32 fp32) per box row.
+static int make_row_map(CUtensorMap* map, const void* base, long long nrows, int D, int elem_bytes) {
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(nrows > 0 ? nrows : 1)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(D) * elem_bytes};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / elem_bytes), 1};
+  return encode_tensor_map(map, elem_bytes, 2, base, dims, strides, box);
+}
 
 static int make_map(CUtensorMap* map, const void* base, int BH, int T, int D, int box_rows) {
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(D), static_cast<cuuint64_t>(T), static_cast<cuuint64_t>(BH)};
@@ -769,10 +936,20 @@ static int launch_mode(const AttnLaunch& L, cudaStream_t stream) {
   using C = Cfg<kMode, kD>;
   CUtensorMap mx0, mx1, my0, my1;
   int rc = 0;
-  rc |= make_map(&mx0, L.x0, L.BH, L.T_rows, kD, C::BM);
-  rc |= make_map(&mx1, L.x1 ? L.x1 : L.x0, L.BH, L.T_rows, kD, C::BM);
-  rc |= make_map(&my0, L.y0, L.BH, L.T_cols, kD, C::BN);
-  rc |= make_map(&my1, L.y1, L.BH, L.T_cols, kD, C::BN);
+  if (L.x_rows) {
+    rc |= make_row_map(&mx0, L.x0, L.x_nrows, kD, 2);
+    rc |= make_row_map(&mx1, L.x1 ? L.x1 : L.x0, L.x_nrows, kD, 2);
+  } else {
+    rc |= make_map(&mx0, L.x0, L.BH, L.T_rows, kD, C::BM);
+    rc |= make_map(&mx1, L.x1 ? L.x1 : L.x0, L.BH, L.T_rows, kD, C::BM);
+  }
+  if (L.y_rows) {
+    rc |= make_row_map(&my0, L.y0, L.y_nrows, kD, 2);
+    rc |= make_row_map(&my1, L.y1, L.y_nrows, kD, 2);
+  } else {
+    rc |= make_map(&my0, L.y0, L.BH, L.T_cols, kD, C::BN);
+    rc |= make_map(&my1, L.y1, L.BH, L.T_cols, kD, C::BN);
+  }
   if (rc) return SCFA_ERR_CUDA;
   AttnArgs a;
   a.BH = L.BH;
@@ -785,6 +962,10 @@ static int launch_mode(const AttnLaunch& L, cudaStream_t stream) {
   a.out_boundary = L.out_boundary;
   a.row_idx = L.row_idx;
   a.row_runs = reinterpret_cast<const int2*>(L.row_runs);
+  a.x_rows = L.x_rows;
+  a.y_rows = L.y_rows;
+  a.o_src = static_cast<const __nv_bfloat16*>(L.o_src);
+  a.delta_out = L.delta_out;
   a.lse2 = L.lse2;
   a.delta = L.delta;
   a.list = L.list;

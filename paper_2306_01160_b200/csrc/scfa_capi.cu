@@ -49,6 +49,24 @@ int encode_tensor_map_bf16_3d(CUtensorMap* map, const void* base, const cuuint64
   return 0;
 }
 
+int encode_tensor_map(CUtensorMap* map, int dtype_bytes, int rank, const void* base, const cuuint64_t* dims,
+                      const cuuint64_t* strides_bytes, const cuuint32_t* box) {
+  auto fn = get_encode();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return 1;
+  }
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(map, dtype_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank,
+                  const_cast<void*>(base), dims, strides_bytes, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+    return 1;
+  }
+  return 0;
+}
+
 static int check_attn_args(int64_t BH, int64_t T_q, int64_t T_kv, int64_t D, int64_t Tq_pad, int64_t Tkv_pad,
                            const void* q, const void* k, const void* v) {
   if (D != 64 && D != 128) {
@@ -74,7 +92,7 @@ static int check_attn_args(int64_t BH, int64_t T_q, int64_t T_kv, int64_t D, int
 
 using namespace scfa;
 
-extern "C" int scfa_abi_version(void) { return 2; }
+extern "C" int scfa_abi_version(void) { return 3; }
 
 extern "C" const char* scfa_last_error(void) { return g_err; }
 
@@ -82,7 +100,7 @@ extern "C" int scfa_attn_fwd(const void* q, const void* k, const void* v, int64_
                              int64_t D, const int32_t* q_idx, const int32_t* q_runs, int64_t Tq_pad, int64_t Tkv_pad,
                              const uint16_t* list, const int32_t* list_count, int64_t list_stride, float scale,
                              int64_t H, int64_t T_out, int out_boundary, void* o, float* m, float* l, float* lse2,
-                             void* stream) {
+                             const int32_t* q_rows, const int32_t* k_rows, int64_t R_q, int64_t R_kv, void* stream) {
   int rc = check_attn_args(BH, T_q, T_kv, D, Tq_pad, Tkv_pad, q, k, v);
   if (rc) return rc;
   if (BH == 0 || T_q == 0) return SCFA_OK;
@@ -110,6 +128,10 @@ extern "C" int scfa_attn_fwd(const void* q, const void* k, const void* v, int64_
   L.list_count = list_count;
   L.list_stride = static_cast<int>(list_stride);
   L.n_row_blocks = static_cast<int>((T_q + 127) / 128);
+  L.x_rows = q_rows;
+  L.y_rows = T_kv > 0 ? k_rows : nullptr;
+  L.x_nrows = R_q;
+  L.y_nrows = R_kv;
   L.out_o = static_cast<__nv_bfloat16*>(o);
   L.out0 = m;
   L.out1 = l;
@@ -124,7 +146,9 @@ extern "C" int scfa_attn_bwd_dq(const void* q, const void* k, const void* v, con
                                 int64_t T_q, int64_t T_kv, int64_t D, const int32_t* q_idx, const int32_t* q_runs,
                                 int64_t Tq_pad, int64_t Tkv_pad, const float* lse2, const float* delta,
                                 const uint16_t* list, const int32_t* list_count, int64_t list_stride, float scale,
-                                int64_t H, int64_t T_out, int out_boundary, float* dq, void* stream) {
+                                int64_t H, int64_t T_out, int out_boundary, float* dq, const int32_t* q_rows,
+                                const int32_t* k_rows, int64_t R_q, int64_t R_kv, const void* o, float* delta_out,
+                                void* stream) {
   int rc = check_attn_args(BH, T_q, T_kv, D, Tq_pad, Tkv_pad, q, k, v);
   if (rc) return rc;
   if (BH == 0 || T_q == 0) return SCFA_OK;
@@ -153,6 +177,20 @@ extern "C" int scfa_attn_bwd_dq(const void* q, const void* k, const void* v, con
   if (T_kv == 0) L.T_cols = static_cast<int>(T_q);
   L.row_idx = q_idx;
   L.row_runs = q_runs;
+  L.x_rows = q_rows;
+  L.y_rows = T_kv > 0 ? k_rows : nullptr;
+  L.x_nrows = R_q;
+  L.y_nrows = R_kv;
+  if (o && !delta_out) {
+    set_error("bwd_dq: the fused delta needs delta_out");
+    return SCFA_ERR_PARAM;
+  }
+  if (o && !q_rows && out_boundary) {
+    set_error("bwd_dq: the fused delta needs row tables or engine layout");
+    return SCFA_ERR_PARAM;
+  }
+  L.o_src = o;
+  L.delta_out = o ? delta_out : nullptr;
   L.n_row_blocks = (L.T_rows + 127) / 128;
   rc = launch_attention(L, static_cast<cudaStream_t>(stream));
   if (rc && !g_err[0]) set_error("attention backward (dQ) launch failed: %s", cudaGetErrorString(cudaGetLastError()));
@@ -163,7 +201,9 @@ extern "C" int scfa_attn_bwd_dkdv(const void* q, const void* k, const void* v, c
                                   int64_t T_q, int64_t T_kv, int64_t D, const int32_t* k_idx, const int32_t* k_runs,
                                   int64_t Tq_pad, int64_t Tkv_pad, const float* lse2, const float* delta,
                                   const uint16_t* list, const int32_t* list_count, int64_t list_stride, float scale,
-                                  int64_t H, int64_t T_out, int out_boundary, float* dk, float* dv, void* stream) {
+                                  int64_t H, int64_t T_out, int out_boundary, float* dk, float* dv,
+                                  const int32_t* q_rows, const int32_t* k_rows, int64_t R_q, int64_t R_kv,
+                                  void* stream) {
   int rc = check_attn_args(BH, T_q, T_kv, D, Tq_pad, Tkv_pad, q, k, v);
   if (rc) return rc;
   if (BH == 0 || T_kv == 0) return SCFA_OK;
@@ -193,6 +233,10 @@ extern "C" int scfa_attn_bwd_dkdv(const void* q, const void* k, const void* v, c
   if (T_q == 0) L.T_cols = static_cast<int>(T_kv);
   L.row_idx = k_idx;
   L.row_runs = k_runs;
+  L.x_rows = k_rows;
+  L.y_rows = T_q > 0 ? q_rows : nullptr;
+  L.x_nrows = R_kv;
+  L.y_nrows = R_q;
   L.n_row_blocks = (L.T_rows + 127) / 128;
   rc = launch_attention(L, static_cast<cudaStream_t>(stream));
   if (rc && !g_err[0]) set_error("attention backward (dK/dV) launch failed: %s", cudaGetErrorString(cudaGetLastError()));

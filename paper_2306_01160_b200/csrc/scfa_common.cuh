@@ -92,6 +92,42 @@ SCFA_DEVICE void tma_load_3d(void* smem_dst, const CUtensorMap* map, uint64_t* b
       : "memory");
 }
 
+// TMA row gather: four rows (r0..r3, outer coordinate) of one box_inner-wide column
+// window starting at c0 land as four consecutive 128-byte rows at smem_dst (512 B).
+// The 128-byte swizzle is a function of the shared-memory address, so 4-row groups
+// at 512-byte offsets of a 1024-aligned tile reproduce the tiled SWIZZLE_128B image
+// (measured: scripts/gather4_test.cu).
+SCFA_DEVICE void tma_gather4(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int r0, int r1, int r2,
+                             int r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// TMA row scatter (the store twin of tma_gather4), tracked by the issuing thread's bulk group.
+SCFA_DEVICE void tma_scatter4(const CUtensorMap* map, const void* smem_src, int c0, int r0, int r1, int r2, int r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.tile::scatter4.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(smem_src))
+      : "memory");
+}
+
+// 2-D tiled TMA store of one box (rows r0.., columns c0..).
+SCFA_DEVICE void tma_store_2d(const CUtensorMap* map, const void* smem_src, int c0, int r0) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(r0), "r"(smem_u32(smem_src))
+               : "memory");
+}
+
+SCFA_DEVICE void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// Wait until every committed bulk store of this thread has finished READING shared memory.
+SCFA_DEVICE void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+SCFA_DEVICE void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 // Plain bulk copy global -> shared (16-byte aligned, size multiple of 16).
 SCFA_DEVICE void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
   asm volatile(

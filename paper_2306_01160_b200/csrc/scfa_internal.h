@@ -32,6 +32,12 @@ struct AttnLaunch {
   const int* row_runs;  // (BH, T_rows_pad) int2: visible streamed-slot run [lo, hi)
   const float* lse2;
   const float* delta;
+  const int* x_rows;   // gather mode: global row of each stationary slot (BH, T_rows_pad); null = tiled
+  const int* y_rows;   // gather mode: global row of each streamed slot (BH, T_cols_pad)
+  long long x_nrows;   // rows of the x / out row tables (gather mode)
+  long long y_nrows;   // rows of the y row tables
+  const void* o_src;   // DQ: O rows (same addressing as dO) for the fused delta = rowsum(dO * O)
+  float* delta_out;    // DQ: delta per query slot (BH, T_rows_pad)
   const uint16_t* list;
   const int* list_count;
   int list_stride;
@@ -44,6 +50,8 @@ struct AttnLaunch {
 };
 
 int launch_attention(const AttnLaunch& L, cudaStream_t stream);
+int encode_tensor_map(CUtensorMap* map, int dtype_bytes, int rank, const void* base, const cuuint64_t* dims,
+                      const cuuint64_t* strides_bytes, const cuuint32_t* box);
 int encode_tensor_map_bf16_3d(CUtensorMap* map, const void* base, const cuuint64_t* dims,
                               const cuuint64_t* strides_bytes, const cuuint32_t* box,
                               const cuuint32_t* elem_strides);

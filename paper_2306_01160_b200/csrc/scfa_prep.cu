@@ -387,7 +387,8 @@ __global__ void __launch_bounds__(kSortThreads) hash_prepare_sort_kernel(
 __global__ void __launch_bounds__(256) hash_prepare_finish_kernel(int T, int T_pad, int excl, const int32_t* perm,
                                                                   const int32_t* scratch, int32_t* rank,
                                                                   int32_t* q_idx, int32_t* k_idx, int32_t* q_hash,
-                                                                  int32_t* k_hash, int2* q_runs, int2* k_runs) {
+                                                                  int32_t* k_hash, int2* q_runs, int2* k_runs,
+                                                                  int32_t* rows, int64_t H) {
   const int64_t bh = blockIdx.y;
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= T_pad) return;
@@ -399,9 +400,11 @@ __global__ void __launch_bounds__(256) hash_prepare_finish_kernel(int T, int T_p
     k_hash[o] = kKHashOob;
     q_runs[o] = make_int2(0, 0);
     k_runs[o] = make_int2(0, 0);
+    if (rows) rows[o] = static_cast<int32_t>(((bh / H) * T + perm[bh * T]) * H + bh % H);
     return;
   }
   const int32_t t = perm[bh * T + s];
+  if (rows) rows[o] = static_cast<int32_t>(((bh / H) * T + t) * H + bh % H);
   const int32_t g = q_hash[o];  // written sorted by kernel 1
   int a, e;
   const int32_t* bd = scratch + bh * (T + 257) + T;
@@ -565,6 +568,16 @@ __global__ void build_aux_kernel(const int32_t* __restrict__ perm, const int32_t
     }
     idx_out[g] = iv;
     if (hash_out) hash_out[g] = hv;
+  }
+}
+
+__global__ void row_map_kernel(const int32_t* __restrict__ perm, int64_t H, int64_t T_perm, int64_t n_slots,
+                               int64_t T_pad, int64_t T_src, int32_t* __restrict__ rows, int64_t total) {
+  for (int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g < total;
+       g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t bh = g / T_pad, s = g - bh * T_pad;
+    const int64_t t = perm[bh * T_perm + (s < n_slots ? s : 0)];
+    rows[g] = static_cast<int32_t>(((bh / H) * T_src + t) * H + bh % H);
   }
 }
 
@@ -746,7 +759,7 @@ extern "C" int scfa_hash_sort(const void* hash, int hash_dtype, int64_t B, int64
 extern "C" int scfa_hash_prepare(const void* hash, int hash_dtype, int64_t B, int64_t T, int64_t H, int64_t sb,
                                  int64_t st, int64_t sh, int flags, int32_t* perm, int32_t* rank, int32_t* scratch,
                                  int32_t* q_idx, int32_t* k_idx, int32_t* q_hash, int32_t* k_hash, int32_t* q_runs,
-                                 int32_t* k_runs, int32_t* err_flag, void* stream) {
+                                 int32_t* k_runs, int32_t* rows, int32_t* err_flag, void* stream) {
   if (T > kPrepMaxT) { set_error("hash_prepare: T > %d (use scfa_hash_sort)", kPrepMaxT); return SCFA_ERR_SHAPE; }
   if (B * H == 0 || T == 0) return SCFA_OK;
   if (B * H > 65535) { set_error("hash_prepare: too many (b, h) slices"); return SCFA_ERR_SHAPE; }
@@ -767,7 +780,8 @@ extern "C" int scfa_hash_prepare(const void* hash, int hash_dtype, int64_t B, in
   dim3 grid(static_cast<unsigned>((T_pad + 255) / 256), static_cast<unsigned>(B * H));
   hash_prepare_finish_kernel<<<grid, 256, 0, s>>>(static_cast<int>(T), T_pad, (flags & SCFA_FLAG_EXCLUDE_SELF) ? 1 : 0,
                                                   perm, scratch, rank, q_idx, k_idx, q_hash, k_hash,
-                                                  reinterpret_cast<int2*>(q_runs), reinterpret_cast<int2*>(k_runs));
+                                                  reinterpret_cast<int2*>(q_runs), reinterpret_cast<int2*>(k_runs),
+                                                  rows, H);
   return check_launch("hash_prepare_finish");
 }
 
@@ -860,6 +874,17 @@ extern "C" int scfa_build_aux(const int32_t* perm, const int32_t* counts, int64_
       perm, counts, H, T_perm, n_slots, T_pad, pad_value, oob_value, hash, hash_dtype, sb, st, sh, hash_oob, pos,
       pos_dtype, ps_bh, ps_t, idx_out, hash ? hash_out : nullptr, total);
   return check_launch("build_aux");
+}
+
+extern "C" int scfa_row_map(const int32_t* perm, int64_t B, int64_t H, int64_t T_perm, int64_t n_slots, int64_t T_pad,
+                            int64_t T_src, int32_t* rows, void* stream) {
+  const int64_t total = B * H * T_pad;
+  if (total == 0) return SCFA_OK;
+  if (B * T_src * H >= (1LL << 31)) { set_error("row_map: row table exceeds 2^31 rows"); return SCFA_ERR_SHAPE; }
+  if (n_slots < 1 || n_slots > T_perm) { set_error("row_map: n_slots must be in [1, T_perm]"); return SCFA_ERR_SHAPE; }
+  row_map_kernel<<<grid_for(total, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(perm, H, T_perm, n_slots, T_pad,
+                                                                                      T_src, rows, total);
+  return check_launch("row_map");
 }
 
 extern "C" int scfa_pack_index(const void* src, int dtype, int64_t BH, int64_t T, int64_t s_bh, int64_t s_t,

@@ -127,6 +127,7 @@ __global__ void __launch_bounds__(128) tile_list_kernel(const __grid_constant__ 
   const int rb = blockIdx.x;
   const int64_t bh = blockIdx.y;
   if (J.list == nullptr || rb >= J.n_rb) return;
+  if (rb == 0 && bh == 0 && threadIdx.x < 2) J.count[static_cast<int64_t>(gridDim.y) * J.n_rb + threadIdx.x] = 0;
   const int n_cb = J.n_cb, B = J.col_block;
   for (int i = threadIdx.x; i <= n_cb; i += blockDim.x) diff[i] = 0;
   if (threadIdx.x == 0) {

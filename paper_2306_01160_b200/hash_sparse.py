@@ -16,6 +16,8 @@ from . import _lib
 from ._kernel import (
     FlashOutputs,
     Problem,
+    RowTables,
+    make_row_tables,
     as_operand,
     attention_backward,
     attention_forward,
@@ -187,20 +189,26 @@ def _prepare_shared(hash_t, sb, st, sh, B, H, T, D, err, exclude_self):
     perm = torch.empty((BH, T), dtype=torch.int32, device=dev)
     rank = torch.empty((BH, T), dtype=torch.int32, device=dev)
     scratch = torch.empty((BH, T + 257), dtype=torch.int32, device=dev)
-    vec = torch.empty((4, BH, T_pad), dtype=torch.int32, device=dev)
+    vec = torch.empty((5, BH, T_pad), dtype=torch.int32, device=dev)
     runs = torch.empty((2, BH, T_pad, 2), dtype=torch.int32, device=dev)
     flags = _lib.FLAG_HASH | (_lib.FLAG_EXCLUDE_SELF if exclude_self else 0)
     _lib.call("scfa_hash_prepare", _lib.ptr(hash_t), _lib.dtype_code(hash_t), B, T, H, sb, st, sh, flags,
               _lib.ptr(perm), _lib.ptr(rank), _lib.ptr(scratch), _lib.ptr(vec[0]), _lib.ptr(vec[1]),
-              _lib.ptr(vec[2]), _lib.ptr(vec[3]), _lib.ptr(runs[0]), _lib.ptr(runs[1]), _lib.ptr(err),
-              _lib.stream_ptr())
+              _lib.ptr(vec[2]), _lib.ptr(vec[3]), _lib.ptr(runs[0]), _lib.ptr(runs[1]), _lib.ptr(vec[4]),
+              _lib.ptr(err), _lib.stream_ptr())
     problem = Problem(B, H, T, T, D, vec[0], vec[1], vec[2], vec[3], flags=flags)
     problem.set_runs(runs[0], runs[1])
+    problem.rows = RowTables(vec[4], vec[4], B * T * H, B * T * H)
     return perm, rank, problem
 
 
-def _sort_batch(q, k, v, q_hash, k_hash, layout, q_pos=None, k_pos=None, check=True, exclude_self=True):
-    """Shared by sort_by_bucket (engine layout) and hash_sparse_attention (boundary layout)."""
+def _sort_batch(q, k, v, q_hash, k_hash, layout, q_pos=None, k_pos=None, check=True, exclude_self=True,
+                materialize=True):
+    """Shared by sort_by_bucket (engine layout) and hash_sparse_attention (boundary layout).
+
+    materialize=False (boundary layout only): no sorted copies of q / k / v; the
+    problem carries row tables (problem.rows) for the gather-mode kernels instead.
+    """
     if layout == "bhtd":
         check_forward_operands(q, k, v)
         B, H, T_Q, D = q.shape
@@ -226,7 +234,13 @@ def _sort_batch(q, k, v, q_hash, k_hash, layout, q_pos=None, k_pos=None, check=T
         k_perm, k_rank = q_perm, q_rank
         if check and int(err.item()):
             raise ShapeError("bucket ids must be non-negative (and < 2**31)")
-        q_s, k_s, v_s = _gather3([q, k, v], [q_perm, q_perm, q_perm], layout)
+        if materialize:
+            q_s, k_s, v_s = _gather3([q, k, v], [q_perm, q_perm, q_perm], layout)
+        else:
+            q_s, k_s, v_s = q, k, v
+            if layout != "bthd":
+                problem.rows = None
+                q_s, k_s, v_s = _gather3([q, k, v], [q_perm, q_perm, q_perm], layout)
         qi, ki, qhs, khs = problem.q_idx, problem.k_idx, problem.q_hash, problem.k_hash
     else:
         q_perm, q_rank = _sort(qh, qsb, qst, qsh, B, H, T_Q, err, q_pos)
@@ -236,10 +250,15 @@ def _sort_batch(q, k, v, q_hash, k_hash, layout, q_pos=None, k_pos=None, check=T
             k_perm, k_rank = _sort(kh, ksb, kst, ksh, B, H, T_KV, err, k_pos)
         if check and int(err.item()):
             raise ShapeError("bucket ids must be non-negative (and < 2**31)")
-        q_s, k_s, v_s = _gather3([q, k, v], [q_perm, k_perm, k_perm], layout)
         qi, qhs = _aux(q_perm, qh, qsb, qst, qsh, B, H, T_Q, _OOB_QI, _OOB_QH, q_pos)
         ki, khs = _aux(k_perm, kh, ksb, kst, ksh, B, H, T_KV, _OOB_KI, _OOB_KH, k_pos)
         problem = Problem(B, H, T_Q, T_KV, D, qi, ki, qhs, khs, flags=_lib.FLAG_HASH)
+        if materialize or layout != "bthd":
+            q_s, k_s, v_s = _gather3([q, k, v], [q_perm, k_perm, k_perm], layout)
+        else:
+            q_s, k_s, v_s = q, k, v
+            problem.rows = make_row_tables(q_perm, k_perm, B, H, T_Q, T_KV, T_Q, T_KV, problem.Tq_pad, problem.Tkv_pad,
+                                      shared=same)
     return SortedBatch(
         q=q_s, k=k_s, v=v_s,
         q_idx=qi[:, :T_Q].view(B, H, T_Q), k_idx=ki[:, :T_KV].view(B, H, T_KV),
@@ -264,8 +283,12 @@ def sort_by_bucket(q, k, v, q_hash, k_hash, q_idx=None, k_idx=None):
 def _problem_of(sb, exclude_self, validate=True):
     flags = _lib.FLAG_HASH | (_lib.FLAG_EXCLUDE_SELF if exclude_self else 0)
     prob = sb.problem
-    B, H, T_Q, D = sb.q.shape
-    T_KV = sb.k.shape[2]
+    if prob is not None and prob.rows is not None:  # operands stayed in (B, T, H, D)
+        B, H, T_Q, D = prob.B, prob.H, prob.T_q, prob.D
+        T_KV = prob.T_kv
+    else:
+        B, H, T_Q, D = sb.q.shape
+        T_KV = sb.k.shape[2]
     if prob is None or prob.T_q != T_Q or prob.T_kv != T_KV:
         dev = sb.q.device
         BH = B * H
@@ -279,6 +302,7 @@ def _problem_of(sb, exclude_self, validate=True):
     if prob.flags != flags:
         clone = Problem(prob.B, prob.H, prob.T_q, prob.T_kv, prob.D, prob.q_idx, prob.k_idx, prob.q_hash,
                         prob.k_hash, flags=flags)
+        clone.rows = prob.rows
         prob = clone
     return prob
 
@@ -333,20 +357,37 @@ def hash_sparse_attention(q, k, v, q_hash, k_hash, scale=None, blocks=BlockSpec(
     return attention_forward(prob, sb.q, sb.k, sb.v, scale, blocks, boundary=(q.shape[1], False)).O
 
 
-def hash_sparse_attention_fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, exclude_self=True):
+def _fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, exclude_self=True, row_tables=False):
+    """The fused boundary-layout fwd + bwd; returns (FlashOutputs, dq, dk, dv, problem).
+
+    row_tables=False (default): Q / K / V are gathered once into bucket order and the
+    kernels stream them with tiled TMA loads (the fast path: tile::gather4 sustains only
+    ~1.6 TB/s chip-wide, scripts/gather_bw.cu).  row_tables=True: the kernels read the
+    caller's tensors through row tables (no copies at all).
+    """
+    q, k, v = as_operand(q), as_operand(k), as_operand(v)
+    sb = _sort_batch(q, k, v, q_hash, k_hash, "bthd", check=False, exclude_self=exclude_self,
+                     materialize=not row_tables)
+    prob = _problem_of(sb, exclude_self)
+    prob.schedule("fwd", "dq", "dkdv")  # runs + all three tile lists in one pass
+    T_Q, T_KV = q.shape[1], k.shape[1]
+    rows = prob.rows if row_tables else None
+    xq, xk, xv = (q, k, v) if row_tables else (sb.q, sb.k, sb.v)
+    outputs = attention_forward(prob, xq, xk, xv, scale, boundary=(T_Q, False), rows=rows)
+    dq, dk, dv = attention_backward(prob, xq, xk, xv, outputs, as_operand(d_out), scale,
+                                    boundary=(T_Q, T_KV, False), rows=rows)
+    return outputs, dq, dk, dv, prob
+
+
+def hash_sparse_attention_fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, exclude_self=True, row_tables=False):
     """Forward + backward through the whole hash path, boundary layout in and out.
 
     Returns (O bf16, dQ, dK, dV fp32), each (B, T, H, D).  The reference
     composes the same from sort_by_bucket -> hash_forward_kernel ->
     hash_backward_kernel(dO sorted by q order) -> inverse permutation; here the
-    permutations are fused into the kernels' loads (sorted copies) and epilogues.
+    inverse permutation is fused into the kernels' epilogues (each row is stored at
+    its original position) and, with row_tables=True, the forward permutation into
+    their TMA gather loads.
     """
-    q, k, v = as_operand(q), as_operand(k), as_operand(v)
-    sb = _sort_batch(q, k, v, q_hash, k_hash, "bthd", check=False, exclude_self=exclude_self)
-    prob = _problem_of(sb, exclude_self)
-    prob.schedule("fwd", "dq", "dkdv")  # runs + all three tile lists in one pass
-    T_Q, T_KV = q.shape[1], k.shape[1]
-    outputs = attention_forward(prob, sb.q, sb.k, sb.v, scale, boundary=(T_Q, False))
-    dq, dk, dv = attention_backward(prob, sb.q, sb.k, sb.v, outputs, as_operand(d_out), scale,
-                                    boundary=(T_Q, T_KV, False))
+    outputs, dq, dk, dv, _ = _fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale, exclude_self, row_tables)
     return outputs.O, dq, dk, dv

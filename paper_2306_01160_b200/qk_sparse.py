@@ -27,6 +27,7 @@ from ._kernel import (
     attention_forward,
     check_forward_operands,
     pack_index,
+    make_row_tables,
 )
 from .errors import ShapeError
 from .tensors import DOMAIN_KEEP, KEY_PAD, QUERY_PAD, BlockSpec, pad128, stream
@@ -137,8 +138,12 @@ def qk_tile_schedule(q_idx, k_idx, blocks=BlockSpec()):
     return causal_j_stops(q_idx, k_idx, blocks)
 
 
-def qk_preprocess(q, k, v, q_keep, k_keep):
-    """Compact, pad and transpose boundary-layout inputs (qk_sparse.py:196-211)."""
+def qk_preprocess(q, k, v, q_keep, k_keep, materialize=True):
+    """Compact, pad and transpose boundary-layout inputs (qk_sparse.py:196-211).
+
+    materialize=False: no compacted copies; q_c / k_c / v_c are the (B, T, H, D) inputs
+    and problem.rows holds the row tables the gather-mode kernels read them through.
+    """
     q, k, v = as_operand(q), as_operand(k), as_operand(v)
     if q.dim() != 4 or k.dim() != 4 or k.shape != v.shape:
         raise ShapeError(f"operand shapes disagree: {tuple(q.shape)}, {tuple(k.shape)}, {tuple(v.shape)}")
@@ -158,12 +163,16 @@ def qk_preprocess(q, k, v, q_keep, k_keep):
         raise ShapeError("keep entries must be 0 or 1")
     T_cq = int(host[:BH].max()) if BH else 0
     T_ck = int(host[BH: 2 * BH].max()) if BH else 0
-    q_c = _gather(q, q_perm, T_cq)
-    k_c = _gather(k, k_perm, T_ck)
-    v_c = _gather(v, k_perm, T_ck)
     q_aux = _aux(q_perm, cnt[:BH], B, H, T_cq, QUERY_PAD, _OOB_Q)
     k_aux = _aux(k_perm, cnt[BH: 2 * BH], B, H, T_ck, KEY_PAD, _OOB_K)
     problem = Problem(B, H, T_cq, T_ck, D, q_aux, k_aux)
+    if materialize:
+        q_c = _gather(q, q_perm, T_cq)
+        k_c = _gather(k, k_perm, T_ck)
+        v_c = _gather(v, k_perm, T_ck)
+    else:
+        q_c, k_c, v_c = q, k, v
+        problem.rows = make_row_tables(q_perm, k_perm, B, H, T_cq, T_ck, T_Q, T_KV, problem.Tq_pad, problem.Tkv_pad)
     return QkPrepared(
         q_c=q_c, k_c=k_c, v_c=v_c,
         q_idx=q_aux[:, :T_cq].view(B, H, T_cq),
@@ -252,18 +261,21 @@ def qk_sparse_attention(q, k, v, q_keep, k_keep, scale=None, blocks=BlockSpec(),
                              boundary=(prep.T_Q, True)).O
 
 
-def qk_sparse_attention_fwd_bwd(q, k, v, q_keep, k_keep, d_out, scale=None):
+def qk_sparse_attention_fwd_bwd(q, k, v, q_keep, k_keep, d_out, scale=None, row_tables=False):
     """Forward + backward through the whole QK path in boundary layout.
 
     Returns (O bf16, dQ, dK, dV fp32), all (B, T, H, D); dropped positions get
     zero outputs and zero gradients.  The reference composes the same thing
     from qk_preprocess -> qk_forward_kernel -> qk_backward_kernel.
     """
-    prep = qk_preprocess(q, k, v, q_keep, k_keep)
+    prep = qk_preprocess(q, k, v, q_keep, k_keep, materialize=not row_tables)
     T_Q, T_KV = q.shape[1], k.shape[1]
-    outputs = attention_forward(prep.problem, prep.q_c, prep.k_c, prep.v_c, scale, boundary=(T_Q, True))
-    dq, dk, dv = attention_backward(prep.problem, prep.q_c, prep.k_c, prep.v_c, outputs, as_operand(d_out), scale,
-                                    boundary=(T_Q, T_KV, True))
+    prob = prep.problem
+    prob.schedule("fwd", "dq", "dkdv")
+    rows = prob.rows if row_tables else None
+    outputs = attention_forward(prob, prep.q_c, prep.k_c, prep.v_c, scale, boundary=(T_Q, True), rows=rows)
+    dq, dk, dv = attention_backward(prob, prep.q_c, prep.k_c, prep.v_c, outputs, as_operand(d_out), scale,
+                                    boundary=(T_Q, T_KV, True), rows=rows)
     return outputs.O, dq, dk, dv
 
 

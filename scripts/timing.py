@@ -75,3 +75,11 @@ for name, buf in bufs.items():
               f"  flush {med(r[:, 5] - r[:, 3]):.0f}  last-acc after p_full {med(r[last, 11] - r[last, 2]):.0f}"
               f"  x_full after X issue {med(r[first, 9] - r[first, 10]):.0f}")
         print("   periods:", per[:14].astype(int).tolist())
+        # producer / flush detail (absolute clocks relative to the row threads' p_full stamp 2)
+        rel = lambda a, b: med(r[:, a] - r[:, b])
+        print(f"   K issue - s_full(row wait end) {rel(14, 1):.0f}  V issue - p_full {rel(15, 2):.0f}"
+              f"  flush y1-ready - p_full {rel(12, 2):.0f}  flush p_full seen - p_full {rel(13, 2):.0f}")
+        lr = lambda a, b: med(r[last, a] - r[last, b])
+        print(f"   last tile: y1-ready - p_full {lr(12, 2):.0f}  p_full seen - p_full {lr(13, 2):.0f}"
+              f"  issued(11) - seen(13) {lr(11, 13):.0f}  acc seen(4) - issued(11) {lr(4, 11):.0f}"
+              f"  V issue(15) - p_full {lr(15, 2):.0f}")

@@ -50,8 +50,9 @@ def test_dense_forward_backward(T):
     assert out.tiles_computed == scfa.dense_tile_count(T) * B * H
 
 
+@pytest.mark.parametrize("rt", [False, True], ids=["tiled", "rowtables"])
 @pytest.mark.parametrize("T,drop", [(256, 0.5), (1024, 0.5), (300, 0.9), (200, 0.0)])
-def test_qk_end_to_end(T, drop):
+def test_qk_end_to_end(T, drop, rt):
     B, H, D = 2, 2, 64
     qb, kb, vb = (np.swapaxes(x, 1, 2) for x in make_batch(B, H, T, D, seed=5))
     qk = scfa.random_keep(B, T, H, drop, 11)
@@ -68,15 +69,16 @@ def test_qk_end_to_end(T, drop):
     dv = dv * (kk.transpose(0, 2, 1)[..., None] > 0)
     o = scfa.qk_sparse_attention(_t(qb), _t(kb), _t(vb), _t(qk), _t(kk))
     _check("O", _np(o), eng(O))
-    o2, gq, gk, gv = scfa.qk_sparse_attention_fwd_bwd(_t(qb), _t(kb), _t(vb), _t(qk), _t(kk), _t(dO))
+    o2, gq, gk, gv = scfa.qk_sparse_attention_fwd_bwd(_t(qb), _t(kb), _t(vb), _t(qk), _t(kk), _t(dO), row_tables=rt)
     _check("O2", _np(o2), eng(O))
     _check("dQ", _np(gq), eng(dq))
     _check("dK", _np(gk), eng(dk))
     _check("dV", _np(gv), eng(dv))
 
 
+@pytest.mark.parametrize("rt", [False, True], ids=["tiled", "rowtables"])
 @pytest.mark.parametrize("T,nb", [(256, 4), (1000, 16), (512, 1)])
-def test_hash_end_to_end(T, nb):
+def test_hash_end_to_end(T, nb, rt):
     B, H, D = 2, 2, 64
     qb, kb, vb = (np.swapaxes(x, 1, 2) for x in make_batch(B, H, T, D, seed=7))
     hb = scfa.random_buckets(B, T, H, nb, 9)
@@ -90,7 +92,7 @@ def test_hash_end_to_end(T, nb):
     ht = _t(hb)
     o = scfa.hash_sparse_attention(_t(qb), _t(kb), _t(vb), ht, ht)
     _check("O", _np(o), eng(O))
-    o2, gq, gk, gv = scfa.hash_sparse_attention_fwd_bwd(_t(qb), _t(kb), _t(vb), ht, ht, _t(dO))
+    o2, gq, gk, gv = scfa.hash_sparse_attention_fwd_bwd(_t(qb), _t(kb), _t(vb), ht, ht, _t(dO), row_tables=rt)
     _check("O2", _np(o2), eng(O))
     _check("dQ", _np(gq), eng(dq))
     _check("dK", _np(gk), eng(dk))
