@@ -47,6 +47,11 @@ enum Mode : int { MODE_FWD = 0, MODE_DQ = 1, MODE_DKDV = 2 };
 
 template <int kMode, int kD>
 struct Cfg {
+  // One CTA per SM runs NSTREAM independent item streams (two at D = 64: each has its
+  // own row warpgroup, producer warp, MMA warp, smem slots and 256 TMEM columns), and a
+  // shared epilogue warpgroup drains finished accumulators for both.
+  static constexpr int NSTREAM = (kD == 64) ? 2 : 1;
+  static constexpr int THREADS = 512;
   static constexpr int BM = 128;                             // stationary rows per work item
   static constexpr int BN = (kMode == MODE_FWD) ? 128 : 64;  // streamed rows per tile
   static constexpr int DCH = kD / 64;                        // 128-byte column chunks
@@ -61,32 +66,48 @@ struct Cfg {
   // accumulate MMAs: K feeds only S in the forward, V feeds only dP in dQ.
   static constexpr bool Y0_EARLY = (kMode == MODE_FWD);
   static constexpr bool Y1_EARLY = (kMode == MODE_DQ);
-  static constexpr int NS0 = (kMode == MODE_FWD && kD == 64) ? 2 : 3;  // keeps two CTAs per SM
-  static constexpr int NS1 = (kMode == MODE_FWD && kD == 64) ? 3 : 2;  // V has the shorter lead
-  // TMEM
-  static constexpr int TM_COLS = (kD == 64) ? 256 : 512;
+  static constexpr int NS0 = (kMode == MODE_FWD) ? 2 : 3;
+  static constexpr int NS1 = (kMode == MODE_FWD) ? ((kD == 64) ? 3 : 2) : 2;
+  // TMEM (per stream)
+  static constexpr int TM_COLS = 512;  // allocated once per CTA
+  static constexpr int TM_STREAM = TM_COLS / NSTREAM;
   static constexpr int TM_S = 0;
   static constexpr int TM_DP = (kMode == MODE_FWD) ? 0 : BN;
   static constexpr int TM_ACC = 128;
   static constexpr int ACC_COLS = (kMode == MODE_DKDV) ? 2 * kD : kD;
   static constexpr int P_COLS = (kMode == MODE_DKDV) ? BN : BN / 2;
-  static constexpr bool OVERLAP = TM_ACC + ACC_COLS + P_COLS <= TM_COLS;
+  static constexpr bool OVERLAP = TM_ACC + ACC_COLS + P_COLS <= TM_STREAM;
   static constexpr int TM_P = OVERLAP ? TM_ACC + ACC_COLS : TM_S;                 // P | dS | P^T
   static constexpr int TM_P2 = OVERLAP ? TM_ACC + ACC_COLS + BN / 2 : TM_DP;      // dS^T (DKDV)
-  // shared memory (all TMA destinations 1024-aligned)
+  static_assert(TM_ACC + ACC_COLS <= TM_STREAM, "TMEM budget");
+  // shared memory per stream (all TMA destinations 1024-aligned)
   static constexpr int OFF_X = 0;
   static constexpr int OFF_Y0 = OFF_X + NXS * XSLOT_BYTES;
   static constexpr int OFF_Y1 = OFF_Y0 + NS0 * Y_BYTES;
   static constexpr int OFF_AUX = OFF_Y1 + NS1 * Y_BYTES;
-  static constexpr int OFF_BAR = OFF_AUX + NS0 * AUX_BYTES;
-  // s_full, s_free, p_full, p_free, acc_full, x_full/empty[NXS], y0_full/empty[NS0], y1_full/empty[NS1],
-  // q_full/empty[NQ] (work-item ring)
+  static constexpr int STREAM_BYTES = ((OFF_AUX + NS0 * AUX_BYTES + 1023) / 1024) * 1024;
+  // per-stream control block after all streams' tiles: s_full, s_free, p_full, p_free,
+  // acc_full, o_free, x_full/empty[NXS], y0_full/empty[NS0], y1_full/empty[NS1],
+  // q_full/empty[NQ] (work ring); the ring
   static constexpr int NQ = 4;
-  static constexpr int N_BARS = 5 + 2 * NXS + 2 * NS0 + 2 * NS1 + 2 * NQ;
+  static constexpr int N_BARS = 6 + 2 * NXS + 2 * NS0 + 2 * NS1 + 2 * NQ + 4;
+  static constexpr int OFF_BAR = 0;
   static constexpr int OFF_RING = OFF_BAR + 8 * N_BARS;  // int2 {item, tiles} x NQ
-  static constexpr int SMEM_BYTES = OFF_RING + 8 * NQ + 16;
+  static constexpr int CTRL_BYTES = ((OFF_RING + 8 * NQ + 15) / 16) * 16;
+  static constexpr int OFF_CTRL = NSTREAM * STREAM_BYTES;
+  // epilogue queues, one per TMEM lane quadrant (row warp q of either stream -> epilogue
+  // warp q), entries taken in ticket order: per quadrant eq_full[QE], eq_empty[QE], a
+  // ticket, entries {int4 info, float inv_l[32]}
+  static constexpr int QE = 3;
+  static constexpr int OFF_EQ = OFF_CTRL + NSTREAM * CTRL_BYTES;
+  static constexpr int EQ_ENTRY = 16 + 4 * 32;
+  static constexpr int EQQ_BYTES = 16 * QE + 16 + QE * EQ_ENTRY;  // one quadrant
+  static constexpr int EQ_BYTES = 4 * EQQ_BYTES;
+  static constexpr int SMEM_BYTES = OFF_EQ + EQ_BYTES + 16;
   static_assert(X_BYTES % 1024 == 0 && Y_BYTES % 1024 == 0, "TMA tiles must stay 1024-aligned");
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
+  // epilogue staging reuses the item's stationary slot
+  static_assert((kMode == MODE_FWD ? BM * kD * 2 : BM * kD * 4) <= XSLOT_BYTES, "staging fits the slot");
 };
 
 struct AttnArgs {
@@ -121,9 +142,9 @@ struct AttnArgs {
 // Diagnostics: per-CTA, per-tile clock64 stamps, 16 slots per tile (see scripts/timing.py).
 #define SCFA_STAMP_AT(i, k)                                                                   \
   if (args.dbg && (i) >= 0 && (i) < args.dbg_tiles)                                          \
-    args.dbg[(static_cast<size_t>(blockIdx.x) * args.dbg_tiles + (i)) * 16 + (k)] = clock64();
+    args.dbg[(static_cast<size_t>(dbg_cta) * args.dbg_tiles + (i)) * 16 + (k)] = clock64();
 #define SCFA_STAMP(k) \
-  if (threadIdx.x == 0) { SCFA_STAMP_AT(tg, k) }
+  if (r == 0) { SCFA_STAMP_AT(tg, k) }
 #define SCFA_MSTAMP(k) SCFA_STAMP_AT(tg, k)
 
 // Work index -> item (bh * n_row_blocks + rb).  Items are handed out dynamically
@@ -203,68 +224,271 @@ SCFA_DEVICE void tmem_ld_cols(uint32_t taddr, uint32_t* r) {
   for (int c = 0; c < N; c += 32) tmem_ld32(taddr + c, *reinterpret_cast<uint32_t(*)[32]>(r + c));
 }
 
+// Per-role stream context, declared inside each role after the register rebalancing so
+// that nothing is live across setmaxnreg.
+#define SCFA_STREAM_SETUP                                                                        \
+  uint8_t* smem = smem_base + s * C::STREAM_BYTES;                                               \
+  uint8_t* ctrl = smem_base + C::OFF_CTRL + s * C::CTRL_BYTES;                                   \
+  const int dbg_cta = blockIdx.x * C::NSTREAM + s;                                               \
+  (void)dbg_cta;                                                                                 \
+  const Bars B = bars_of<C>(ctrl);                                                               \
+  const MBar bar_s_full = B.s_full, bar_s_free = B.s_free, bar_p_full = B.p_full;                \
+  const MBar bar_p_free = B.p_free, bar_acc_full = B.acc_full, bar_x_full = B.x_full;            \
+  const MBar bar_x_empty = B.x_empty, bar_y0_full = B.y0_full, bar_y0_empty = B.y0_empty;        \
+  const MBar bar_y1_full = B.y1_full, bar_y1_empty = B.y1_empty, bar_q_full = B.q_full;          \
+  const MBar bar_q_empty = B.q_empty;                                                            \
+  (void)bar_s_full; (void)bar_s_free; (void)bar_p_full; (void)bar_p_free; (void)bar_acc_full;    \
+  (void)bar_x_full; (void)bar_x_empty; (void)bar_y0_full; (void)bar_y0_empty; (void)bar_y1_full; \
+  (void)bar_y1_empty; (void)bar_q_full; (void)bar_q_empty;                                       \
+  int2* ring = reinterpret_cast<int2*>(ctrl + C::OFF_RING);                                      \
+  int* work_ctr = const_cast<int*>(args.list_count) + args.n_items;                              \
+  const uint32_t tmem = *tmem_slot + static_cast<uint32_t>(s * C::TM_STREAM);                    \
+  (void)ring; (void)work_ctr; (void)tmem; (void)smem;
+
+struct Bars {
+  MBar s_full, s_free, p_full, p_free, acc_full, o_free, x_full, x_empty, y0_full, y0_empty, y1_full, y1_empty, q_full,
+      q_empty;
+};
+
+template <class C>
+SCFA_DEVICE Bars bars_of(uint8_t* base) {
+  Bars b;
+  const MBar p0(smem_u32(base + C::OFF_BAR));
+  int i = 0;
+  b.s_full = p0 + i++;
+  b.s_free = p0 + i++;
+  b.p_full = p0 + i++;
+  b.p_free = p0 + i++;
+  b.acc_full = p0 + i++;
+  b.o_free = p0 + i++;
+  b.x_full = p0 + i;
+  i += C::NXS;
+  b.x_empty = p0 + i;
+  i += C::NXS;
+  b.y0_full = p0 + i;
+  i += C::NS0;
+  b.y0_empty = p0 + i;
+  i += C::NS0;
+  b.y1_full = p0 + i;
+  i += C::NS1;
+  b.y1_empty = p0 + i;
+  i += C::NS1;
+  b.q_full = p0 + i;
+  i += C::NQ;
+  b.q_empty = p0 + i;
+  return b;
+}
+
+// One bounded wait: suspends the warp (no issue slots) until the phase completes or
+// about `ns` nanoseconds pass; returns whether it completed.
+SCFA_DEVICE bool mbar_try(MBar bar, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(bar.a), "r"(parity), "r"(ns)
+      : "memory");
+  return ok != 0;
+}
+
+// ------------------------------------------------------------------ epilogue warpgroup
+// Drains finished items of both streams: waits for an item handed over by the row
+// threads (mailbox) and its accumulators (acc_full), reads them out of TMEM, releases
+// them (o_free: the stream's next item may accumulate), stages the rows in the item's
+// stationary slot and copies them out — each row to its original position — then hands
+// the slot back to the producer (x_empty).  The row threads never wait for any of it.
 template <int kMode, int kD>
-__global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
+SCFA_DEVICE void epilogue_wg(const AttnArgs& args, uint8_t* smem_base, uint32_t tmem0, int warp, int lane,
+                             int dbg_cta0) {
+  using C = Cfg<kMode, kD>;
+  const int r = threadIdx.x & 127;
+  const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+  int cnt[2] = {0, 0};
+  int live_streams = C::NSTREAM;
+  uint8_t* eqb = smem_base + C::OFF_EQ + (warp & 3) * C::EQQ_BYTES;
+  const MBar eq(smem_u32(eqb));
+  for (int k = 0; live_streams > 0; ++k) {
+    {
+      const int slot = k % C::QE;
+      mbar_wait_lazy(eq + slot, (k / C::QE) & 1);
+      const uint8_t* ent = eqb + 16 * C::QE + 16 + slot * C::EQ_ENTRY;
+      const int4 info = *reinterpret_cast<const int4*>(ent);
+      const float inv_l = reinterpret_cast<const float*>(ent + 16)[lane];
+      mbar_arrive(eq + C::QE + slot);
+      if (info.y < 0) {  // a stream's end
+        --live_streams;
+        continue;
+      }
+      const int s = info.x;
+      const int2 item = make_int2(info.y, info.z);
+      uint8_t* smem = smem_base + s * C::STREAM_BYTES;
+      uint8_t* ctrl = smem_base + C::OFF_CTRL + s * C::CTRL_BYTES;
+      const Bars B = bars_of<C>(ctrl);
+      const int ia = cnt[s]++;
+      const int bh = item.x / args.n_row_blocks, rb = item.x - bh * args.n_row_blocks;
+      const int row = rb * C::BM + r;
+      const size_t foff = static_cast<size_t>(bh) * args.T_rows_pad + row;
+      const int pos = args.x_rows ? args.x_rows[foff] : args.row_idx[foff];
+      size_t orow = 0;
+      const bool live = out_row(args, bh, row, pos, orow);
+      const uint32_t t_acc = tmem0 + static_cast<uint32_t>(s * C::TM_STREAM) + lane_off + C::TM_ACC;
+      uint8_t* stage = smem + C::OFF_X + (ia % C::NXS) * C::XSLOT_BYTES;
+      mbar_wait_lazy(B.acc_full, ia & 1);
+      tc_fence_after();
+      if (kMode == MODE_FWD) {
+        constexpr int RB = kD * 2;  // bf16 output row
+#pragma unroll
+        for (int c = 0; c < kD; c += 32) {
+          uint32_t v[32];
+          tmem_ld32(t_acc + c, v);
+          tmem_wait_ld();
+          uint32_t w[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            w[i] = pack_bf16(__uint_as_float(v[2 * i]) * inv_l, __uint_as_float(v[2 * i + 1]) * inv_l);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) stage_put<RB>(stage, r, c / 8 + i, w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+        }
+        tc_fence_before();
+        mbar_arrive(B.o_free);
+        stage_copy_out<RB>(stage, warp & 3, lane, reinterpret_cast<uint8_t*>(args.out_o), static_cast<long long>(orow) * RB,
+                           live);
+      } else if (kMode == MODE_DQ) {
+        constexpr int RB = kD * 4;
+#pragma unroll
+        for (int c = 0; c < kD; c += 32) {
+          uint32_t v[32];
+          tmem_ld32(t_acc + c, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * args.scale);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) stage_put<RB>(stage, r, c / 4 + i, v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        }
+        tc_fence_before();
+        mbar_arrive(B.o_free);
+        stage_copy_out<RB>(stage, warp & 3, lane, reinterpret_cast<uint8_t*>(args.out0), static_cast<long long>(orow) * RB,
+                           live);
+      } else {
+        // dK (scale * acc[kD:2kD]) staged; at D = 64 dV (acc[0:kD]) is held in registers so
+        // the accumulators are released before either copy-out
+        constexpr int RB = kD * 4;
+#pragma unroll
+        for (int c = 0; c < kD; c += 32) {
+          uint32_t v[32];
+          tmem_ld32(t_acc + kD + c, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * args.scale);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) stage_put<RB>(stage, r, c / 4 + i, v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        }
+        if (kD == 64) {
+          uint32_t dv[kD];
+          tmem_ld32(t_acc, *reinterpret_cast<uint32_t(*)[32]>(dv));
+          tmem_ld32(t_acc + 32, *reinterpret_cast<uint32_t(*)[32]>(dv + 32));
+          tmem_wait_ld();
+          tc_fence_before();
+          mbar_arrive(B.o_free);
+          stage_copy_out<RB>(stage, warp & 3, lane, reinterpret_cast<uint8_t*>(args.out0),
+                             static_cast<long long>(orow) * RB, live);
+#pragma unroll
+          for (int i = 0; i < kD / 4; ++i) stage_put<RB>(stage, r, i, dv[4 * i], dv[4 * i + 1], dv[4 * i + 2], dv[4 * i + 3]);
+          stage_copy_out<RB>(stage, warp & 3, lane, reinterpret_cast<uint8_t*>(args.out1),
+                             static_cast<long long>(orow) * RB, live);
+        } else {
+          stage_copy_out<RB>(stage, warp & 3, lane, reinterpret_cast<uint8_t*>(args.out0),
+                             static_cast<long long>(orow) * RB, live);
+#pragma unroll
+          for (int c = 0; c < kD; c += 32) {
+            uint32_t v[32];
+            tmem_ld32(t_acc + c, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 8; ++i) stage_put<RB>(stage, r, c / 4 + i, v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          }
+          tc_fence_before();
+          mbar_arrive(B.o_free);
+          stage_copy_out<RB>(stage, warp & 3, lane, reinterpret_cast<uint8_t*>(args.out1),
+                             static_cast<long long>(orow) * RB, live);
+        }
+      }
+      fence_proxy_async_smem();  // the next TMA load into this slot comes after these accesses
+      mbar_arrive(B.x_empty + (ia % C::NXS));
+    }
+  }
+}
+
+template <int kMode, int kD>
+__global__ void __launch_bounds__(512, 1)
     scfa_attn_kernel(const __grid_constant__ CUtensorMap tm_x0, const __grid_constant__ CUtensorMap tm_x1,
                      const __grid_constant__ CUtensorMap tm_y0, const __grid_constant__ CUtensorMap tm_y1,
                      const AttnArgs args) {
   using C = Cfg<kMode, kD>;
-  extern __shared__ __align__(1024) uint8_t smem[];
+  extern __shared__ __align__(1024) uint8_t smem_base[];
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
-  uint64_t* bar_s_full = bars + 0;
-  uint64_t* bar_s_free = bars + 1;
-  uint64_t* bar_p_full = bars + 2;
-  uint64_t* bar_p_free = bars + 3;
-  uint64_t* bar_acc_full = bars + 4;
-  uint64_t* bar_x_full = bars + 5;
-  uint64_t* bar_x_empty = bar_x_full + C::NXS;
-  uint64_t* bar_y0_full = bar_x_empty + C::NXS;
-  uint64_t* bar_y0_empty = bar_y0_full + C::NS0;
-  uint64_t* bar_y1_full = bar_y0_empty + C::NS0;
-  uint64_t* bar_y1_empty = bar_y1_full + C::NS1;
-  uint64_t* bar_q_full = bar_y1_empty + C::NS1;
-  uint64_t* bar_q_empty = bar_q_full + C::NQ;
-  int2* ring = reinterpret_cast<int2*>(smem + C::OFF_RING);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::OFF_RING + 8 * C::NQ);
-  int* work_ctr = const_cast<int*>(args.list_count) + args.n_items;  // [0] next item, [1] CTAs done
+  const int wg = warp >> 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_base + C::OFF_EQ + C::EQ_BYTES);
 
   if (threadIdx.x == 0) {
-    if (smem_u32(smem) & 1023) __trap();  // TMA SWIZZLE_128B destinations need 1024-byte alignment
-    mbar_init(bar_s_full, 1);
-    mbar_init(bar_s_free, 128);
-    mbar_init(bar_p_full, 128);
-    mbar_init(bar_p_free, 1);
-    mbar_init(bar_acc_full, 1);
-    for (int i = 0; i < C::NXS; ++i) {
-      mbar_init(bar_x_full + i, 1);
-      mbar_init(bar_x_empty + i, 128);  // released by the row threads after the epilogue (staging)
+    if (smem_u32(smem_base) & 1023) __trap();  // TMA SWIZZLE_128B destinations need 1024-byte alignment
+    for (int st = 0; st < C::NSTREAM; ++st) {
+      const Bars b = bars_of<C>(smem_base + C::OFF_CTRL + st * C::CTRL_BYTES);
+      mbar_init(b.s_full, 1);
+      mbar_init(b.s_free, 128);
+      mbar_init(b.p_full, 128);
+      mbar_init(b.p_free, 1);
+      mbar_init(b.acc_full, 1);
+      mbar_init(b.o_free, 128);  // epilogue threads: accumulators read, the next item may overwrite
+      for (int i = 0; i < C::NXS; ++i) {
+        mbar_init(b.x_full + i, 1);
+        mbar_init(b.x_empty + i, 128);  // released by the epilogue threads after staging
+      }
+      for (int i = 0; i < C::NS0; ++i) {
+        mbar_init(b.y0_full + i, 1);
+        mbar_init(b.y0_empty + i, 1);
+      }
+      for (int i = 0; i < C::NS1; ++i) {
+        mbar_init(b.y1_full + i, 1);
+        mbar_init(b.y1_empty + i, 1);
+      }
+      for (int i = 0; i < C::NQ; ++i) {
+        mbar_init(b.q_full + i, 1);
+        mbar_init(b.q_empty + i, 1 + 128);  // the MMA thread + the row threads
+      }
     }
-    for (int i = 0; i < C::NS0; ++i) {
-      mbar_init(bar_y0_full + i, 1);
-      mbar_init(bar_y0_empty + i, 1);
-    }
-    for (int i = 0; i < C::NS1; ++i) {
-      mbar_init(bar_y1_full + i, 1);
-      mbar_init(bar_y1_empty + i, 1);
-    }
-    for (int i = 0; i < C::NQ; ++i) {
-      mbar_init(bar_q_full + i, 1);
-      mbar_init(bar_q_empty + i, 1 + 128);  // the MMA thread + the row threads
+    for (int q = 0; q < 4; ++q) {
+      uint8_t* eqb = smem_base + C::OFF_EQ + q * C::EQQ_BYTES;
+      const MBar eq(smem_u32(eqb));
+      for (int i = 0; i < C::QE; ++i) {
+        mbar_init(eq + i, 32);          // a row warp: its quadrant of an item handed over
+        mbar_init(eq + C::QE + i, 32);  // the quadrant's epilogue warp: entry read
+      }
+      reinterpret_cast<int*>(eqb + 16 * C::QE)[0] = 0;  // ticket
     }
     fence_barrier_init();
   }
-  if (warp == 5) tmem_alloc<C::TM_COLS>(tmem_slot);
+  if (warp == 13) tmem_alloc<C::TM_COLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 4) {
+  // roles: warps 0-3 rows of stream 0, 4-7 rows of stream 1, 8-11 epilogue (both
+  // streams), 12 / 14 producer of stream 0 / 1, 13 / 15 MMA issuer of stream 0 / 1.
+  // Register rebalancing happens first thing inside each warpgroup's branch (nothing
+  // live across it, no merge after it): the row warpgroups take the file the epilogue /
+  // producer / MMA warps do not need.
+  constexpr int kRowRegs = (C::NSTREAM == 2) ? 176 : 240;
+  const int s = (wg < 2) ? wg : ((warp >= 12) ? ((warp - 12) >> 1) : 0);
+  const bool active = s < C::NSTREAM;
+  if (wg == 3) {
+   asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
+   if (((warp - 12) & 1) == 0 && active) {
     // ------------------------------------------------------------ TMA producer warp
+    SCFA_STREAM_SETUP
     if (lane == 0) {
       tma_prefetch_desc(&tm_x0);
       tma_prefetch_desc(&tm_y0);
@@ -284,7 +508,7 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
           e.y = args.list_count[e.x];
         }
         const int qs = k % C::NQ;
-        if (k >= C::NQ) mbar_wait(bar_q_empty + qs, ((k / C::NQ) - 1) & 1);
+        if (k >= C::NQ) mbar_wait_lazy(bar_q_empty + qs, ((k / C::NQ) - 1) & 1);
         ring[qs] = e;
         mbar_arrive(bar_q_full + qs);
       }
@@ -301,10 +525,9 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
       const int bh = lb / args.n_row_blocks, rb = lb - bh * args.n_row_blocks;
       const uint16_t* lst = args.list + static_cast<size_t>(lb) * args.list_stride;
       const int xs = ia % C::NXS;
-      if (ia >= C::NXS) mbar_wait(bar_x_empty + xs, ((ia / C::NXS) - 1) & 1);
+      if (ia >= C::NXS) mbar_wait_lazy(bar_x_empty + xs, ((ia / C::NXS) - 1) & 1);
       uint8_t* xb = smem + C::OFF_X + xs * C::XSLOT_BYTES;
       if (lane == 0) {
-        SCFA_STAMP_AT(tg, 10);
         mbar_arrive_expect_tx(bar_x_full + xs, C::XSLOT_BYTES);
       }
       __syncwarp();
@@ -331,7 +554,7 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
           r4 = __ldg(reinterpret_cast<const int4*>(args.y_rows + static_cast<size_t>(bh) * args.T_cols_pad + col0) + lane);
         // y0 ring (+ per-column lse2 / delta for dK/dV)
         const int st = tg % C::NS0;
-        if (tg >= C::NS0) mbar_wait(bar_y0_empty + st, ((tg / C::NS0) - 1) & 1);
+        if (tg >= C::NS0) mbar_wait_lazy(bar_y0_empty + st, ((tg / C::NS0) - 1) & 1);
         uint8_t* yb = smem + C::OFF_Y0 + st * C::Y_BYTES;
         if (lane == 0) {
           SCFA_STAMP_AT(tg, 14);
@@ -355,7 +578,7 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
         }
         // y1 ring
         const int st1 = tg % C::NS1;
-        if (tg >= C::NS1) mbar_wait(bar_y1_empty + st1, ((tg / C::NS1) - 1) & 1);
+        if (tg >= C::NS1) mbar_wait_lazy(bar_y1_empty + st1, ((tg / C::NS1) - 1) & 1);
         uint8_t* yb1 = smem + C::OFF_Y1 + st1 * C::Y_BYTES;
         if (lane == 0) {
           SCFA_STAMP_AT(tg, 15);
@@ -375,18 +598,21 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
       }
       ++ia;
     }
-  } else if (warp == 5) {
+   } else if (((warp - 12) & 1) == 1 && active) {
     // ------------------------------------------------------------ MMA issuer
+    SCFA_STREAM_SETUP
     if (lane == 0) {
       constexpr uint32_t idesc_s = make_idesc_bf16(128, C::BN, false, false);
       constexpr uint32_t idesc_acc = make_idesc_bf16(128, kD, false, true);
       // the accumulate MMAs of tile `p` (P V | dS K | P^T dO + dS^T Q)
+      int tg = 0, ia = 0;
       auto flush = [&](int ptg, bool first, bool last) {
         const int s0 = ptg % C::NS0, s1 = ptg % C::NS1;
-        if (kMode == MODE_FWD) mbar_wait(bar_y1_full + s1, (ptg / C::NS1) & 1);  // V not needed before
+        if (kMode == MODE_FWD) mbar_wait_lazy(bar_y1_full + s1, (ptg / C::NS1) & 1);  // V not needed before
         SCFA_STAMP_AT(ptg, 12);
-        mbar_wait(bar_p_full, ptg & 1);
+        mbar_wait_lazy(bar_p_full, ptg & 1);
         SCFA_STAMP_AT(ptg, 13);
+        if (first && ia > 0) mbar_wait_lazy(B.o_free, (ia - 1) & 1);  // the epilogue has read the previous item
         tc_fence_after();
         const uint32_t y0_addr = smem_u32(smem + C::OFF_Y0 + s0 * C::Y_BYTES);
         const uint32_t y1_addr = smem_u32(smem + C::OFF_Y1 + s1 * C::Y_BYTES);
@@ -412,12 +638,11 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
         umma_commit(bar_p_free);
         if (last) umma_commit(bar_acc_full);
       };
-      int tg = 0, ia = 0;
       int p_tg = -1;
       bool p_first = false, p_last = false;
       for (int k = 0;; ++k) {
         const int qs = k % C::NQ;
-        mbar_wait(bar_q_full + qs, (k / C::NQ) & 1);
+        mbar_wait_lazy(bar_q_full + qs, (k / C::NQ) & 1);
         const int2 item = ring[qs];
         mbar_arrive(bar_q_empty + qs);
         if (item.x < 0) break;
@@ -426,15 +651,15 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
         const int xs = ia % C::NXS;
         const uint32_t x0_addr = smem_u32(smem + C::OFF_X + xs * C::XSLOT_BYTES);
         const uint32_t x1_addr = x0_addr + C::X_BYTES;
-        mbar_wait(bar_x_full + xs, (ia / C::NXS) & 1);
+        mbar_wait_lazy(bar_x_full + xs, (ia / C::NXS) & 1);
         SCFA_STAMP_AT(tg, 9);
         for (int t = 0; t < n; ++t, ++tg) {
           const int s0 = tg % C::NS0, s1 = tg % C::NS1;
           SCFA_MSTAMP(6);
-          mbar_wait(bar_y0_full + s0, (tg / C::NS0) & 1);
-          if (kMode != MODE_FWD) mbar_wait(bar_y1_full + s1, (tg / C::NS1) & 1);
+          mbar_wait_lazy(bar_y0_full + s0, (tg / C::NS0) & 1);
+          if (kMode != MODE_FWD) mbar_wait_lazy(bar_y1_full + s1, (tg / C::NS1) & 1);
           if (C::OVERLAP) {
-            if (tg > 0) mbar_wait(bar_s_free, (tg - 1) & 1);
+            if (tg > 0) mbar_wait_lazy(bar_s_free, (tg - 1) & 1);
           } else if (p_tg >= 0) {
             flush(p_tg, p_first, p_last);  // aliased P: the accumulate MMAs must read it first
             p_tg = -1;
@@ -473,15 +698,40 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
         // The item's last tile accumulates now, not behind the next item's first S: the
         // row threads' epilogue waits for it, and the next item may not be ready yet.
         if (p_tg >= 0) flush(p_tg, p_first, p_last);
-        SCFA_STAMP_AT(p_tg, 11);
         p_tg = -1;
         ++ia;
       }
     }
+   }
+  } else if (wg == 2) {
+    // ------------------------------------------------------------ epilogue warpgroup
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 104;" ::: "memory");
+    epilogue_wg<kMode, kD>(args, smem_base, *tmem_slot, warp, lane, 0);
+  } else if (!active) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 24;" ::: "memory");  // idle row warpgroup (one stream)
   } else {
     // ------------------------------------------------------------ row threads
-    const int r = threadIdx.x;  // 0..127 == TMEM lane
-    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRowRegs) : "memory");
+    SCFA_STREAM_SETUP
+    const int r = threadIdx.x & 127;  // 0..127 == TMEM lane
+    // hand an item (or the stream's end, lb = -1) to the epilogue queue: a ticket per
+    // item keeps one queue for both streams in completion order
+    int tg = 0, ia = 0;
+    auto handoff = [&](int lb_, int n_, float inv_l_) {
+      // per row warp: quadrant (warp & 3) of the item goes to epilogue warp (warp & 3)
+      uint8_t* eqb = smem_base + C::OFF_EQ + (warp & 3) * C::EQQ_BYTES;
+      int tk = 0;
+      if (lane == 0) tk = atomicAdd(reinterpret_cast<int*>(eqb + 16 * C::QE), 1);
+      tk = __shfl_sync(0xffffffffu, tk, 0);
+      const int slot = tk % C::QE;
+      const MBar eq(smem_u32(eqb));
+      if (tk >= C::QE) mbar_wait(eq + C::QE + slot, ((tk / C::QE) - 1) & 1);
+      uint8_t* ent = eqb + 16 * C::QE + 16 + slot * C::EQ_ENTRY;
+      reinterpret_cast<float*>(ent + 16)[lane] = inv_l_;
+      if (lane == 0) *reinterpret_cast<int4*>(ent) = make_int4(s, lb_, n_, 0);
+      mbar_arrive(eq + slot);
+    };
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const uint32_t t_s = tmem + lane_off + C::TM_S;
     const uint32_t t_dp = tmem + lane_off + C::TM_DP;
     const uint32_t t_p = tmem + lane_off + C::TM_P;
@@ -490,7 +740,6 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
     const float sl = args.scale_log2;
     const float NEG_INF = -INFINITY;
     constexpr int NW = C::BN / 32;
-    int tg = 0, ia = 0;
     // per-item metadata is fetched one item ahead (its global-load latency hides behind
     // the current item), and each tile's list entry one tile ahead
     int nx_idx = 0, nx_e0 = 0;
@@ -665,33 +914,10 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
           mbar_arrive(bar_p_full);
           SCFA_STAMP(2);
         }
-        // ---------------- epilogue: O / l (fused scatter), M, L, lse2
+        // ---------------- hand O / l to the epilogue warpgroup; write M, L, lse2 here
+        const float inv_l = (l_run > 0.f) ? rcp_approx(l_run) : 0.f;
         if (n > 0) {
-          mbar_wait(bar_acc_full, ia & 1);
-          tc_fence_after();
-          if (threadIdx.x == 0) { SCFA_STAMP_AT(tg - 1, 4) }
-        }
-        const float inv_l = (l_run > 0.f) ? 1.f / l_run : 0.f;
-        if (n > 0) {
-          constexpr int RB = kD * 2;  // bf16 output row, staged in the freed stationary slot
-          uint8_t* stage = smem + C::OFF_X + (ia % C::NXS) * C::XSLOT_BYTES;
-#pragma unroll
-          for (int c = 0; c < kD; c += 32) {
-            uint32_t v[32];
-            tmem_ld32(t_acc + c, v);
-            tmem_wait_ld();
-            uint32_t w[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i)
-              w[i] = pack_bf16(__uint_as_float(v[2 * i]) * inv_l, __uint_as_float(v[2 * i + 1]) * inv_l);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) stage_put<RB>(stage, r, c / 8 + i, w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
-          }
-          stage_copy_out<RB>(stage, warp, lane, reinterpret_cast<uint8_t*>(args.out_o),
-                             static_cast<long long>(orow) * RB, live);
-          fence_proxy_async_smem();  // the next TMA load into this slot comes after these accesses
-          mbar_arrive(bar_x_empty + (ia % C::NXS));
-          tc_fence_before();  // O read before the next item's first accumulate (ordered by p_full)
+          handoff(lb, n, inv_l);
           ++ia;
         } else if (live) {
           uint4* dst = reinterpret_cast<uint4*>(args.out_o + orow * kD);
@@ -709,7 +935,6 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
         } else {
           args.out_lse2[roff] = INFINITY;  // pad slot: read (never used) by the dK/dV column loads
         }
-        if (threadIdx.x == 0) { SCFA_STAMP_AT(tg - 1, 8) }
       } else {
         // ---------------- backward passes: P and dS recomputed from (lse2, delta)
         float my_nlse = 0.f, my_ndelta = 0.f;
@@ -835,59 +1060,30 @@ __global__ void __launch_bounds__(192, (kD == 64) ? 2 : 1)
           mbar_arrive(bar_p_full);
           SCFA_STAMP(2);
         }
-        if (n > 0) {
-          mbar_wait(bar_acc_full, ia & 1);
-          tc_fence_after();
-          if (threadIdx.x == 0) { SCFA_STAMP_AT(tg - 1, 4) }
-        }
-        const int n_out = (kMode == MODE_DKDV) ? 2 : 1;
-        constexpr int RB = kD * 4;  // fp32 gradient row, staged in the freed stationary slot
-        uint8_t* stage = smem + C::OFF_X + (ia % C::NXS) * C::XSLOT_BYTES;
+        if (n > 0) {  // hand the accumulators to the epilogue warpgroup
+          handoff(lb, n, 0.f);
+          ++ia;
+        } else if (live) {
 #pragma unroll
-        for (int o = 0; o < n_out; ++o) {
-          // DQ: out0 = scale * dQ.  DKDV: out0 = scale * dK (acc + D), out1 = dV (acc).
-          const int col = (kMode == MODE_DKDV && o == 0) ? kD : 0;
-          const float mul = (o == 0) ? args.scale : 1.f;
-          float* dst = (o == 0) ? args.out0 : args.out1;
-          if (n > 0) {
-#pragma unroll
-            for (int c = 0; c < kD; c += 32) {
-              uint32_t v[32];
-              tmem_ld32(t_acc + col + c, v);
-              tmem_wait_ld();
-#pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * mul);
-#pragma unroll
-              for (int i = 0; i < 8; ++i) stage_put<RB>(stage, r, c / 4 + i, v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-            }
-            stage_copy_out<RB>(stage, warp, lane, reinterpret_cast<uint8_t*>(dst), static_cast<long long>(orow) * RB,
-                               live);
-          } else if (live) {
-            float4* d4 = reinterpret_cast<float4*>(dst + orow * kD);
+          for (int o = 0; o < ((kMode == MODE_DKDV) ? 2 : 1); ++o) {
+            float4* d4 = reinterpret_cast<float4*>(((o == 0) ? args.out0 : args.out1) + orow * kD);
 #pragma unroll
             for (int i = 0; i < kD / 4; ++i) d4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
           }
         }
-        if (n > 0) {
-          fence_proxy_async_smem();
-          mbar_arrive(bar_x_empty + (ia % C::NXS));
-        }
-        if (threadIdx.x == 0) { SCFA_STAMP_AT(tg - 1, 8) }
-        if (n > 0) {
-          tc_fence_before();
-          ++ia;
-        }
       }
     }
+    handoff(-1, 0, 0.f);  // end of the stream
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == 13) {
     tc_fence_after();
-    tmem_dealloc<C::TM_COLS>(tmem);
+    tmem_dealloc<C::TM_COLS>(*tmem_slot);
   }
   if (threadIdx.x == 0) {  // the last CTA to finish re-arms the work counter for the next launch
+    int* work_ctr = const_cast<int*>(args.list_count) + args.n_items;  // [0] next item, [1] CTAs done
     __threadfence();
     if (atomicAdd(work_ctr + 1, 1) == static_cast<int>(gridDim.x) - 1) {
       work_ctr[0] = 0;
@@ -982,34 +1178,42 @@ static int launch_mode(const AttnLaunch& L, cudaStream_t stream) {
   a.dbg = g_dbg_buf;
   a.dbg_tiles = g_dbg_tiles;
   auto kern = scfa_attn_kernel<kMode, kD>;
-  static int per_sm = 0;  // resident CTAs per SM: 2 at D = 64 (TMEM 256 cols each) when shared memory allows
-  if (per_sm == 0) {
+  static bool attr = false;  // one persistent CTA per SM, C::NSTREAM item streams in it
+  if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES) != cudaSuccess)
       return SCFA_ERR_CUDA;
-    int dev = 0, sm_smem = 0, reserved = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-    cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev);
-    per_sm = (C::TM_COLS <= 256 && 2 * (C::SMEM_BYTES + reserved) <= sm_smem) ? 2 : 1;
-    g_per_sm[kMode][kD == 64 ? 0 : 1] = per_sm;
+    g_per_sm[kMode][kD == 64 ? 0 : 1] = C::NSTREAM;
+    attr = true;
   }
   if (a.n_items == 0) return SCFA_OK;
-  int grid = sm_count() * per_sm;
-  if (grid > a.n_items) grid = a.n_items;
-  kern<<<grid, 192, C::SMEM_BYTES, stream>>>(mx0, mx1, my0, my1, a);
+  int grid = sm_count();
+  if (grid * C::NSTREAM > a.n_items) grid = (a.n_items + C::NSTREAM - 1) / C::NSTREAM;
+  kern<<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(mx0, mx1, my0, my1, a);
   return cudaGetLastError() == cudaSuccess ? SCFA_OK : SCFA_ERR_CUDA;
 }
 
+#ifndef SCFA_ONLY
+#define SCFA_ONLY(m, d) 1
+#endif
 int launch_attention(const AttnLaunch& L, cudaStream_t stream) {
-  if (L.D == 64) {
-    if (L.mode == MODE_FWD) return launch_mode<MODE_FWD, 64>(L, stream);
-    if (L.mode == MODE_DQ) return launch_mode<MODE_DQ, 64>(L, stream);
-    if (L.mode == MODE_DKDV) return launch_mode<MODE_DKDV, 64>(L, stream);
-  } else if (L.D == 128) {
-    if (L.mode == MODE_FWD) return launch_mode<MODE_FWD, 128>(L, stream);
-    if (L.mode == MODE_DQ) return launch_mode<MODE_DQ, 128>(L, stream);
-    if (L.mode == MODE_DKDV) return launch_mode<MODE_DKDV, 128>(L, stream);
-  }
+#if SCFA_ONLY(0, 64)
+  if (L.D == 64 && L.mode == MODE_FWD) return launch_mode<MODE_FWD, 64>(L, stream);
+#endif
+#if SCFA_ONLY(1, 64)
+  if (L.D == 64 && L.mode == MODE_DQ) return launch_mode<MODE_DQ, 64>(L, stream);
+#endif
+#if SCFA_ONLY(2, 64)
+  if (L.D == 64 && L.mode == MODE_DKDV) return launch_mode<MODE_DKDV, 64>(L, stream);
+#endif
+#if SCFA_ONLY(0, 128)
+  if (L.D == 128 && L.mode == MODE_FWD) return launch_mode<MODE_FWD, 128>(L, stream);
+#endif
+#if SCFA_ONLY(1, 128)
+  if (L.D == 128 && L.mode == MODE_DQ) return launch_mode<MODE_DQ, 128>(L, stream);
+#endif
+#if SCFA_ONLY(2, 128)
+  if (L.D == 128 && L.mode == MODE_DKDV) return launch_mode<MODE_DKDV, 128>(L, stream);
+#endif
   return SCFA_ERR_SHAPE;
 }
 

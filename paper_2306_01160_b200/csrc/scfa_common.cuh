@@ -41,26 +41,35 @@ SCFA_DEVICE bool elect_one() {
 
 // ---------------------------------------------------------------- mbarrier
 
-SCFA_DEVICE void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+// An mbarrier by its 32-bit shared-memory address (one register, immediate offsets).
+struct MBar {
+  uint32_t a;
+  SCFA_DEVICE MBar() : a(0) {}
+  SCFA_DEVICE explicit MBar(uint32_t addr) : a(addr) {}
+  SCFA_DEVICE MBar(uint64_t* p) : a(static_cast<uint32_t>(__cvta_generic_to_shared(p))) {}
+  SCFA_DEVICE MBar operator+(int i) const { return MBar(a + 8u * static_cast<uint32_t>(i)); }
+};
+
+SCFA_DEVICE void mbar_init(MBar bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar.a), "r"(count));
 }
 
 SCFA_DEVICE void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
-SCFA_DEVICE void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+SCFA_DEVICE void mbar_arrive(MBar bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar.a) : "memory");
 }
 
-SCFA_DEVICE void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+SCFA_DEVICE void mbar_arrive_expect_tx(MBar bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar.a),
                "r"(bytes)
                : "memory");
 }
 
-SCFA_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t addr = smem_u32(bar);
+SCFA_DEVICE void mbar_wait(MBar bar, uint32_t parity) {
+  uint32_t addr = bar.a;
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "WAIT_%=:\n\t"
@@ -68,6 +77,24 @@ SCFA_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!P1 bra WAIT_%=;\n\t}" ::"r"(addr),
       "r"(parity), "r"(0x989680)
       : "memory");
+}
+
+// Wait with back-off, for the warps that mostly wait (producer, MMA issuer, epilogue):
+// a failed probe sleeps instead of re-polling, so their spinning does not take issue
+// slots from the softmax warps on the same SM sub-partition.
+SCFA_DEVICE void mbar_wait_lazy(MBar bar, uint32_t parity, uint32_t sleep_ns = 64) {
+  uint32_t ok = 0;
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n\t}"
+        : "=r"(ok)
+        : "r"(bar.a), "r"(parity)
+        : "memory");
+    if (ok) break;
+    __nanosleep(sleep_ns);
+  }
 }
 
 // ---------------------------------------------------------------- proxies
@@ -83,12 +110,12 @@ SCFA_DEVICE void tma_prefetch_desc(const CUtensorMap* map) {
 }
 
 // 3-D tiled TMA load (coordinates innermost first) completing on `bar`.
-SCFA_DEVICE void tma_load_3d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+SCFA_DEVICE void tma_load_3d(void* smem_dst, const CUtensorMap* map, MBar bar, int c0, int c1,
                              int c2) {
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar.a), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
 
@@ -97,12 +124,12 @@ SCFA_DEVICE void tma_load_3d(void* smem_dst, const CUtensorMap* map, uint64_t* b
 // The 128-byte swizzle is a function of the shared-memory address, so 4-row groups
 // at 512-byte offsets of a 1024-aligned tile reproduce the tiled SWIZZLE_128B image
 // (measured: scripts/gather4_test.cu).
-SCFA_DEVICE void tma_gather4(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int r0, int r1, int r2,
+SCFA_DEVICE void tma_gather4(void* smem_dst, const CUtensorMap* map, MBar bar, int c0, int r0, int r1, int r2,
                              int r3) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar.a)
       : "memory");
 }
 
@@ -129,11 +156,11 @@ SCFA_DEVICE void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read
 SCFA_DEVICE void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 // Plain bulk copy global -> shared (16-byte aligned, size multiple of 16).
-SCFA_DEVICE void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+SCFA_DEVICE void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, MBar bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
           smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(gsrc)), "r"(bytes), "r"(smem_u32(bar))
+      "l"(reinterpret_cast<uint64_t>(gsrc)), "r"(bytes), "r"(bar.a)
       : "memory");
 }
 
@@ -157,10 +184,10 @@ SCFA_DEVICE void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_
 SCFA_DEVICE void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
 // Make `bar` track completion of every tcgen05.mma issued so far by this thread.
-SCFA_DEVICE void umma_commit(uint64_t* bar) {
+SCFA_DEVICE void umma_commit(MBar bar) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-          smem_u32(bar))
+          bar.a)
       : "memory");
 }
 
@@ -258,6 +285,14 @@ SCFA_DEVICE void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" 
 SCFA_DEVICE float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Approximate reciprocal (MUFU.RCP, no IEEE slow-path subroutine: kernels that use
+// setmaxnreg must not contain calls).
+SCFA_DEVICE float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 

@@ -18,7 +18,7 @@ import bench
 from paper_2306_01160_b200 import _lib, hash_sparse as hs
 from paper_2306_01160_b200._kernel import attention_backward, attention_forward
 
-TILES = 160
+TILES = 256
 SLOTS = 16
 
 cfg = dict(bench.CFG)
@@ -55,31 +55,44 @@ print("ctas/sm", [lib.scfa_debug_ctas_per_sm(m, 64) for m in range(3)])
 med = lambda x: float(np.median(x)) if len(x) else float("nan")
 for name, buf in bufs.items():
     d = buf.view(grid, TILES, SLOTS).cpu().numpy().astype(np.float64)
+    # whole-kernel view: per stream, first tile start .. last tile end (SM clocks differ per SM,
+    # so only per-stream spans are comparable)
+    spans, ntiles = [], []
+    for c in range(grid):
+        rr = d[c]
+        m = rr[:, 0] > 0
+        if m.sum() < 2:
+            continue
+        rr = rr[m]
+        spans.append(rr[:, 2].max() - rr[:, 0].min())
+        ntiles.append(len(rr))
+    spans, ntiles = np.array(spans), np.array(ntiles)
+    print(f"{name}: streams {len(spans)}  tiles/stream median {med(ntiles):.0f} max {ntiles.max()}"
+          f"  span clk median {med(spans):.0f} max {spans.max():.0f}  (truncated at {TILES} tiles)")
     for cta in (0, 1, grid // 2):
         r = d[cta]
         n = int((r[:, 0] > 0).sum())
         r = r[:n]
         if n < 3:
             continue
-        last = np.flatnonzero(r[:, 4] > 0)  # last tile of each item
-        first = np.flatnonzero(r[:, 9] > 0)  # first tile of each item
-        inner = np.setdiff1d(np.arange(n - 1), last)
-        per = np.diff(r[:, 0])
-        print(f"{name} cta {cta}: tiles {n} items {len(last)}  period(inner) {med(per[inner]):.0f}"
-              f"  period(boundary) {med(per[last[last < n - 1]]):.0f}  s_wait {med(r[:, 1] - r[:, 0]):.0f}"
-              f"  rows {med(r[:, 2] - r[:, 1]):.0f}")
-        print(f"   boundary: acc_wait {med(r[last, 4] - r[last, 2]):.0f}  epilogue {med(r[last, 8] - r[last, 4]):.0f}"
-              f"  next s_wait {med(r[last[last < n - 1] + 1, 1] - r[last[last < n - 1] + 1, 0]):.0f}"
-              f"  gap->next tile {med(r[last[last < n - 1] + 1, 0] - r[last[last < n - 1], 8]):.0f}")
-        print(f"   mma: wait_y/free {med(r[:, 7] - r[:, 6]):.0f}  issue_S {med(r[:, 3] - r[:, 7]):.0f}"
-              f"  flush {med(r[:, 5] - r[:, 3]):.0f}  last-acc after p_full {med(r[last, 11] - r[last, 2]):.0f}"
-              f"  x_full after X issue {med(r[first, 9] - r[first, 10]):.0f}")
+        first = np.flatnonzero(r[:, 9] > 0)  # first tile of each item (MMA stamp)
+        first = first[first > 0]
+        last = first - 1
+        inner = np.setdiff1d(np.arange(1, n), first)
+        per = np.diff(r[:, 0])  # per[i] = stamp0(i+1) - stamp0(i)
+        gap = r[1:n, 0] - r[:n - 1, 2]  # from a tile's p_full to the next tile's top
+        print(f"{name} stream {cta}: tiles {n} items {len(first) + 1}  period(inner) {med(per[inner - 1]):.0f}"
+              f"  period(item boundary) {med(per[first - 1]):.0f}  s_wait {med(r[:n, 1] - r[:n, 0]):.0f}"
+              f"  rows {med(r[:n, 2] - r[:n, 1]):.0f}  gap(inner) {med(gap[inner - 1]):.0f}  gap(boundary) {med(gap[first - 1]):.0f}")
+        print(f"   mma: wait_y/free {med(r[:n, 7] - r[:n, 6]):.0f}  issue_S {med(r[:n, 3] - r[:n, 7]):.0f}"
+              f"  flush {med(r[:n, 5] - r[:n, 3]):.0f}")
         print("   periods:", per[:14].astype(int).tolist())
+        L = last
+        print(f"   boundary: p_full->handoff start {med(r[L, 4] - r[L, 2]):.0f}  barriers+ticket {med(r[L, 8] - r[L, 4]):.0f}"
+              f"  queue wait {med(r[L, 10] - r[L, 8]):.0f}  write+arrive {med(r[L, 11] - r[L, 10]):.0f}"
+              f"  handoff end->next tile {med(r[L + 1, 0] - r[L, 11]):.0f}")
         # producer / flush detail (absolute clocks relative to the row threads' p_full stamp 2)
         rel = lambda a, b: med(r[:, a] - r[:, b])
         print(f"   K issue - s_full(row wait end) {rel(14, 1):.0f}  V issue - p_full {rel(15, 2):.0f}"
               f"  flush y1-ready - p_full {rel(12, 2):.0f}  flush p_full seen - p_full {rel(13, 2):.0f}")
-        lr = lambda a, b: med(r[last, a] - r[last, b])
-        print(f"   last tile: y1-ready - p_full {lr(12, 2):.0f}  p_full seen - p_full {lr(13, 2):.0f}"
-              f"  issued(11) - seen(13) {lr(11, 13):.0f}  acc seen(4) - issued(11) {lr(4, 11):.0f}"
-              f"  V issue(15) - p_full {lr(15, 2):.0f}")
+
