@@ -50,7 +50,11 @@ struct Cfg {
   // One CTA per SM runs NSTREAM independent item streams (two at D = 64: each has its
   // own row warpgroup, producer warp, MMA warp, smem slots and 256 TMEM columns), and a
   // shared epilogue warpgroup drains finished accumulators for both.
-  static constexpr int NSTREAM = (kD == 64) ? 2 : 1;
+  // Backward ("ALT"): one stream per CTA whose tiles alternate between the two row
+  // warpgroups (a tile's P / dS depend only on that tile), each with its own S / dP TMEM
+  // buffer, so S(t+1) runs while P(t) is computed and both warpgroups work at once.
+  static constexpr bool ALT = false;  // (kMode != MODE_FWD): measured slower — one MMA issuer per SM paces it
+  static constexpr int NSTREAM = ALT ? 1 : ((kD == 64) ? 2 : 1);
   static constexpr int THREADS = 512;
   static constexpr int BM = 128;                             // stationary rows per work item
   static constexpr int BN = (kMode == MODE_FWD) ? 128 : 64;  // streamed rows per tile
@@ -66,17 +70,22 @@ struct Cfg {
   // accumulate MMAs: K feeds only S in the forward, V feeds only dP in dQ.
   static constexpr bool Y0_EARLY = (kMode == MODE_FWD);
   static constexpr bool Y1_EARLY = (kMode == MODE_DQ);
-  static constexpr int NS0 = (kMode == MODE_FWD) ? 2 : 3;
-  static constexpr int NS1 = (kMode == MODE_FWD) ? ((kD == 64) ? 3 : 2) : 2;
+  static constexpr int NS0 = (kMode == MODE_FWD) ? 2 : ((ALT && kD == 64) ? 6 : 3);
+  static constexpr int NS1 = (kMode == MODE_FWD) ? ((kD == 64) ? 3 : 2) : ((ALT && kD == 64) ? 5 : 2);
   // TMEM (per stream)
   static constexpr int TM_COLS = 512;  // allocated once per CTA
   static constexpr int TM_STREAM = TM_COLS / NSTREAM;
+  // FWD: S [0,128) O [128,128+D) P bf16 [128+D, 192+D).  ALT: buffer j at j*128 holds
+  // S [0,64) and dP [64,128), with P / dS (bf16) written over them; accumulators at 256.
+  static constexpr int TM_BUF = 128;
+  // ALT: S / dP buffers in TMEM (tile t uses buffer t % NBUF, row warpgroup t % 2)
+  static constexpr int NBUF = (ALT && 3 * TM_BUF + ((kMode == MODE_DKDV) ? 2 * kD : kD) <= 512) ? 3 : 2;
   static constexpr int TM_S = 0;
   static constexpr int TM_DP = (kMode == MODE_FWD) ? 0 : BN;
-  static constexpr int TM_ACC = 128;
+  static constexpr int TM_ACC = ALT ? NBUF * TM_BUF : 128;
   static constexpr int ACC_COLS = (kMode == MODE_DKDV) ? 2 * kD : kD;
   static constexpr int P_COLS = (kMode == MODE_DKDV) ? BN : BN / 2;
-  static constexpr bool OVERLAP = TM_ACC + ACC_COLS + P_COLS <= TM_STREAM;
+  static constexpr bool OVERLAP = !ALT && (TM_ACC + ACC_COLS + P_COLS <= TM_STREAM);
   static constexpr int TM_P = OVERLAP ? TM_ACC + ACC_COLS : TM_S;                 // P | dS | P^T
   static constexpr int TM_P2 = OVERLAP ? TM_ACC + ACC_COLS + BN / 2 : TM_DP;      // dS^T (DKDV)
   static_assert(TM_ACC + ACC_COLS <= TM_STREAM, "TMEM budget");
@@ -90,7 +99,7 @@ struct Cfg {
   // acc_full, o_free, x_full/empty[NXS], y0_full/empty[NS0], y1_full/empty[NS1],
   // q_full/empty[NQ] (work ring); the ring
   static constexpr int NQ = 4;
-  static constexpr int N_BARS = 6 + 2 * NXS + 2 * NS0 + 2 * NS1 + 2 * NQ + 4;
+  static constexpr int N_BARS = 12 + 2 * NXS + 2 * NS0 + 2 * NS1 + 2 * NQ;
   static constexpr int OFF_BAR = 0;
   static constexpr int OFF_RING = OFF_BAR + 8 * N_BARS;  // int2 {item, tiles} x NQ
   static constexpr int CTRL_BYTES = ((OFF_RING + 8 * NQ + 15) / 16) * 16;
@@ -247,7 +256,7 @@ SCFA_DEVICE void tmem_ld_cols(uint32_t taddr, uint32_t* r) {
 
 struct Bars {
   MBar s_full, s_free, p_full, p_free, acc_full, o_free, x_full, x_empty, y0_full, y0_empty, y1_full, y1_empty, q_full,
-      q_empty;
+      q_empty;  // s_full / p_full / p_free: three consecutive barriers (TMEM buffers in ALT)
 };
 
 template <class C>
@@ -255,10 +264,13 @@ SCFA_DEVICE Bars bars_of(uint8_t* base) {
   Bars b;
   const MBar p0(smem_u32(base + C::OFF_BAR));
   int i = 0;
-  b.s_full = p0 + i++;
+  b.s_full = p0 + i;
+  i += 3;
   b.s_free = p0 + i++;
-  b.p_full = p0 + i++;
-  b.p_free = p0 + i++;
+  b.p_full = p0 + i;
+  i += 3;
+  b.p_free = p0 + i;
+  i += 3;
   b.acc_full = p0 + i++;
   b.o_free = p0 + i++;
   b.x_full = p0 + i;
@@ -311,18 +323,51 @@ SCFA_DEVICE void epilogue_wg(const AttnArgs& args, uint8_t* smem_base, uint32_t 
   const MBar eq(smem_u32(eqb));
   for (int k = 0; live_streams > 0; ++k) {
     {
-      const int slot = k % C::QE;
-      mbar_wait_lazy(eq + slot, (k / C::QE) & 1);
-      const uint8_t* ent = eqb + 16 * C::QE + 16 + slot * C::EQ_ENTRY;
-      const int4 info = *reinterpret_cast<const int4*>(ent);
-      const float inv_l = reinterpret_cast<const float*>(ent + 16)[lane];
-      mbar_arrive(eq + C::QE + slot);
-      if (info.y < 0) {  // a stream's end
-        --live_streams;
-        continue;
+      int s;
+      int2 item;
+      float inv_l = 0.f;
+      if (C::ALT) {  // one stream: follow its work ring (items finish in ring order)
+        s = 0;
+        const Bars B0 = bars_of<C>(smem_base + C::OFF_CTRL);
+        const int qs = k % C::NQ;
+        mbar_wait_lazy(B0.q_full + qs, (k / C::NQ) & 1);
+        item = reinterpret_cast<const int2*>(smem_base + C::OFF_CTRL + C::OFF_RING)[qs];
+        mbar_arrive(B0.q_empty + qs);
+        if (item.x < 0) {
+          --live_streams;
+          continue;
+        }
+        if (item.y == 0) {  // no visible pair in the block: zero gradients (and delta)
+          const int bh = item.x / args.n_row_blocks, rb = item.x - bh * args.n_row_blocks;
+          const int row = rb * C::BM + r;
+          const size_t foff = static_cast<size_t>(bh) * args.T_rows_pad + row;
+          const int pos = args.x_rows ? args.x_rows[foff] : args.row_idx[foff];
+          size_t orow = 0;
+          if (kMode == MODE_DQ && args.delta_out) args.delta_out[foff] = 0.f;
+          if (out_row(args, bh, row, pos, orow)) {
+#pragma unroll
+            for (int o = 0; o < ((kMode == MODE_DKDV) ? 2 : 1); ++o) {
+              float4* d4 = reinterpret_cast<float4*>(((o == 0) ? args.out0 : args.out1) + orow * kD);
+#pragma unroll
+              for (int i = 0; i < kD / 4; ++i) d4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+          }
+          continue;
+        }
+      } else {
+        const int slot = k % C::QE;
+        mbar_wait_lazy(eq + slot, (k / C::QE) & 1);
+        const uint8_t* ent = eqb + 16 * C::QE + 16 + slot * C::EQ_ENTRY;
+        const int4 info = *reinterpret_cast<const int4*>(ent);
+        inv_l = reinterpret_cast<const float*>(ent + 16)[lane];
+        mbar_arrive(eq + C::QE + slot);
+        if (info.y < 0) {  // a stream's end
+          --live_streams;
+          continue;
+        }
+        s = info.x;
+        item = make_int2(info.y, info.z);
       }
-      const int s = info.x;
-      const int2 item = make_int2(info.y, info.z);
       uint8_t* smem = smem_base + s * C::STREAM_BYTES;
       uint8_t* ctrl = smem_base + C::OFF_CTRL + s * C::CTRL_BYTES;
       const Bars B = bars_of<C>(ctrl);
@@ -438,10 +483,12 @@ __global__ void __launch_bounds__(512, 1)
     if (smem_u32(smem_base) & 1023) __trap();  // TMA SWIZZLE_128B destinations need 1024-byte alignment
     for (int st = 0; st < C::NSTREAM; ++st) {
       const Bars b = bars_of<C>(smem_base + C::OFF_CTRL + st * C::CTRL_BYTES);
-      mbar_init(b.s_full, 1);
+      for (int j = 0; j < 3; ++j) {
+        mbar_init(b.s_full + j, 1);
+        mbar_init(b.p_full + j, 128);
+        mbar_init(b.p_free + j, 1);
+      }
       mbar_init(b.s_free, 128);
-      mbar_init(b.p_full, 128);
-      mbar_init(b.p_free, 1);
       mbar_init(b.acc_full, 1);
       mbar_init(b.o_free, 128);  // epilogue threads: accumulators read, the next item may overwrite
       for (int i = 0; i < C::NXS; ++i) {
@@ -458,7 +505,8 @@ __global__ void __launch_bounds__(512, 1)
       }
       for (int i = 0; i < C::NQ; ++i) {
         mbar_init(b.q_full + i, 1);
-        mbar_init(b.q_empty + i, 1 + 128);  // the MMA thread + the row threads
+        // the MMA thread + the row threads (+ the second row warpgroup and the epilogue in ALT)
+        mbar_init(b.q_empty + i, C::ALT ? 1 + 128 + 128 + 128 : 1 + 128);
       }
     }
     for (int q = 0; q < 4; ++q) {
@@ -481,9 +529,9 @@ __global__ void __launch_bounds__(512, 1)
   // Register rebalancing happens first thing inside each warpgroup's branch (nothing
   // live across it, no merge after it): the row warpgroups take the file the epilogue /
   // producer / MMA warps do not need.
-  constexpr int kRowRegs = (C::NSTREAM == 2) ? 176 : 240;
-  const int s = (wg < 2) ? wg : ((warp >= 12) ? ((warp - 12) >> 1) : 0);
-  const bool active = s < C::NSTREAM;
+  constexpr int kRowRegs = (C::NSTREAM == 2 || C::ALT) ? 176 : 240;
+  const int s = C::ALT ? 0 : ((wg < 2) ? wg : ((warp >= 12) ? ((warp - 12) >> 1) : 0));
+  const bool active = C::ALT ? (wg < 2 || ((warp - 12) >> 1) == 0) : (s < C::NSTREAM);
   if (wg == 3) {
    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
    if (((warp - 12) & 1) == 0 && active) {
@@ -547,8 +595,12 @@ __global__ void __launch_bounds__(512, 1)
           if (C::NX == 2) tma_load_3d(xb + C::X_BYTES + c * C::BM * 128, &tm_x1, bar_x_full + xs, c * 64, rb * C::BM, bh);
         }
       }
+      // list entries one tile ahead: a dependent global load per tile would pace the
+      // whole stream at one L2 round trip per tile
+      int ent_next = lst[0];
       for (int t = 0; t < n; ++t, ++tg) {
-        const int col0 = (lst[t] & 0x7fff) * C::BN;
+        const int col0 = (ent_next & 0x7fff) * C::BN;
+        if (t + 1 < n) ent_next = lst[t + 1];
         int4 r4 = make_int4(0, 0, 0, 0);
         if (gy && lane < C::BN / 4)
           r4 = __ldg(reinterpret_cast<const int4*>(args.y_rows + static_cast<size_t>(bh) * args.T_cols_pad + col0) + lane);
@@ -600,8 +652,10 @@ __global__ void __launch_bounds__(512, 1)
     }
    } else if (((warp - 12) & 1) == 1 && active) {
     // ------------------------------------------------------------ MMA issuer
+    // The whole warp runs the loop (warp-uniform control flow keeps the descriptors in
+    // uniform registers); one elected lane issues the MMAs and their commits.
     SCFA_STREAM_SETUP
-    if (lane == 0) {
+    {
       constexpr uint32_t idesc_s = make_idesc_bf16(128, C::BN, false, false);
       constexpr uint32_t idesc_acc = make_idesc_bf16(128, kD, false, true);
       // the accumulate MMAs of tile `p` (P V | dS K | P^T dO + dS^T Q)
@@ -609,34 +663,39 @@ __global__ void __launch_bounds__(512, 1)
       auto flush = [&](int ptg, bool first, bool last) {
         const int s0 = ptg % C::NS0, s1 = ptg % C::NS1;
         if (kMode == MODE_FWD) mbar_wait_lazy(bar_y1_full + s1, (ptg / C::NS1) & 1);  // V not needed before
-        SCFA_STAMP_AT(ptg, 12);
-        mbar_wait_lazy(bar_p_full, ptg & 1);
-        SCFA_STAMP_AT(ptg, 13);
+        if (lane == 0) { SCFA_STAMP_AT(ptg, 12); }
+        const int jb = C::ALT ? (ptg % C::NBUF) : 0;  // TMEM buffer holding tile ptg's P / dS
+        mbar_wait(bar_p_full + jb, C::ALT ? ((ptg / C::NBUF) & 1) : (ptg & 1));
+        if (lane == 0) { SCFA_STAMP_AT(ptg, 13); }
         if (first && ia > 0) mbar_wait_lazy(B.o_free, (ia - 1) & 1);  // the epilogue has read the previous item
         tc_fence_after();
         const uint32_t y0_addr = smem_u32(smem + C::OFF_Y0 + s0 * C::Y_BYTES);
         const uint32_t y1_addr = smem_u32(smem + C::OFF_Y1 + s1 * C::Y_BYTES);
         const uint32_t acc = tmem + C::TM_ACC;
+        const uint32_t pb = tmem + jb * C::TM_BUF;
+        if (elect_one()) {
 #pragma unroll
         for (int k = 0; k < C::BN / 16; ++k) {
           const uint32_t on = (!first || k > 0);
           if (kMode == MODE_FWD) {  // O += P V
-            umma_ts(acc, tmem + C::TM_P + k * 8, make_sdesc_sw128(y1_addr + k * 2048, C::BN * 128, 1024), idesc_acc,
+            umma_ts(acc, pb + C::TM_P + k * 8, make_sdesc_sw128(y1_addr + k * 2048, C::BN * 128, 1024), idesc_acc,
                     on);
           } else if (kMode == MODE_DQ) {  // dQ += dS K
-            umma_ts(acc, tmem + C::TM_P + k * 8, make_sdesc_sw128(y0_addr + k * 2048, C::BN * 128, 1024), idesc_acc,
+            umma_ts(acc, pb + C::TM_P + k * 8, make_sdesc_sw128(y0_addr + k * 2048, C::BN * 128, 1024), idesc_acc,
                     on);
           } else {  // dV += P^T dO ; dK += dS^T Q
-            umma_ts(acc, tmem + C::TM_P + k * 8, make_sdesc_sw128(y1_addr + k * 2048, C::BN * 128, 1024), idesc_acc,
+            umma_ts(acc, pb + C::TM_P + k * 8, make_sdesc_sw128(y1_addr + k * 2048, C::BN * 128, 1024), idesc_acc,
                     on);
-            umma_ts(acc + kD, tmem + C::TM_P2 + k * 8, make_sdesc_sw128(y0_addr + k * 2048, C::BN * 128, 1024),
+            umma_ts(acc + kD, pb + C::TM_P2 + k * 8, make_sdesc_sw128(y0_addr + k * 2048, C::BN * 128, 1024),
                     idesc_acc, on);
           }
         }
         if (!C::Y0_EARLY) umma_commit(bar_y0_empty + s0);
         if (!C::Y1_EARLY) umma_commit(bar_y1_empty + s1);
-        umma_commit(bar_p_free);
+        umma_commit(bar_p_free + jb);
         if (last) umma_commit(bar_acc_full);
+        }
+        __syncwarp();
       };
       int p_tg = -1;
       bool p_first = false, p_last = false;
@@ -644,7 +703,7 @@ __global__ void __launch_bounds__(512, 1)
         const int qs = k % C::NQ;
         mbar_wait_lazy(bar_q_full + qs, (k / C::NQ) & 1);
         const int2 item = ring[qs];
-        mbar_arrive(bar_q_empty + qs);
+        if (lane == 0) mbar_arrive(bar_q_empty + qs);  // one arrival for the MMA warp
         if (item.x < 0) break;
         const int n = item.y;
         if (n == 0) continue;
@@ -652,29 +711,34 @@ __global__ void __launch_bounds__(512, 1)
         const uint32_t x0_addr = smem_u32(smem + C::OFF_X + xs * C::XSLOT_BYTES);
         const uint32_t x1_addr = x0_addr + C::X_BYTES;
         mbar_wait_lazy(bar_x_full + xs, (ia / C::NXS) & 1);
-        SCFA_STAMP_AT(tg, 9);
+        if (lane == 0) { SCFA_STAMP_AT(tg, 9); }
         for (int t = 0; t < n; ++t, ++tg) {
           const int s0 = tg % C::NS0, s1 = tg % C::NS1;
-          SCFA_MSTAMP(6);
+          if (lane == 0) { SCFA_MSTAMP(6); }
           mbar_wait_lazy(bar_y0_full + s0, (tg / C::NS0) & 1);
           if (kMode != MODE_FWD) mbar_wait_lazy(bar_y1_full + s1, (tg / C::NS1) & 1);
-          if (C::OVERLAP) {
+          const int j = C::ALT ? (tg % C::NBUF) : 0;  // TMEM buffer of this tile
+          if (C::ALT) {
+            if (tg >= C::NBUF) mbar_wait(bar_p_free + j, ((tg / C::NBUF) - 1) & 1);  // tile tg-NBUF accumulated
+          } else if (C::OVERLAP) {
             if (tg > 0) mbar_wait_lazy(bar_s_free, (tg - 1) & 1);
           } else if (p_tg >= 0) {
             flush(p_tg, p_first, p_last);  // aliased P: the accumulate MMAs must read it first
             p_tg = -1;
           }
-          SCFA_MSTAMP(7);
+          if (lane == 0) { SCFA_MSTAMP(7); }
           tc_fence_after();
           const uint32_t y0_addr = smem_u32(smem + C::OFF_Y0 + s0 * C::Y_BYTES);
           const uint32_t y1_addr = smem_u32(smem + C::OFF_Y1 + s1 * C::Y_BYTES);
           // S = X0 . Y0^T  (and dP = X1 . Y1^T), K = head dim, both operands K-major.
+          if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < kD / 16; ++k) {
             const uint32_t koff = (k & 3) * 32;
             const uint32_t a = x0_addr + (k >> 2) * (C::BM * 128) + koff;
             const uint32_t b = y0_addr + (k >> 2) * (C::BN * 128) + koff;
-            umma_ss(tmem + C::TM_S, make_sdesc_sw128(a, 16, 1024), make_sdesc_sw128(b, 16, 1024), idesc_s, k > 0);
+            umma_ss(tmem + j * C::TM_BUF + C::TM_S, make_sdesc_sw128(a, 16, 1024), make_sdesc_sw128(b, 16, 1024),
+                    idesc_s, k > 0);
           }
           if (kMode != MODE_FWD) {
 #pragma unroll
@@ -682,18 +746,21 @@ __global__ void __launch_bounds__(512, 1)
               const uint32_t koff = (k & 3) * 32;
               const uint32_t a = x1_addr + (k >> 2) * (C::BM * 128) + koff;
               const uint32_t b = y1_addr + (k >> 2) * (C::BN * 128) + koff;
-              umma_ss(tmem + C::TM_DP, make_sdesc_sw128(a, 16, 1024), make_sdesc_sw128(b, 16, 1024), idesc_s, k > 0);
+              umma_ss(tmem + j * C::TM_BUF + C::TM_DP, make_sdesc_sw128(a, 16, 1024), make_sdesc_sw128(b, 16, 1024),
+                      idesc_s, k > 0);
             }
           }
-          umma_commit(bar_s_full);
+          umma_commit(bar_s_full + j);
           if (C::Y0_EARLY) umma_commit(bar_y0_empty + s0);
           if (C::Y1_EARLY) umma_commit(bar_y1_empty + s1);
-          SCFA_MSTAMP(3);
+          }
+          __syncwarp();
+          if (lane == 0) { SCFA_MSTAMP(3); }
           if (p_tg >= 0) flush(p_tg, p_first, p_last);  // overlap: tile t-1 accumulates behind S(t)
           p_tg = tg;
           p_first = (t == 0);
           p_last = (t == n - 1);
-          SCFA_MSTAMP(5);
+          if (lane == 0) { SCFA_MSTAMP(5); }
         }
         // The item's last tile accumulates now, not behind the next item's first S: the
         // row threads' epilogue waits for it, and the next item may not be ready yet.
@@ -978,13 +1045,18 @@ __global__ void __launch_bounds__(512, 1)
             my_ndelta = -args.delta[roff];
           }
         }
+        // ALT: this warpgroup takes the stream's tiles with tg % 2 == wg, in TMEM buffer tg % NBUF
         for (int t = 0; t < n; ++t, ++tg) {
           const int entry = entry_next;
           if (t + 1 < n) entry_next = lst[t + 1];
+          if (C::ALT && (tg & 1) != wg) continue;
+          const int jb = C::ALT ? (tg % C::NBUF) : 0;
+          const uint32_t t_sb = t_s + jb * C::TM_BUF, t_dpb = t_dp + jb * C::TM_BUF;
+          const uint32_t t_pb = t_p + jb * C::TM_BUF, t_p2b = t_p2 + jb * C::TM_BUF;
           const bool full = (entry & 0x8000) != 0;
           const int col0 = (entry & 0x7fff) * C::BN;
           SCFA_STAMP(0);
-          mbar_wait(bar_s_full, tg & 1);
+          mbar_wait(bar_s_full + jb, C::ALT ? ((tg / C::NBUF) & 1) : (tg & 1));
           SCFA_STAMP(1);
           tc_fence_after();
           const float* clse = nullptr;
@@ -1002,17 +1074,15 @@ __global__ void __launch_bounds__(512, 1)
           } else {
             run_mask<NW>(run.x - col0, run.y - col0, vis);
           }
-          // 32-column chunks (bounded register pressure): read S and dP, compute P (and
-          // dS), store; the first store waits for the previous tile's accumulate MMAs,
-          // which read these columns.  (Aliased layout: chunk k's P/dS land in columns
-          // [16k, 16k+16) of S/dP, below the chunks still to be read.)
+          // 32-column chunks: read S and dP, compute P (and dS), store them over the
+          // columns already read (chunk k's P / dS land in columns [16k, 16k+16) of S / dP)
 #pragma unroll
           for (int cc = 0; cc < C::BN; cc += 32) {
             float sv[32], dv[32];
-            tmem_ld32(t_s + cc, *reinterpret_cast<uint32_t(*)[32]>(sv));
-            tmem_ld32(t_dp + cc, *reinterpret_cast<uint32_t(*)[32]>(dv));
+            tmem_ld32(t_sb + cc, *reinterpret_cast<uint32_t(*)[32]>(sv));
+            tmem_ld32(t_dpb + cc, *reinterpret_cast<uint32_t(*)[32]>(dv));
             tmem_wait_ld();
-            if (C::OVERLAP && cc + 32 == C::BN) {
+            if (!C::ALT && C::OVERLAP && cc + 32 == C::BN) {
               tc_fence_before();
               mbar_arrive(bar_s_free);
             }
@@ -1024,10 +1094,10 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
                 for (int e = 0; e < 4; ++e) { nl[e] = my_nlse; nd[e] = my_ndelta; }
               } else {
-                const float4 a = *reinterpret_cast<const float4*>(clse + c);
-                const float4 b = *reinterpret_cast<const float4*>(cdelta + c);
-                nl[0] = -a.x; nl[1] = -a.y; nl[2] = -a.z; nl[3] = -a.w;
-                nd[0] = -b.x; nd[1] = -b.y; nd[2] = -b.z; nd[3] = -b.w;
+                const float4 a4 = *reinterpret_cast<const float4*>(clse + c);
+                const float4 b4 = *reinterpret_cast<const float4*>(cdelta + c);
+                nl[0] = -a4.x; nl[1] = -a4.y; nl[2] = -a4.z; nl[3] = -a4.w;
+                nd[0] = -b4.x; nd[1] = -b4.y; nd[2] = -b4.z; nd[3] = -b4.w;
               }
 #pragma unroll
               for (int e = 0; e < 4; e += 2) {
@@ -1044,26 +1114,26 @@ __global__ void __launch_bounds__(512, 1)
                 pk_ds[(c - cc + e) >> 1] = pack_bf16(d0, d1);
               }
             }
-            if (cc == 0) {
+            if (!C::ALT && cc == 0) {  // the previous tile's accumulate MMAs read these columns
               if (tg > 0) mbar_wait(bar_p_free, (tg - 1) & 1);
               tc_fence_after();
             }
             if (kMode == MODE_DQ) {
-              tmem_st16(t_p + cc / 2, pk_ds);
+              tmem_st16(t_pb + cc / 2, pk_ds);
             } else {
-              tmem_st16(t_p + cc / 2, pk_p);
-              tmem_st16(t_p2 + cc / 2, pk_ds);
+              tmem_st16(t_pb + cc / 2, pk_p);
+              tmem_st16(t_p2b + cc / 2, pk_ds);
             }
           }
           tmem_wait_st();
           tc_fence_before();
-          mbar_arrive(bar_p_full);
+          mbar_arrive(bar_p_full + jb);
           SCFA_STAMP(2);
         }
-        if (n > 0) {  // hand the accumulators to the epilogue warpgroup
-          handoff(lb, n, 0.f);
+        if (n > 0) {  // accumulators to the epilogue (ALT: it follows the work ring itself)
+          if (!C::ALT) handoff(lb, n, 0.f);
           ++ia;
-        } else if (live) {
+        } else if (!C::ALT && live) {
 #pragma unroll
           for (int o = 0; o < ((kMode == MODE_DKDV) ? 2 : 1); ++o) {
             float4* d4 = reinterpret_cast<float4*>(((o == 0) ? args.out0 : args.out1) + orow * kD);
@@ -1073,7 +1143,7 @@ __global__ void __launch_bounds__(512, 1)
         }
       }
     }
-    handoff(-1, 0, 0.f);  // end of the stream
+    if (!C::ALT) handoff(-1, 0, 0.f);  // end of the stream
   }
 
   tc_fence_before();
