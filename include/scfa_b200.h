@@ -122,6 +122,13 @@ int scfa_gather_rows3(int n, const void* const* srcs, void* const* dsts, const i
                       const int64_t* strides, int elem_bytes, int64_t B, int64_t H, int64_t D,
                       const int64_t* T_perm, const int64_t* n_slots, void* stream);
 
+/* Source-ordered variant of scfa_gather_rows3: rows are read in memory order and row
+ * (b, t, h) is written to slot rank[b*H + h, t] of dst (B*H, n_slots, D) (slots >= n_slots
+ * dropped).  ranks[n] are (B*H, T) int32 inverse permutations; strides as gather_rows3.  */
+int scfa_permute_rows3(int n, const void* const* srcs, void* const* dsts, const int32_t* const* ranks,
+                       const int64_t* strides, int elem_bytes, int64_t B, int64_t T, int64_t H, int64_t D,
+                       const int64_t* n_slots, void* stream);
+
 /* Inverse: dst row (b,t,h) = src[bh, rank[bh,t]] if rank < n_slots else 0.
  * Replaces qk_postprocess (qk_sparse.py:214-225) and hash_scatter +
  * from_heads (hash_sparse.py:216-220,238).  src (B*H, n_slots, D) contiguous

@@ -477,6 +477,46 @@ __global__ void __launch_bounds__(256) gather_rows3_kernel(const __grid_constant
   }
 }
 
+// The same permutation as gather_rows3 driven from the source side: rows are read in
+// memory order (fully sequential) and each 128-byte row is written to its slot
+// rank[bh, t] (slots >= n_slots are dropped).  One tensor per blockIdx.y.
+__global__ void __launch_bounds__(256) permute_rows3_kernel(const __grid_constant__ GatherJobs J, int eb, int64_t T,
+                                                            int64_t H, int64_t D, int64_t B) {
+  const int64_t row_bytes = D * eb;
+  const int vecs = static_cast<int>(row_bytes / 16);
+  const int j = blockIdx.y;
+  const int64_t n_rows = B * T * H;
+  const int64_t total = n_rows * vecs;
+  const uint8_t* __restrict__ src = J.src[j];
+  uint8_t* __restrict__ dst = J.dst[j];
+  const int32_t* __restrict__ rank = J.perm[j];  // rank here: position -> slot
+  const int64_t n_slots = J.n_slots[j], sb = J.sb[j], st = J.st[j], sh = J.sh[j];
+  constexpr int U = 4;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t g0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; g0 < total; g0 += stride * U) {
+    uint4 v[U];
+    int64_t doff[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t g = g0 + u * stride;
+      doff[u] = -1;
+      if (g < total) {
+        const int64_t r = g / vecs;  // (b, t, h), h fastest
+        const int c = static_cast<int>(g - r * vecs);
+        const int64_t h = r % H, bt = r / H;
+        const int64_t t = bt % T, b = bt / T;
+        const int64_t bh = b * H + h;
+        const int32_t slot = __ldg(rank + bh * T + t);
+        v[u] = __ldg(reinterpret_cast<const uint4*>(src + (b * sb + t * st + h * sh) * eb) + c);
+        if (slot < n_slots) doff[u] = ((bh * n_slots + slot) * D) * eb + c * 16;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (doff[u] >= 0) *reinterpret_cast<uint4*>(dst + doff[u]) = v[u];
+  }
+}
+
 __global__ void gather_rows_kernel(const uint8_t* __restrict__ src, int eb, int64_t H, int64_t D, int64_t sb,
                                    int64_t st, int64_t sh, const int32_t* __restrict__ perm, int64_t T_perm,
                                    int64_t n_slots, uint8_t* __restrict__ dst, int64_t n_rows) {
@@ -815,6 +855,31 @@ extern "C" int scfa_gather_rows3(int n, const void* const* srcs, void* const* ds
   dim3 grid(static_cast<unsigned>(g), static_cast<unsigned>(n));
   gather_rows3_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(J, n, elem_bytes, H, D, B * H);
   return check_launch("gather_rows3");
+}
+
+extern "C" int scfa_permute_rows3(int n, const void* const* srcs, void* const* dsts, const int32_t* const* ranks,
+                                  const int64_t* strides, int elem_bytes, int64_t B, int64_t T, int64_t H, int64_t D,
+                                  const int64_t* n_slots, void* stream) {
+  if (n < 1 || n > 3) { set_error("permute_rows3: 1 to 3 tensors"); return SCFA_ERR_PARAM; }
+  if ((D * elem_bytes) % 16 != 0) { set_error("row bytes must be a multiple of 16"); return SCFA_ERR_SHAPE; }
+  GatherJobs J{};
+  for (int i = 0; i < n; ++i) {
+    J.src[i] = static_cast<const uint8_t*>(srcs[i]);
+    J.dst[i] = static_cast<uint8_t*>(dsts[i]);
+    J.perm[i] = ranks[i];
+    J.sb[i] = strides[3 * i];
+    J.st[i] = strides[3 * i + 1];
+    J.sh[i] = strides[3 * i + 2];
+    J.n_slots[i] = n_slots[i];
+    J.T_perm[i] = T;
+  }
+  const int64_t work = B * T * H * (D * elem_bytes / 16);
+  if (work == 0) return SCFA_OK;
+  int64_t g = (work + 256 * 4 - 1) / (256 * 4);
+  if (g > 148 * 16) g = 148 * 16;
+  dim3 grid(static_cast<unsigned>(g), static_cast<unsigned>(n));
+  permute_rows3_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(J, elem_bytes, T, H, D, B);
+  return check_launch("permute_rows3");
 }
 
 extern "C" int scfa_gather_rows(const void* src, int elem_bytes, int64_t B, int64_t H, int64_t D, int64_t sb,

@@ -379,7 +379,8 @@ def _fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, exclude_self=True, row_
     return outputs, dq, dk, dv, prob
 
 
-def hash_sparse_attention_fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, exclude_self=True, row_tables=False):
+def hash_sparse_attention_fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, exclude_self=True, row_tables=False,
+                                  out=None):
     """Forward + backward through the whole hash path, boundary layout in and out.
 
     Returns (O bf16, dQ, dK, dV fp32), each (B, T, H, D).  The reference
@@ -388,6 +389,62 @@ def hash_sparse_attention_fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, ex
     inverse permutation is fused into the kernels' epilogues (each row is stored at
     its original position) and, with row_tables=True, the forward permutation into
     their TMA gather loads.
+
+    Host (CPU) inputs are streamed: the batch is split per b and host->device copies,
+    the attention and device->host copies of consecutive batch elements overlap on
+    three CUDA streams (every (b, h) slice is independent, hash_sparse.py:223-238, so
+    the results are those of one call).  `out` may give the four host result tensors
+    (pinned memory keeps the copies asynchronous).
     """
-    outputs, dq, dk, dv, _ = _fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale, exclude_self, row_tables)
-    return outputs.O, dq, dk, dv
+    if not (isinstance(q, torch.Tensor) and not q.is_cuda):
+        outputs, dq, dk, dv, _ = _fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale, exclude_self, row_tables)
+        return outputs.O, dq, dk, dv
+    return _fwd_bwd_host(q, k, v, q_hash, k_hash, d_out, scale, exclude_self, out)
+
+
+_COPY_STREAMS = {}
+
+
+def _copy_streams(dev):
+    """Persistent H2D / D2H streams per device (the caching allocator pools by stream:
+    fresh streams per call would mean fresh cudaMalloc's every call)."""
+    if dev not in _COPY_STREAMS:
+        _COPY_STREAMS[dev] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+    return _COPY_STREAMS[dev]
+
+
+def _fwd_bwd_host(q, k, v, q_hash, k_hash, d_out, scale, exclude_self, out):
+    dev = torch.device("cuda", torch.cuda.current_device())
+    B, T, H, D = q.shape
+    same = k_hash is q_hash
+    q_hash, k_hash = torch.as_tensor(q_hash), torch.as_tensor(k_hash)
+    if out is None:
+        pin = torch.cuda.is_available()
+        out = [torch.empty((B, T, H, D), dtype=torch.bfloat16, pin_memory=pin)] + [
+            torch.empty((B, k.shape[1] if i else T, H, D), dtype=torch.float32, pin_memory=pin) for i in range(3)]
+    comp = torch.cuda.current_stream(dev)
+    h2d, d2h = _copy_streams(dev)
+    h2d.wait_stream(comp)
+    d2h.wait_stream(comp)
+    keep = []
+    for b in range(B):
+        sl = slice(b, b + 1)
+        with torch.cuda.stream(h2d):
+            xs = [t[sl].to(dev, non_blocking=True) for t in (q, k, v, d_out, q_hash)]
+            kh = xs[4] if same else k_hash[sl].to(dev, non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(h2d)
+        comp.wait_event(ready)
+        for t in xs + [kh]:
+            t.record_stream(comp)
+        outputs, dq, dk, dv, _ = _fwd_bwd(xs[0], xs[1], xs[2], xs[4], kh, xs[3], scale, exclude_self)
+        done = torch.cuda.Event()
+        done.record(comp)
+        with torch.cuda.stream(d2h):
+            d2h.wait_event(done)
+            for dst, src in zip(out, (outputs.O, dq, dk, dv)):
+                dst[sl].copy_(src, non_blocking=True)
+                src.record_stream(d2h)
+        keep.append((xs, kh, outputs, dq, dk, dv))
+    comp.wait_stream(d2h)  # results are on the host once the caller's stream reaches here
+    return tuple(out)

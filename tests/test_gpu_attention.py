@@ -97,3 +97,19 @@ def test_hash_end_to_end(T, nb, rt):
     _check("dQ", _np(gq), eng(dq))
     _check("dK", _np(gk), eng(dk))
     _check("dV", _np(gv), eng(dv))
+
+
+def test_hash_host_streaming_matches_device():
+    """Host inputs: per-batch streamed fwd+bwd equals the single device call bit for bit."""
+    B, H, T, D, nb = 3, 2, 640, 64, 8
+    rng = np.random.default_rng(21)
+    x = [torch.from_numpy(rng.standard_normal((B, T, H, D)).astype(np.float32)).to(torch.bfloat16) for _ in range(4)]
+    h = torch.from_numpy(scfa.random_buckets(B, T, H, nb, 3))
+    dev = [t.cuda() for t in x]
+    want = scfa.hash_sparse_attention_fwd_bwd(dev[0], dev[1], dev[2], h.cuda(), h.cuda(), dev[3])
+    host = [t.pin_memory() for t in x]
+    got = scfa.hash_sparse_attention_fwd_bwd(host[0], host[1], host[2], h, h, host[3])
+    torch.cuda.synchronize()
+    for a, b in zip(got, want):
+        assert not a.is_cuda
+        assert torch.equal(a, b.cpu())
