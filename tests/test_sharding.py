@@ -1,0 +1,71 @@
+"""(b, h) sharding across ranks: unit ranges, slices, and a world_size-2 gloo run on CPU.
+
+The per-segment compute is the NumPy oracle (test infrastructure) so the multi-process
+path — partition, independent per-segment calls, gather to rank 0 — is checked here
+without a GPU; on GPUs the same helpers run with the CUDA path and NCCL.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import scfa_oracle as orc
+from paper_2306_01160_b200.sharding import gather_segments, run_sharded, shard_segments
+
+
+@pytest.mark.parametrize("B,H,world", [(4, 12, 1), (4, 12, 2), (4, 12, 8), (3, 5, 4), (2, 3, 7)])
+def test_segments_partition_units(B, H, world):
+    seen = []
+    for r in range(world):
+        for b, h0, h1 in shard_segments(B, H, r, world):
+            assert 0 <= b < B and 0 <= h0 < h1 <= H
+            seen += [b * H + h for h in range(h0, h1)]
+    assert seen == list(range(B * H))  # contiguous, ordered, no overlap
+
+
+def _hash_oracle(q, k, v, hsh):
+    """(1, T, h, D) float64 slices -> oracle hash attention O (1, T, h, D), exclude_self."""
+    T = q.shape[1]
+    e = lambda x: np.swapaxes(x.numpy(), 1, 2)
+    hh = hsh.numpy().transpose(0, 2, 1)
+    pos = np.arange(T)
+    vis = orc.visibility(pos, pos, hh, hh, exclude_self=True)
+    O, _, _ = orc.attention(e(q), e(k), e(v), vis)
+    return (torch.from_numpy(np.swapaxes(O, 1, 2)),)
+
+
+def _worker(rank, world, port, q, k, v, hsh, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        res = run_sharded(_hash_oracle, [q, k, v, hsh], rank, world)
+        full = gather_segments(res, q.shape, torch.float64)
+        if rank == 0:
+            out.copy_(full[0])
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_two_rank_gloo_matches_single_process():
+    B, T, H, D = 2, 96, 3, 16
+    rng = np.random.default_rng(0)
+    q, k, v = (torch.from_numpy(rng.standard_normal((B, T, H, D))) for _ in range(3))
+    hsh = torch.from_numpy(rng.integers(0, 4, (B, T, H)))
+    out = torch.zeros((B, T, H, D), dtype=torch.float64).share_memory_()
+    mp.start_processes(_worker, args=(2, _free_port(), q, k, v, hsh, out), nprocs=2, join=True, start_method="fork")
+    want = torch.cat([torch.cat([_hash_oracle(q[b:b + 1, :, h:h + 1], k[b:b + 1, :, h:h + 1], v[b:b + 1, :, h:h + 1],
+                                              hsh[b:b + 1, :, h:h + 1])[0] for h in range(H)], dim=2)
+                      for b in range(B)])
+    assert torch.allclose(out, want, atol=1e-12)
