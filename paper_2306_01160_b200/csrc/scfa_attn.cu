@@ -53,7 +53,7 @@ struct Cfg {
   // Backward ("ALT"): one stream per CTA whose tiles alternate between the two row
   // warpgroups (a tile's P / dS depend only on that tile), each with its own S / dP TMEM
   // buffer, so S(t+1) runs while P(t) is computed and both warpgroups work at once.
-  static constexpr bool ALT = false;  // (kMode != MODE_FWD): measured slower — one MMA issuer per SM paces it
+  static constexpr bool ALT = (kMode == MODE_DKDV);  // measured: dK/dV gains, dQ loses (one MMA issuer paces it)
   static constexpr int NSTREAM = ALT ? 1 : ((kD == 64) ? 2 : 1);
   static constexpr int THREADS = 512;
   static constexpr int BM = 128;                             // stationary rows per work item
@@ -182,6 +182,11 @@ SCFA_DEVICE bool out_row(const AttnArgs& a, int bh, int row, int pos, size_t& of
   off = (static_cast<size_t>(b) * a.T_out + pos) * a.H + h;
   return true;
 }
+
+// Which element pairs of a 32-column chunk take the polynomial exp2 (FMA pipe) instead of
+// MUFU.  Measured: none — the loops are issue / latency bound rather than MUFU bound, and
+// the polynomial's extra instructions cost more than the MUFU time they free.
+SCFA_DEVICE constexpr bool kPolyPair(int pair) { return false && (pair & 3) == 3; }
 
 SCFA_DEVICE uint32_t bits_below(int n) { return n <= 0 ? 0u : (n >= 32 ? 0xffffffffu : ((1u << n) - 1u)); }
 
@@ -732,24 +737,22 @@ __global__ void __launch_bounds__(512, 1)
           const uint32_t y1_addr = smem_u32(smem + C::OFF_Y1 + s1 * C::Y_BYTES);
           // S = X0 . Y0^T  (and dP = X1 . Y1^T), K = head dim, both operands K-major.
           if (elect_one()) {
-#pragma unroll
-          for (int k = 0; k < kD / 16; ++k) {
-            const uint32_t koff = (k & 3) * 32;
-            const uint32_t a = x0_addr + (k >> 2) * (C::BM * 128) + koff;
-            const uint32_t b = y0_addr + (k >> 2) * (C::BN * 128) + koff;
-            umma_ss(tmem + j * C::TM_BUF + C::TM_S, make_sdesc_sw128(a, 16, 1024), make_sdesc_sw128(b, 16, 1024),
-                    idesc_s, k > 0);
-          }
-          if (kMode != MODE_FWD) {
+            // S and dP are independent accumulation chains: interleaving their K steps lets
+            // the tensor pipe overlap one chain's dependent steps with the other's
 #pragma unroll
             for (int k = 0; k < kD / 16; ++k) {
               const uint32_t koff = (k & 3) * 32;
-              const uint32_t a = x1_addr + (k >> 2) * (C::BM * 128) + koff;
-              const uint32_t b = y1_addr + (k >> 2) * (C::BN * 128) + koff;
-              umma_ss(tmem + j * C::TM_BUF + C::TM_DP, make_sdesc_sw128(a, 16, 1024), make_sdesc_sw128(b, 16, 1024),
+              const uint32_t a = x0_addr + (k >> 2) * (C::BM * 128) + koff;
+              const uint32_t b = y0_addr + (k >> 2) * (C::BN * 128) + koff;
+              umma_ss(tmem + j * C::TM_BUF + C::TM_S, make_sdesc_sw128(a, 16, 1024), make_sdesc_sw128(b, 16, 1024),
                       idesc_s, k > 0);
+              if (kMode != MODE_FWD) {
+                const uint32_t a1 = x1_addr + (k >> 2) * (C::BM * 128) + koff;
+                const uint32_t b1 = y1_addr + (k >> 2) * (C::BN * 128) + koff;
+                umma_ss(tmem + j * C::TM_BUF + C::TM_DP, make_sdesc_sw128(a1, 16, 1024), make_sdesc_sw128(b1, 16, 1024),
+                        idesc_s, k > 0);
+              }
             }
-          }
           umma_commit(bar_s_full + j);
           if (C::Y0_EARLY) umma_commit(bar_y0_empty + s0);
           if (C::Y1_EARLY) umma_commit(bar_y1_empty + s1);
@@ -882,7 +885,8 @@ __global__ void __launch_bounds__(512, 1)
                 tc_fence_before();
                 mbar_arrive(bar_s_free);  // S fully read: the next tile's S may overwrite it
               }
-              if (__any_sync(0xffffffffu, wv != 0xffffffffu)) {
+              const bool partial = __any_sync(0xffffffffu, wv != 0xffffffffu);
+              if (partial) {
 #pragma unroll
                 for (int c = 0; c < 32; ++c) x[c] = ((wv >> c) & 1u) ? x[c] : mask_val;
               }
@@ -954,8 +958,12 @@ __global__ void __launch_bounds__(512, 1)
               for (int c = 0; c < 32; c += 2) {
                 float a0, a1;
                 fma2(a0, a1, x[c], x[c + 1], sl, sl, nm, nm);
-                a0 = ex2(a0);
-                a1 = ex2(a1);
+                if (!partial && kPolyPair(c >> 1)) {  // no masked (-inf) inputs in this chunk
+                  ex2_poly2(a0, a1, a0, a1);
+                } else {
+                  a0 = ex2(a0);
+                  a1 = ex2(a1);
+                }
                 const int q = (c >> 1) & 1;
                 add2(la[2 * q], la[2 * q + 1], la[2 * q], la[2 * q + 1], a0, a1);
                 pk[c >> 1] = pack_bf16(a0, a1);
@@ -1103,8 +1111,12 @@ __global__ void __launch_bounds__(512, 1)
               for (int e = 0; e < 4; e += 2) {
                 float p0, p1, d0, d1;
                 fma2(p0, p1, sv[c - cc + e], sv[c - cc + e + 1], sl, sl, nl[e], nl[e + 1]);
-                p0 = ex2(p0);
-                p1 = ex2(p1);
+                if (kPolyPair((c - cc + e) >> 1)) {
+                  ex2_poly2(p0, p1, p0, p1);  // part of the exponentials on the FMA pipe
+                } else {
+                  p0 = ex2(p0);
+                  p1 = ex2(p1);
+                }
                 const uint32_t wv = vis[(c + e) >> 5];
                 p0 = ((wv >> ((c + e) & 31)) & 1u) ? p0 : 0.f;
                 p1 = ((wv >> ((c + e + 1) & 31)) & 1u) ? p1 : 0.f;

@@ -137,13 +137,25 @@ __global__ void __launch_bounds__(128) tile_list_kernel(const __grid_constant__ 
   __syncthreads();
   const int row = rb * kRowBlock + threadIdx.x;
   const int2 r = (row < J.T_rows_pad) ? J.runs[bh * J.T_rows_pad + row] : make_int2(0, 0);
-  if (r.y > r.x) {
-    atomicAdd(&diff[r.x / B], 1);
-    atomicAdd(&diff[(r.y - 1) / B + 1], -1);
-    atomicMax(&full_lo, (r.x + B - 1) / B);
-    atomicMin(&full_hi, r.y / B);
-  } else {
-    atomicMin(&full_hi, 0);  // a row that sees nothing: no tile of this block is full
+  // Rows of a bucket share run starts (and neighbours share ends): aggregate equal
+  // addresses within the warp before the shared-memory atomics, and reduce the full-tile
+  // bounds per warp, so no address sees 128 serialized updates.
+  const bool nonempty = r.y > r.x;
+  const int a_lo = nonempty ? r.x / B : -1 - static_cast<int>(threadIdx.x & 31);
+  const int a_hi = nonempty ? (r.y - 1) / B + 1 : -1 - static_cast<int>(threadIdx.x & 31);
+  {
+    const unsigned lo_peers = __match_any_sync(0xffffffffu, a_lo);
+    if (nonempty && (lo_peers & ((1u << (threadIdx.x & 31)) - 1u)) == 0) atomicAdd(&diff[a_lo], __popc(lo_peers));
+    const unsigned hi_peers = __match_any_sync(0xffffffffu, a_hi);
+    if (nonempty && (hi_peers & ((1u << (threadIdx.x & 31)) - 1u)) == 0) atomicAdd(&diff[a_hi], -__popc(hi_peers));
+  }
+  const int my_lo = nonempty ? (r.x + B - 1) / B : n_cb;  // first fully covered block
+  const int my_hi = nonempty ? r.y / B : 0;                // one past the last fully covered block
+  const int w_lo = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(nonempty ? my_lo : 0)) ;
+  const int w_hi = static_cast<int>(__reduce_min_sync(0xffffffffu, static_cast<unsigned>(my_hi)));
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&full_lo, w_lo);
+    atomicMin(&full_hi, w_hi);
   }
   __syncthreads();
   // ---- ascending compaction of {cb : prefix(diff)[cb] > 0}; thread i owns a chunk

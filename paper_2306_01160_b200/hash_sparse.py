@@ -366,13 +366,25 @@ def _fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, exclude_self=True, row_
     caller's tensors through row tables (no copies at all).
     """
     q, k, v = as_operand(q), as_operand(k), as_operand(v)
-    sb = _sort_batch(q, k, v, q_hash, k_hash, "bthd", check=False, exclude_self=exclude_self,
-                     materialize=not row_tables)
+    sb = _sort_batch(q, k, v, q_hash, k_hash, "bthd", check=False, exclude_self=exclude_self, materialize=False)
     prob = _problem_of(sb, exclude_self)
-    prob.schedule("fwd", "dq", "dkdv")  # runs + all three tile lists in one pass
     T_Q, T_KV = q.shape[1], k.shape[1]
     rows = prob.rows if row_tables else None
-    xq, xk, xv = (q, k, v) if row_tables else (sb.q, sb.k, sb.v)
+    if row_tables:
+        xq, xk, xv = q, k, v
+        prob.schedule("fwd", "dq", "dkdv")  # runs + all three tile lists in one pass
+    else:
+        # the bucket-ordered copies (side stream) and the tile lists (this stream) are
+        # independent: overlap them
+        main = torch.cuda.current_stream(q.device)
+        side = _copy_streams(q.device)[2]
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            xq, xk, xv = _gather3([q, k, v], [sb.q_perm, sb.k_perm, sb.k_perm], "bthd")
+        prob.schedule("fwd", "dq", "dkdv")
+        main.wait_stream(side)
+        for t in (xq, xk, xv):
+            t.record_stream(main)
     outputs = attention_forward(prob, xq, xk, xv, scale, boundary=(T_Q, False), rows=rows)
     dq, dk, dv = attention_backward(prob, xq, xk, xv, outputs, as_operand(d_out), scale,
                                     boundary=(T_Q, T_KV, False), rows=rows)
@@ -406,10 +418,10 @@ _COPY_STREAMS = {}
 
 
 def _copy_streams(dev):
-    """Persistent H2D / D2H streams per device (the caching allocator pools by stream:
-    fresh streams per call would mean fresh cudaMalloc's every call)."""
+    """Persistent H2D / D2H / side-work streams per device (the caching allocator pools
+    by stream: fresh streams per call would mean fresh cudaMalloc's every call)."""
     if dev not in _COPY_STREAMS:
-        _COPY_STREAMS[dev] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+        _COPY_STREAMS[dev] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev))
     return _COPY_STREAMS[dev]
 
 
@@ -423,7 +435,7 @@ def _fwd_bwd_host(q, k, v, q_hash, k_hash, d_out, scale, exclude_self, out):
         out = [torch.empty((B, T, H, D), dtype=torch.bfloat16, pin_memory=pin)] + [
             torch.empty((B, k.shape[1] if i else T, H, D), dtype=torch.float32, pin_memory=pin) for i in range(3)]
     comp = torch.cuda.current_stream(dev)
-    h2d, d2h = _copy_streams(dev)
+    h2d, d2h, _ = _copy_streams(dev)
     h2d.wait_stream(comp)
     d2h.wait_stream(comp)
     keep = []
