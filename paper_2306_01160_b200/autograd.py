@@ -1,0 +1,68 @@
+"""torch.autograd for the sparse attention calls.
+
+The reference API is forward-only (qk_sparse.py:228-239, hash_sparse.py:223-238);
+its backward exists only at kernel level (qk_backward_kernel / hash_backward_kernel).
+These Functions compose the same path as the reference's kernel-level backward
+(SURVEY.md §8c): the forward keeps the index preparation, bucket-ordered operands
+and saved log-sum-exp, and the backward runs the dQ and dK/dV kernels, whose
+epilogues write each gradient row straight back to its original position.
+"""
+
+import torch
+
+from ._kernel import as_operand, attention_backward, attention_forward
+
+__all__ = ["hash_sparse_attention_autograd", "qk_sparse_attention_autograd"]
+
+
+class _HashSparseAttention(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, q, k, v, q_hash, k_hash, scale, exclude_self):
+        from .hash_sparse import _problem_of, _sort_batch
+
+        qb, kb, vb = as_operand(q), as_operand(k), as_operand(v)
+        sb = _sort_batch(qb, kb, vb, q_hash, k_hash, "bthd", exclude_self=exclude_self)
+        prob = _problem_of(sb, exclude_self)
+        prob.schedule("fwd", "dq", "dkdv")
+        out = attention_forward(prob, sb.q, sb.k, sb.v, scale, boundary=(q.shape[1], False))
+        ctx.state = (prob, sb, out, scale, q.shape[1], k.shape[1], q.dtype, k.dtype, v.dtype)
+        return out.O.to(q.dtype)
+
+    @staticmethod
+    def backward(ctx, d_out):
+        prob, sb, out, scale, T_Q, T_KV, qt, kt, vt = ctx.state
+        dq, dk, dv = attention_backward(prob, sb.q, sb.k, sb.v, out, as_operand(d_out.contiguous()), scale,
+                                        boundary=(T_Q, T_KV, False))
+        ctx.state = None
+        return dq.to(qt), dk.to(kt), dv.to(vt), None, None, None, None
+
+
+class _QkSparseAttention(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, q, k, v, q_keep, k_keep, scale):
+        from .qk_sparse import qk_preprocess
+
+        prep = qk_preprocess(q, k, v, q_keep, k_keep)
+        prob = prep.problem
+        prob.schedule("fwd", "dq", "dkdv")
+        out = attention_forward(prob, prep.q_c, prep.k_c, prep.v_c, scale, boundary=(q.shape[1], True))
+        ctx.state = (prob, prep, out, scale, q.shape[1], k.shape[1], q.dtype, k.dtype, v.dtype)
+        return out.O.to(q.dtype)
+
+    @staticmethod
+    def backward(ctx, d_out):
+        prob, prep, out, scale, T_Q, T_KV, qt, kt, vt = ctx.state
+        dq, dk, dv = attention_backward(prob, prep.q_c, prep.k_c, prep.v_c, out, as_operand(d_out.contiguous()),
+                                        scale, boundary=(T_Q, T_KV, True))
+        ctx.state = None
+        return dq.to(qt), dk.to(kt), dv.to(vt), None, None, None
+
+
+def hash_sparse_attention_autograd(q, k, v, q_hash, k_hash, scale=None, exclude_self=True):
+    """hash_sparse_attention (hash_sparse.py:223-238) with gradients w.r.t. q, k, v."""
+    return _HashSparseAttention.apply(q, k, v, q_hash, k_hash, scale, exclude_self)
+
+
+def qk_sparse_attention_autograd(q, k, v, q_keep, k_keep, scale=None):
+    """qk_sparse_attention (qk_sparse.py:228-239) with gradients w.r.t. q, k, v."""
+    return _QkSparseAttention.apply(q, k, v, q_keep, k_keep, scale)

@@ -113,3 +113,26 @@ def test_hash_host_streaming_matches_device():
     for a, b in zip(got, want):
         assert not a.is_cuda
         assert torch.equal(a, b.cpu())
+
+
+@pytest.mark.parametrize("mode", ["hash", "qk"])
+def test_autograd_matches_fused_fwd_bwd(mode):
+    """dynamic_sparse_attention under autograd: same O and gradients as the *_fwd_bwd calls."""
+    B, H, T, D = 2, 2, 384, 64
+    rng = np.random.default_rng(8)
+    x = [torch.from_numpy(rng.standard_normal((B, T, H, D)).astype(np.float32)).to(torch.bfloat16).cuda()
+         for _ in range(4)]
+    if mode == "hash":
+        idx = torch.from_numpy(scfa.random_buckets(B, T, H, 8, 4)).cuda()
+        o2, gq, gk, gv = scfa.hash_sparse_attention_fwd_bwd(x[0], x[1], x[2], idx, idx, x[3])
+        qi = ki = idx
+    else:
+        qi = torch.from_numpy(scfa.random_keep(B, T, H, 0.5, 4)).cuda()
+        ki = torch.from_numpy(scfa.random_keep(B, T, H, 0.5, 5)).cuda()
+        o2, gq, gk, gv = scfa.qk_sparse_attention_fwd_bwd(x[0], x[1], x[2], qi, ki, x[3])
+    q, k, v = (t.float().requires_grad_(True) for t in x[:3])
+    o = scfa.dynamic_sparse_attention(q, k, v, qi, ki, sparsity_mode=mode)
+    o.backward(x[3].float())
+    assert torch.equal(o.detach().to(torch.bfloat16), o2)
+    for name, a, b in (("dQ", q.grad, gq), ("dK", k.grad, gk), ("dV", v.grad, gv)):
+        assert torch.equal(a, b), name
