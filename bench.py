@@ -148,6 +148,61 @@ def cpu_baseline(qkvd, buckets, cfg, max_seconds=30.0):
     }
 
 
+# ---------------------------------------------------------------- cfg3: QK-sparse at T = 16k
+
+def live_pairs_qk(q_keep, k_keep):
+    """Visible pairs of QK-sparse causal attention: per (b, h), sum over kept queries of the
+    kept keys at or before them."""
+    B, T, H = q_keep.shape
+    kc = np.cumsum(k_keep > 0, axis=1)  # kept keys at positions <= t
+    return int(np.sum(np.where(q_keep > 0, kc, 0)))
+
+
+def measure_qk_cfg3(args, dev, barrier, max_over_ranks, T=16384, drop=0.5):
+    """BASELINE.json configs[2] at drop 0.5: QK-sparse fwd+bwd, B=4 H=12 T=16384 D=64, next to
+    the dense causal comparator at the same shape (extra fields of the bench line)."""
+    import torch
+
+    import paper_2306_01160_b200 as scfa
+
+    B, H, D = 4, 12, 64
+    gen = torch.Generator(device=dev).manual_seed(16)
+    q, k, v, dO = (torch.randn((B, T, H, D), device=dev, generator=gen).to(torch.bfloat16) for _ in range(4))
+    qk = scfa.random_keep(B, T, H, drop, 6)
+    kk = scfa.random_keep(B, T, H, drop, 7)
+    qkd, kkd = torch.from_numpy(qk).to(dev), torch.from_numpy(kk).to(dev)
+    p_live = live_pairs_qk(qk, kk)
+    stream = torch.cuda.current_stream()
+
+    def timed(fn):
+        for _ in range(args.warmup):
+            fn()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            fn()
+        e1.record(stream)
+        barrier()
+        return max_over_ranks(e0.elapsed_time(e1) / args.steps)
+
+    ms = timed(lambda: scfa.qk_sparse_attention_fwd_bwd(q, k, v, qkd, kkd, dO))
+    qe, ke, ve, de = (x.transpose(1, 2).contiguous() for x in (q, k, v, dO))
+
+    def dense():
+        o = scfa.flash_forward(qe, ke, ve)
+        scfa.flash_backward(qe, ke, ve, o, de)
+
+    dense_ms = timed(dense)
+    flops = 14.0 * D * p_live
+    return {"workload": f"cfg3: QK-sparse SCFA fwd+bwd, B={B} H={H} T={T} D={D}, drop {drop}",
+            "ms_per_step": ms, "effective_tflops": flops / (ms * 1e-3) / 1e12, "p_live": p_live,
+            "dense_causal_ms": dense_ms,
+            "dense_effective_tflops": 14.0 * D * B * H * T * (T + 1) / 2 / (dense_ms * 1e-3) / 1e12,
+            "speedup_vs_dense": dense_ms / ms,
+            "timing": "CUDA events, eager (QK prep reads the kept counts back once per call, qk_sparse.py:58)"}
+
+
 # ---------------------------------------------------------------- GPU arm
 
 def run_ours(args, cfg):
@@ -305,6 +360,8 @@ def run_ours(args, cfg):
     dense_flops = 14.0 * D * B * H * T * (T + 1) / 2
     del qe, ke, ve, de, o
 
+    cfg3 = None if args.no_cfg3 else measure_qk_cfg3(args, dev, barrier, max_over_ranks)
+
     # end to end through the public API with host buffers: H2D inputs, D2H outputs + gradients
     outs_host = [torch.empty(r.shape, dtype=r.dtype, pin_memory=True) for r in res]
     h2d = sum(x.numel() * x.element_size() for x in host) + host_h.numel() * host_h.element_size()
@@ -356,6 +413,8 @@ def run_ours(args, cfg):
                          "speedup_of_scfa": dense_ms / ms},
         "clocks": sampler.summary(),
     }
+    if cfg3 is not None:
+        line["cfg3_qk"] = cfg3
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(qkvd, buckets, cfg)
     if rank == 0:
@@ -399,6 +458,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cfg3", action="store_true", help="skip the QK-sparse T=16k side measurement")
     ap.add_argument("--T", type=int, default=None)
     args = ap.parse_args()
     cfg = dict(CFG)
