@@ -18,21 +18,39 @@ import bench
 from paper_2306_01160_b200 import _lib, hash_sparse as hs
 from paper_2306_01160_b200._kernel import attention_backward, attention_forward
 
-TILES = 256
+TILES = 512
 SLOTS = 16
 
+MODE = sys.argv[1] if len(sys.argv) > 1 else "hash"
 cfg = dict(bench.CFG)
 qkvd, buckets = bench.make_inputs(cfg)
 dev = torch.device("cuda")
 q, k, v, dO = (torch.from_numpy(x).to(dev, torch.bfloat16) for x in qkvd)
 hb = torch.from_numpy(buckets).to(dev)
 T = cfg["T"]
-sb = hs._sort_batch(q, k, v, hb, hb, "bthd", check=False)
-prob = hs._problem_of(sb, True)
-prob.schedule("fwd", "dq", "dkdv")
+if MODE == "dense":
+    from paper_2306_01160_b200.dense import causal_problem
+
+    qe, ke, ve, de = (x.transpose(1, 2).contiguous() for x in (q, k, v, dO))
+    prob = causal_problem(cfg["B"], cfg["H"], T, cfg["D"], dev)
+    prob.schedule("fwd", "dq", "dkdv")
+
+    class _SB:
+        pass
+
+    sb = _SB()
+    sb.q, sb.k, sb.v = qe, ke, ve
+    dO = de
+    run = lambda: (attention_forward(prob, sb.q, sb.k, sb.v), None)
+else:
+    sb = hs._sort_batch(q, k, v, hb, hb, "bthd", check=False)
+    prob = hs._problem_of(sb, True)
+    prob.schedule("fwd", "dq", "dkdv")
+bnd_f = None if MODE == "dense" else (T, False)
+bnd_b = None if MODE == "dense" else (T, T, False)
 for _ in range(3):
-    out = attention_forward(prob, sb.q, sb.k, sb.v, boundary=(T, False))
-    g = attention_backward(prob, sb.q, sb.k, sb.v, out, dO, boundary=(T, T, False))
+    out = attention_forward(prob, sb.q, sb.k, sb.v, boundary=bnd_f)
+    g = attention_backward(prob, sb.q, sb.k, sb.v, out, dO, boundary=bnd_b)
 torch.cuda.synchronize()
 lib = _lib.load()
 grid = 148 * max(1, max(lib.scfa_debug_ctas_per_sm(m, 64) for m in range(3)))
@@ -46,8 +64,8 @@ def hook(name, phase):
 
 
 _lib.EVENT_HOOK = hook
-out = attention_forward(prob, sb.q, sb.k, sb.v, boundary=(T, False))
-g = attention_backward(prob, sb.q, sb.k, sb.v, out, dO, boundary=(T, T, False))
+out = attention_forward(prob, sb.q, sb.k, sb.v, boundary=bnd_f)
+g = attention_backward(prob, sb.q, sb.k, sb.v, out, dO, boundary=bnd_b)
 torch.cuda.synchronize()
 _lib.EVENT_HOOK = None
 print("ctas/sm", [lib.scfa_debug_ctas_per_sm(m, 64) for m in range(3)])
