@@ -12,16 +12,16 @@ import torch
 
 from ._kernel import as_operand, attention_backward, attention_forward
 
-__all__ = ["hash_sparse_attention_autograd", "qk_sparse_attention_autograd"]
+__all__ = ["dense_causal_attention_autograd", "hash_sparse_attention_autograd", "qk_sparse_attention_autograd"]
 
 
 class _HashSparseAttention(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, q, k, v, q_hash, k_hash, scale, exclude_self):
+    def forward(ctx, q, k, v, q_hash, k_hash, scale, exclude_self, check):
         from .hash_sparse import _problem_of, _sort_batch
 
         qb, kb, vb = as_operand(q), as_operand(k), as_operand(v)
-        sb = _sort_batch(qb, kb, vb, q_hash, k_hash, "bthd", exclude_self=exclude_self)
+        sb = _sort_batch(qb, kb, vb, q_hash, k_hash, "bthd", exclude_self=exclude_self, check=check)
         prob = _problem_of(sb, exclude_self)
         prob.schedule("fwd", "dq", "dkdv")
         out = attention_forward(prob, sb.q, sb.k, sb.v, scale, boundary=(q.shape[1], False))
@@ -34,7 +34,7 @@ class _HashSparseAttention(torch.autograd.Function):
         dq, dk, dv = attention_backward(prob, sb.q, sb.k, sb.v, out, as_operand(d_out.contiguous()), scale,
                                         boundary=(T_Q, T_KV, False))
         ctx.state = None
-        return dq.to(qt), dk.to(kt), dv.to(vt), None, None, None, None
+        return dq.to(qt), dk.to(kt), dv.to(vt), None, None, None, None, None
 
 
 class _QkSparseAttention(torch.autograd.Function):
@@ -58,11 +58,51 @@ class _QkSparseAttention(torch.autograd.Function):
         return dq.to(qt), dk.to(kt), dv.to(vt), None, None, None
 
 
-def hash_sparse_attention_autograd(q, k, v, q_hash, k_hash, scale=None, exclude_self=True):
-    """hash_sparse_attention (hash_sparse.py:223-238) with gradients w.r.t. q, k, v."""
-    return _HashSparseAttention.apply(q, k, v, q_hash, k_hash, scale, exclude_self)
+def hash_sparse_attention_autograd(q, k, v, q_hash, k_hash, scale=None, exclude_self=True, check=True):
+    """hash_sparse_attention (hash_sparse.py:223-238) with gradients w.r.t. q, k, v.
+
+    check=False skips the bucket-id validation read-back (one host sync per call) for
+    callers whose ids are valid by construction, e.g. an argmax over LSH projections.
+    """
+    return _HashSparseAttention.apply(q, k, v, q_hash, k_hash, scale, exclude_self, check)
 
 
 def qk_sparse_attention_autograd(q, k, v, q_keep, k_keep, scale=None):
     """qk_sparse_attention (qk_sparse.py:228-239) with gradients w.r.t. q, k, v."""
     return _QkSparseAttention.apply(q, k, v, q_keep, k_keep, scale)
+
+
+_DENSE_PROBLEMS = {}
+
+
+class _DenseCausalAttention(torch.autograd.Function):
+    """The comparator (dense.py:33-93) on boundary-layout (B, T, H, D) operands: the
+    operands are transposed once into engine layout, the epilogues write O and the
+    gradients straight back to (B, T, H, D)."""
+
+    @staticmethod
+    def forward(ctx, q, k, v, scale):
+        from .dense import causal_problem
+
+        B, T, H, D = q.shape
+        eng = [as_operand(x).transpose(1, 2).contiguous() for x in (q, k, v)]
+        key = (B, H, T, D, eng[0].device)
+        prob = _DENSE_PROBLEMS.get(key)
+        if prob is None:  # the causal schedule depends on the shape only
+            prob = _DENSE_PROBLEMS[key] = causal_problem(B, H, T, D, eng[0].device)
+            prob.schedule("fwd", "dq", "dkdv")
+        out = attention_forward(prob, *eng, scale, boundary=(T, False))
+        ctx.state = (prob, eng, out, scale, T, q.dtype, k.dtype, v.dtype)
+        return out.O.to(q.dtype)
+
+    @staticmethod
+    def backward(ctx, d_out):
+        prob, eng, out, scale, T, qt, kt, vt = ctx.state
+        dq, dk, dv = attention_backward(prob, *eng, out, as_operand(d_out.contiguous()), scale, boundary=(T, T, False))
+        ctx.state = None
+        return dq.to(qt), dk.to(kt), dv.to(vt), None
+
+
+def dense_causal_attention_autograd(q, k, v, scale=None):
+    """Dense causal attention on (B, T, H, D) operands with gradients (dense.py:33-93)."""
+    return _DenseCausalAttention.apply(q, k, v, scale)
