@@ -20,7 +20,8 @@ from .errors import (
 )
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libscfa_b200.so")
+# SCFA_LIB overrides the path (A/B timing of two builds); the default is the in-tree build
+LIB_PATH = os.environ.get("SCFA_LIB") or os.path.join(_HERE, "lib", "libscfa_b200.so")
 
 OK = 0
 ERR_SHAPE, ERR_FORMAT, ERR_PARAM, ERR_NUMERIC, ERR_CONTRACT, ERR_CUDA = 1, 2, 3, 4, 5, 6

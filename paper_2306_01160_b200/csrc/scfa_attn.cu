@@ -665,14 +665,14 @@ __global__ void __launch_bounds__(512, 1)
       constexpr uint32_t idesc_acc = make_idesc_bf16(128, kD, false, true);
       // the accumulate MMAs of tile `p` (P V | dS K | P^T dO + dS^T Q)
       int tg = 0, ia = 0;
-      auto flush = [&](int ptg, bool first, bool last) {
+      auto flush = [&](int ptg, bool first, bool last, int pia) {
         const int s0 = ptg % C::NS0, s1 = ptg % C::NS1;
         if (kMode == MODE_FWD) mbar_wait_lazy(bar_y1_full + s1, (ptg / C::NS1) & 1);  // V not needed before
         if (lane == 0) { SCFA_STAMP_AT(ptg, 12); }
         const int jb = C::ALT ? (ptg % C::NBUF) : 0;  // TMEM buffer holding tile ptg's P / dS
         mbar_wait(bar_p_full + jb, C::ALT ? ((ptg / C::NBUF) & 1) : (ptg & 1));
         if (lane == 0) { SCFA_STAMP_AT(ptg, 13); }
-        if (first && ia > 0) mbar_wait_lazy(B.o_free, (ia - 1) & 1);  // the epilogue has read the previous item
+        if (first && pia > 0) mbar_wait_lazy(B.o_free, (pia - 1) & 1);  // the epilogue has read the previous item
         tc_fence_after();
         const uint32_t y0_addr = smem_u32(smem + C::OFF_Y0 + s0 * C::Y_BYTES);
         const uint32_t y1_addr = smem_u32(smem + C::OFF_Y1 + s1 * C::Y_BYTES);
@@ -702,10 +702,18 @@ __global__ void __launch_bounds__(512, 1)
         }
         __syncwarp();
       };
-      int p_tg = -1;
+      // The item's last tile accumulates behind the next item's first S, as inner tiles do,
+      // when the next item is already staged; otherwise (the producer is behind, or no
+      // item is left) it accumulates at once, since the epilogue waits for it.
+      constexpr bool kDeferLast = true;
+      int p_tg = -1, p_ia = 0;
       bool p_first = false, p_last = false;
       for (int k = 0;; ++k) {
         const int qs = k % C::NQ;
+        if (p_tg >= 0 && (!kDeferLast || !mbar_test(bar_q_full + qs, (k / C::NQ) & 1))) {
+          flush(p_tg, p_first, p_last, p_ia);
+          p_tg = -1;
+        }
         mbar_wait_lazy(bar_q_full + qs, (k / C::NQ) & 1);
         const int2 item = ring[qs];
         if (lane == 0) mbar_arrive(bar_q_empty + qs);  // one arrival for the MMA warp
@@ -715,6 +723,11 @@ __global__ void __launch_bounds__(512, 1)
         const int xs = ia % C::NXS;
         const uint32_t x0_addr = smem_u32(smem + C::OFF_X + xs * C::XSLOT_BYTES);
         const uint32_t x1_addr = x0_addr + C::X_BYTES;
+        if (p_tg >= 0 && !(mbar_test(bar_x_full + xs, (ia / C::NXS) & 1) &&
+                           mbar_test(bar_y0_full + tg % C::NS0, (tg / C::NS0) & 1))) {
+          flush(p_tg, p_first, p_last, p_ia);
+          p_tg = -1;
+        }
         mbar_wait_lazy(bar_x_full + xs, (ia / C::NXS) & 1);
         if (lane == 0) { SCFA_STAMP_AT(tg, 9); }
         for (int t = 0; t < n; ++t, ++tg) {
@@ -728,7 +741,7 @@ __global__ void __launch_bounds__(512, 1)
           } else if (C::OVERLAP) {
             if (tg > 0) mbar_wait_lazy(bar_s_free, (tg - 1) & 1);
           } else if (p_tg >= 0) {
-            flush(p_tg, p_first, p_last);  // aliased P: the accumulate MMAs must read it first
+            flush(p_tg, p_first, p_last, p_ia);  // aliased P: the accumulate MMAs must read it first
             p_tg = -1;
           }
           if (lane == 0) { SCFA_MSTAMP(7); }
@@ -759,18 +772,16 @@ __global__ void __launch_bounds__(512, 1)
           }
           __syncwarp();
           if (lane == 0) { SCFA_MSTAMP(3); }
-          if (p_tg >= 0) flush(p_tg, p_first, p_last);  // overlap: tile t-1 accumulates behind S(t)
+          if (p_tg >= 0) flush(p_tg, p_first, p_last, p_ia);  // overlap: tile t-1 accumulates behind S(t)
           p_tg = tg;
+          p_ia = ia;
           p_first = (t == 0);
           p_last = (t == n - 1);
           if (lane == 0) { SCFA_MSTAMP(5); }
         }
-        // The item's last tile accumulates now, not behind the next item's first S: the
-        // row threads' epilogue waits for it, and the next item may not be ready yet.
-        if (p_tg >= 0) flush(p_tg, p_first, p_last);
-        p_tg = -1;
         ++ia;
       }
+      if (p_tg >= 0) flush(p_tg, p_first, p_last, p_ia);
     }
    }
   } else if (wg == 2) {

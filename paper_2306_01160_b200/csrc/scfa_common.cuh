@@ -79,6 +79,19 @@ SCFA_DEVICE void mbar_wait(MBar bar, uint32_t parity) {
       : "memory");
 }
 
+// Non-blocking probe: has the phase with this parity completed?
+SCFA_DEVICE bool mbar_test(MBar bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(bar.a), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
 // Wait with back-off, for the warps that mostly wait (producer, MMA issuer, epilogue):
 // a failed probe sleeps instead of re-polling, so their spinning does not take issue
 // slots from the softmax warps on the same SM sub-partition.

@@ -10,6 +10,9 @@
 //   1 pipe    : as 0, the next chunk's ld issued before this chunk's exponentials
 //   2 nomax   : as 0 without the max chain / vote (exponent base fixed)
 //   3 mufu    : exponentials only on register data (no TMEM traffic)
+//   4 full+mma: as 0 while a ninth warp issues back-to-back M=128 N=64 K=16 MMAs into the
+//               unused TMEM columns [128,192) of both halves (TMEM / tensor-pipe contention)
+//   5 full+ts : as 4 with TS-mode MMAs (A = the P columns in TMEM, as the PV MMA)
 #include <stdio.h>
 
 #include "scfa_common.cuh"
@@ -81,13 +84,42 @@ __device__ __forceinline__ void tile(uint32_t t_s, uint32_t t_p, float sl, float
 }
 
 template <int V>
-__global__ void __launch_bounds__(256, 1) loop_kernel(int tiles, unsigned long long* out, float* sink) {
+__global__ void __launch_bounds__(288, 1) loop_kernel(int tiles, unsigned long long* out, float* sink) {
   __shared__ uint32_t slot;
+  __shared__ int done;
+  extern __shared__ __align__(1024) uint8_t dsm[];
   const int warp = threadIdx.x >> 5, wg = warp >> 2;
   if (warp == 0) tmem_alloc<512>(&slot);
+  if (threadIdx.x == 0) done = 0;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (warp == 8) {
+    __syncthreads();
+    if (V == 4 || V == 5) {
+      constexpr uint32_t idesc = make_idesc_bf16(128, 64, false, false);
+      constexpr uint32_t idesc_ts = make_idesc_bf16(128, 64, false, true);
+      const uint32_t a = smem_u32(dsm), b = smem_u32(dsm + 16384);
+      for (int it = 0; *reinterpret_cast<volatile int*>(&done) < 256 && it < 1000000; ++it) {
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            if (V == 4)
+              umma_ss(slot + 128 + (k & 1) * 256, make_sdesc_sw128(a + (k & 3) * 32, 16, 1024),
+                      make_sdesc_sw128(b + (k & 3) * 32, 16, 1024), idesc, 1);
+            else
+              umma_ts(slot + 128 + (k & 1) * 256, slot + 192 + (k & 1) * 256 + (k >> 1) * 8,
+                      make_sdesc_sw128(b + (k & 3) * 2048, 128 * 128, 1024), idesc_ts, 1);
+          }
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    tc_fence_before();
+    __syncthreads();
+    return;
+  }
   const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
   const uint32_t t_s = slot + lane_base + wg * 256, t_p = t_s + 192;
   // fill S with something finite
@@ -106,8 +138,10 @@ __global__ void __launch_bounds__(256, 1) loop_kernel(int tiles, unsigned long l
   const float sl = 0.18f;
   __syncthreads();
   const long long t0 = clock64();
-  for (int t = 0; t < tiles; ++t) tile<V>(t_s, t_p, sl, m_run, l_run, xr);
+  for (int t = 0; t < tiles; ++t) tile<(V >= 4) ? 0 : V>(t_s, t_p, sl, m_run, l_run, xr);
   const long long t1 = clock64();
+  atomicAdd(&done, 1);
+  __syncthreads();
   sink[blockIdx.x * 256 + threadIdx.x] = l_run + m_run + xr[3];
   if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
   tc_fence_before();
@@ -118,9 +152,11 @@ __global__ void __launch_bounds__(256, 1) loop_kernel(int tiles, unsigned long l
 template <int V>
 static void run(const char* name, unsigned long long* d, float* sink) {
   const int tiles = 512;
-  loop_kernel<V><<<148, 256>>>(tiles, d, sink);
-  cudaDeviceSynchronize();
-  loop_kernel<V><<<148, 256>>>(tiles, d, sink);
+  cudaFuncSetAttribute(loop_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+  for (int rep = 0; rep < 2; ++rep) {
+    loop_kernel<V><<<148, 288, 65536>>>(tiles, d, sink);
+    cudaDeviceSynchronize();
+  }
   cudaError_t e = cudaDeviceSynchronize();
   unsigned long long h[148];
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
@@ -141,5 +177,7 @@ int main() {
   run<1>("pipe", d, sink);
   run<2>("nomax", d, sink);
   run<3>("mufu", d, sink);
+  run<4>("full+mma", d, sink);
+  run<5>("full+ts", d, sink);
   return 0;
 }
