@@ -46,6 +46,7 @@ extern "C" {
 #define SCFA_DT_U8 2
 #define SCFA_DT_I32 3
 #define SCFA_DT_I64 4
+#define SCFA_DT_BF16 5 /* activations only (scfa_lsh_buckets) */
 
 /* attention flags */
 #define SCFA_FLAG_EXCLUDE_SELF 1 /* strict causality q_idx > k_idx (_kernel.py:83-84) */
@@ -284,6 +285,16 @@ int scfa_debug_timing(void* buf, int64_t tiles_per_cta);
 /* Resident CTAs per SM the attention launcher chose for pass `mode` (0 fwd, 1 dQ,
  * 2 dK/dV) at head dim D; 0 before the first launch, -1 for bad arguments.     */
 int scfa_debug_ctas_per_sm(int mode, int64_t D);
+
+/* Angular LSH bucket ids (lsh_buckets, hash_sparse.py:34-52) on the device.
+ * x: (B, T, H, D) activations of dtype SCFA_DT_F32 / _F64 / _BF16 with element strides
+ * (sb, st, sh, sd); R: (B*H, D, nb/2) float64 projections, contiguous (the reference draws
+ * them per (b, h) from its Philox stream, tensors.py:86-93); out[b*ob + t*ot + h*oh] =
+ * argmax([x R, -x R]) as int64 (first maximum).  Float64 arithmetic; nb even in [2, 64],
+ * D <= 192.  Replaces the reference's per-(b, h) numpy loop (hash_sparse.py:44-51).     */
+int scfa_lsh_buckets(const void* x, int x_dtype, int64_t B, int64_t T, int64_t H, int64_t D, int64_t sb,
+                     int64_t st, int64_t sh, int64_t sd, const double* R, int nb, int64_t* out, int64_t ob,
+                     int64_t ot, int64_t oh, void* stream);
 
 #ifdef __cplusplus
 }

@@ -147,3 +147,26 @@ def live_pairs_hash(q_hash, k_hash, exclude_self=True):
             c = np.bincount(q_hash[b, :, h])
             total += int(np.sum(c * (c - 1) // 2 + (0 if exclude_self else c)))
     return total
+
+
+# ---------------------------------------------------------------- bucket producer
+
+def philox_stream(seed, domain, index=0):
+    """numpy Generator for one (seed, domain, index) Philox key (tensors.py:86-93)."""
+    key = ((seed & ((1 << 64) - 1)) << 64) | ((domain & 0xFF) << 56) | (index & ((1 << 56) - 1))
+    return np.random.Generator(np.random.Philox(key=key))
+
+
+def lsh_buckets(x, nb, seed, domain_projections=1):
+    """Angular LSH ids (hash_sparse.py:34-52): per (b, h) R = D x nb/2 normal from the
+    (seed, DOMAIN_PROJECTIONS=1, b*H + h) stream, id = argmax([xR, -xR]) (first max)."""
+    x = np.asarray(x)
+    B, T, H, D = x.shape
+    out = np.empty((B, T, H), dtype=np.int64)
+    for b in range(B):
+        for h in range(H):
+            r = philox_stream(seed, domain_projections, b * H + h).standard_normal((D, nb // 2))
+            rot = x[b, :, h, :] @ r
+            out[b, :, h] = np.argmax(np.concatenate([rot, -rot], axis=1), axis=1)
+    return out
+

@@ -25,7 +25,7 @@ LIB_PATH = os.environ.get("SCFA_LIB") or os.path.join(_HERE, "lib", "libscfa_b20
 
 OK = 0
 ERR_SHAPE, ERR_FORMAT, ERR_PARAM, ERR_NUMERIC, ERR_CONTRACT, ERR_CUDA = 1, 2, 3, 4, 5, 6
-DT_F32, DT_F64, DT_U8, DT_I32, DT_I64 = 0, 1, 2, 3, 4
+DT_F32, DT_F64, DT_U8, DT_I32, DT_I64, DT_BF16 = 0, 1, 2, 3, 4, 5
 FLAG_EXCLUDE_SELF, FLAG_HASH = 1, 2
 
 _ERRORS = {
@@ -57,6 +57,7 @@ _SIGS = {
     "scfa_build_schedule": [_P, _P, _P, _P, _L, _L, _L, _L, _L, _I, _P, _P, _I, _P, _P, _L, _P, _P, _L, _P, _P,
                             _L, _P, _P],
     "scfa_ref_schedule": [_P, _P, _P, _P, _L, _L, _L, _L, _L, _L, _L, _I, _P, _P, _P, _P],
+    "scfa_lsh_buckets": [_P, _I, _L, _L, _L, _L, _L, _L, _L, _L, _P, _I, _P, _L, _L, _L, _P],
     "scfa_attn_fwd": [_P, _P, _P, _L, _L, _L, _L, _P, _P, _L, _L, _P, _P, _L, _F, _L, _L, _I, _P, _P, _P, _P,
                       _P, _P, _L, _L, _P],
     "scfa_bwd_prep": [_P, _P, _P, _P, _P, _L, _L, _L, _L, _P, _L, _L, _P, _P, _P, _P],

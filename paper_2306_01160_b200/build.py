@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "lib")
 LIB_PATH = os.path.join(LIB_DIR, "libscfa_b200.so")
-SOURCES = ["scfa_attn.cu", "scfa_prep.cu", "scfa_sched.cu", "scfa_capi.cu"]
+SOURCES = ["scfa_attn.cu", "scfa_prep.cu", "scfa_sched.cu", "scfa_capi.cu", "scfa_lsh.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

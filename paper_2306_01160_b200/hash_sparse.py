@@ -63,19 +63,29 @@ def random_buckets(B, T, H, nb, seed):
 def lsh_buckets(x, nb, seed):
     """Angular LSH codes for (B, T, H, D) vectors (hash_sparse.py:34-52).
 
-    The projections are drawn from the reference's Philox streams on the host
-    so ids agree with the reference; the projection + argmax runs on the GPU.
+    The projections are drawn from the reference's Philox streams on the host (one
+    D x nb/2 standard-normal matrix per (b, h), tensors.py:86-93), so ids agree with
+    the reference; the projection and the argmax of [xR, -xR] run on the GPU in float64
+    (scfa_lsh_buckets).  Returns int64 (B, T, H) on the device.
     """
     if nb < 2 or nb % 2 != 0:
         raise ParameterError(f"number of buckets must be even and >= 2, got {nb}")
     x = torch.as_tensor(x)
+    if x.dim() != 4:
+        raise ShapeError("lsh_buckets expects (B, T, H, D) vectors")
     B, T, H, D = x.shape
     dev = x.device if x.is_cuda else torch.device("cuda")
+    if x.dtype not in (torch.float32, torch.float64, torch.bfloat16):
+        x = x.to(torch.float64)
+    x = x.to(dev)
     R = np.stack([stream(seed, DOMAIN_PROJECTIONS, b * H + h).standard_normal((D, nb // 2))
-                  for b in range(B) for h in range(H)]).reshape(B, H, D, nb // 2)
-    R = torch.from_numpy(R).to(dev)
-    rot = torch.einsum("bthd,bhdn->bthn", x.to(dev, torch.float64), R)
-    return torch.cat([rot, -rot], dim=-1).argmax(dim=-1)
+                  for b in range(B) for h in range(H)]) if B * H else np.zeros((0, D, nb // 2))
+    R = torch.from_numpy(np.ascontiguousarray(R, dtype=np.float64)).to(dev)
+    out = torch.empty((B, T, H), dtype=torch.int64, device=dev)
+    dt = _lib.DT_BF16 if x.dtype == torch.bfloat16 else _lib.dtype_code(x)
+    _lib.call("scfa_lsh_buckets", _lib.ptr(x), dt, B, T, H, D, *x.stride(), _lib.ptr(R), nb, _lib.ptr(out),
+              *out.stride(), _lib.stream_ptr(dev))
+    return out
 
 
 def normalize_keys(q):

@@ -44,8 +44,21 @@ class LMConfig:
 def lsh_bucket_ids(k, R):
     """Bucket ids (B, T, H) int64 of keys k (B, T, H, D) under projections R (H, D, nb/2).
 
-    argmax of [kR, -kR] with first-max ties (np.argmax order, hash_sparse.py:47-51).
+    argmax of [kR, -kR] with first-max ties (np.argmax order, hash_sparse.py:47-51).  On
+    the GPU this is the scfa_lsh_buckets kernel (float64, R shared by the batch); the
+    torch expression serves the CPU host-logic tests.
     """
+    if k.is_cuda:
+        from . import _lib
+
+        B, T, H, D = k.shape
+        Rb = R.to(torch.float64).unsqueeze(0).expand(B, *R.shape).contiguous()
+        out = torch.empty((B, T, H), dtype=torch.int64, device=k.device)
+        dt = _lib.DT_BF16 if k.dtype == torch.bfloat16 else _lib.dtype_code(k)
+        kk = k if k.dtype in (torch.bfloat16, torch.float32, torch.float64) else k.float()
+        _lib.call("scfa_lsh_buckets", _lib.ptr(kk), dt, B, T, H, D, *kk.stride(), _lib.ptr(Rb), 2 * R.shape[-1],
+                  _lib.ptr(out), *out.stride(), _lib.stream_ptr(k.device))
+        return out
     with torch.autocast(k.device.type, enabled=False):
         rot = torch.einsum("bthd,hdn->bthn", k.float(), R)
     return torch.cat([rot, -rot], dim=-1).argmax(dim=-1)

@@ -18,6 +18,8 @@ reference's public functions in float64:
          (:145-179) -> hash_scatter (:216-220); backward via
          hash_backward_kernel (:182-213) on dO sorted by q_idx.
   dense: flash_forward / flash_backward (dense.py:33-93).
+  lsh:   lsh_buckets (hash_sparse.py:34-52) at several bucket counts (lsh_small.npz;
+         `--lsh-only` regenerates just that file).
 
 Stored per case (one .npz): the integer provenance (compaction indices,
 counts, sorted positions / buckets, reference schedules at BlockSpec(64,64)),
@@ -188,11 +190,30 @@ CASES = [
 ]
 
 
+def lsh_case():
+    """lsh_buckets (hash_sparse.py:34-52) of the reference on float32 boundary-layout
+    vectors, several bucket counts (incl. nb/2 not a power of two)."""
+    from scfa.hash_sparse import lsh_buckets
+
+    rng = np.random.default_rng(300)
+    x = rng.standard_normal((2, 200, 3, 32)).astype(np.float32)
+    x[0, :4] = 0.0  # zero vectors: every projection ties at 0 -> id 0
+    arrays = {"x": x}
+    for nb in (2, 6, 16, 64):
+        arrays[f"ids_nb{nb}"] = lsh_buckets(x, nb, 31)
+    return arrays, {"seed": 31, "nbs": [2, 6, 16, 64]}
+
+
 def main():
     try:
         import scfa  # noqa: F401
     except ImportError:
         sys.exit("run with PYTHONPATH=/root/reference/pkg/src (the reference package)")
+    if "--lsh-only" in sys.argv:
+        arrays, meta = lsh_case()
+        np.savez_compressed(os.path.join(HERE, "lsh_small.npz"), **arrays)
+        print("lsh_small", meta)
+        return
     index = {}
     for name, fn, kw, fdt in CASES:
         arrays, meta = fn(name, **kw)
@@ -204,6 +225,9 @@ def main():
         print(name, meta)
     with open(os.path.join(HERE, "cases.json"), "w") as f:
         json.dump(index, f, indent=1, sort_keys=True)
+    arrays, meta = lsh_case()
+    np.savez_compressed(os.path.join(HERE, "lsh_small.npz"), **arrays)
+    print("lsh_small", meta)
 
 
 if __name__ == "__main__":
