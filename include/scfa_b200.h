@@ -250,6 +250,14 @@ int scfa_bwd_prep(const void* o, const void* d_out, const float* lse2_in, const 
                   const int32_t* q_idx, int64_t H, int64_t T_out, void* d_out_sorted, float* delta,
                   float* lse2_out, void* stream);
 
+/* The same delta pass for shared hash ids (every position has a slot) driven from the
+ * source side: o and d_out are (B, T, H, D) bf16 read in memory order; rank (B*H, T)
+ * int32 position -> slot (scfa_hash_prepare); dO row (b, t, h) is written to slot
+ * rank[bh, t] of d_out_sorted (B*H, T, D) and delta[bh, rank[bh, t]] = rowsum(dO * O)
+ * (qk_sparse.py:168, hash_sparse.py:194); delta (B*H, Tq_pad) slots >= T are set to 0. */
+int scfa_bwd_prep_rank(const void* o, const void* d_out, int64_t B, int64_t T, int64_t H, int64_t D,
+                       int64_t Tq_pad, const int32_t* rank, void* d_out_sorted, float* delta, void* stream);
+
 /* Backward pass 1 (dQ, query-block owner, _kernel.py:173-179).  q_runs, list_dq,
  * count_dq from scfa_build_schedule.  dq (B*H, T_q, D) f32, or (B, T_out, H, D)
  * scattered by q_idx when out_boundary (as scfa_attn_fwd), or the rows q_rows of a

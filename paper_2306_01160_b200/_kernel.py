@@ -280,7 +280,7 @@ def attention_forward(problem, q, k, v, scale=None, blocks=None, boundary=None, 
     return out
 
 
-def attention_backward(problem, q, k, v, outputs, d_out, scale=None, boundary=None, rows=None):
+def attention_backward(problem, q, k, v, outputs, d_out, scale=None, boundary=None, rows=None, q_rank=None):
     """dQ, dK, dV (fp32) recomputing P from the saved statistics.
 
     boundary=None: d_out and outputs.O are engine layout in kernel order and the
@@ -325,6 +325,12 @@ def attention_backward(problem, q, k, v, outputs, d_out, scale=None, boundary=No
     if lse_in is not None and (rows is not None or boundary is None):
         lse2 = lse_in  # from our forward; delta is fused into the dQ kernel
         fuse = True
+    elif lse_in is not None and q_rank is not None and T_q == Tq_out:
+        # shared hash ids (every position has a slot): the delta pass reads O / dO in
+        # memory order and writes dO / delta at each position's slot
+        lse2, fuse = lse_in, False
+        _lib.call("scfa_bwd_prep_rank", _lib.ptr(O), _lib.ptr(d_out), B, T_q, H, D, Tq_pad, _lib.ptr(q_rank),
+                  _lib.ptr(d_sorted), _lib.ptr(delta), _lib.stream_ptr())
     else:
         fuse = False
         lse2 = torch.empty((BH, Tq_pad), dtype=torch.float32, device=dev)

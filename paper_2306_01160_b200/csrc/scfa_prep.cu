@@ -977,6 +977,63 @@ extern "C" int scfa_validate_sorted(const int32_t* idx, const int32_t* hash, int
   return check_launch("validate_sorted");
 }
 
+// The boundary-layout delta pass driven from the source side (shared hash ids: every
+// position has a slot): O and dO rows are read in memory order (b, t, h) — fully
+// sequential — and dO lands at its slot rank[bh, t] of d_out_sorted, delta at
+// delta[bh, rank].  Slots past T (padding to Tq_pad) get delta 0.
+__global__ void bwd_prep_rank_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ d_out,
+                                     int64_t H, int64_t T, int64_t D, int64_t Tq_pad,
+                                     const int32_t* __restrict__ rank, __nv_bfloat16* __restrict__ d_out_sorted,
+                                     float* __restrict__ delta, int64_t rows, int64_t BH) {
+  const int tpr = static_cast<int>(D / 8);
+  const int64_t g = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t main_threads = rows * tpr;
+  if (g >= main_threads) {  // padding slots
+    const int64_t p = g - main_threads, npad = Tq_pad - T;
+    if (npad > 0 && p < BH * npad) {
+      const int64_t bh = p / npad;
+      delta[bh * Tq_pad + T + (p - bh * npad)] = 0.f;
+    }
+    return;
+  }
+  const int64_t r = g / tpr;  // (b, t, h) row, h fastest
+  const int part = static_cast<int>(g - r * tpr);
+  const int64_t h = r % H, bt = r / H;
+  const int64_t t = bt % T, b = bt / T;
+  const int64_t bh = b * H + h;
+  const int32_t slot = __ldg(rank + bh * T + t);
+  const uint4 a = __ldg(reinterpret_cast<const uint4*>(o + r * D) + part);
+  const uint4 c = __ldg(reinterpret_cast<const uint4*>(d_out + r * D) + part);
+  *reinterpret_cast<uint4*>(d_out_sorted + (bh * T + slot) * D + part * 8) = c;
+  const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+  const __nv_bfloat162* c2 = reinterpret_cast<const __nv_bfloat162*>(&c);
+  float acc = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 x = __bfloat1622float2(a2[i]);
+    const float2 y = __bfloat1622float2(c2[i]);
+    acc = fmaf(x.x, y.x, acc);
+    acc = fmaf(x.y, y.y, acc);
+  }
+  // rows never straddle warps (tpr is a power of two <= 32, main_threads a multiple of tpr)
+  for (int w = tpr >> 1; w > 0; w >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, w);
+  if (part == 0) delta[bh * Tq_pad + slot] = acc;
+}
+
+extern "C" int scfa_bwd_prep_rank(const void* o, const void* d_out, int64_t B, int64_t T, int64_t H, int64_t D,
+                                  int64_t Tq_pad, const int32_t* rank, void* d_out_sorted, float* delta,
+                                  void* stream) {
+  if (D % 8 != 0 || D / 8 > 32 || ((D / 8) & (D / 8 - 1))) { set_error("bwd_prep_rank: unsupported D"); return SCFA_ERR_SHAPE; }
+  if (Tq_pad < T) { set_error("bwd_prep_rank: Tq_pad < T"); return SCFA_ERR_SHAPE; }
+  const int64_t rows = B * T * H;
+  const int64_t threads = rows * (D / 8) + B * H * (Tq_pad - T);
+  if (threads == 0) return SCFA_OK;
+  bwd_prep_rank_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(d_out), H, T, D, Tq_pad, rank,
+      static_cast<__nv_bfloat16*>(d_out_sorted), delta, rows, B * H);
+  return check_launch("bwd_prep_rank");
+}
+
 extern "C" int scfa_bwd_prep(const void* o, const void* d_out, const float* lse2_in, const float* m, const float* l,
                              int64_t BH, int64_t T_q, int64_t D, int64_t Tq_pad, const int32_t* q_idx, int64_t H,
                              int64_t T_out, void* d_out_sorted, float* delta, float* lse2_out, void* stream) {

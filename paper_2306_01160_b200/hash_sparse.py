@@ -189,6 +189,22 @@ def _gather3(xs, perms, layout):
     return outs
 
 
+def _permute3(xs, ranks, T_perm):
+    """As _gather3 for boundary-layout ('bthd') tensors, driven from the source side:
+    rows are read in memory order and each is written to its slot rank[bh, t]
+    (scfa_permute_rows3; measured ~10% faster than the gather at cfg2, random-row
+    writes instead of random-row reads)."""
+    outs, strides = [], []
+    for x in xs:
+        B, T, H, D = x.shape
+        strides += [x.stride(0), x.stride(1), x.stride(2)]
+        outs.append(torch.empty((B, H, T_perm, D), dtype=x.dtype, device=x.device))
+    _lib.call("scfa_permute_rows3", len(xs), _lib.ptr_array(xs), _lib.ptr_array(outs), _lib.ptr_array(ranks),
+              _lib.i64_array(strides), xs[0].element_size(), B, T, H, D, _lib.i64_array([T_perm] * len(xs)),
+              _lib.stream_ptr())
+    return outs
+
+
 _PREP_MAX_T = 16384
 
 
@@ -390,14 +406,18 @@ def _fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, exclude_self=True, row_
         side = _copy_streams(q.device)[2]
         side.wait_stream(main)
         with torch.cuda.stream(side):
-            xq, xk, xv = _gather3([q, k, v], [sb.q_perm, sb.k_perm, sb.k_perm], "bthd")
+            if sb.q_rank is not None and sb.k_rank is not None and T_Q == T_KV:
+                xq, xk, xv = _permute3([q, k, v], [sb.q_rank, sb.k_rank, sb.k_rank], T_Q)
+            else:
+                xq, xk, xv = _gather3([q, k, v], [sb.q_perm, sb.k_perm, sb.k_perm], "bthd")
         prob.schedule("fwd", "dq", "dkdv")
         main.wait_stream(side)
         for t in (xq, xk, xv):
             t.record_stream(main)
     outputs = attention_forward(prob, xq, xk, xv, scale, boundary=(T_Q, False), rows=rows)
     dq, dk, dv = attention_backward(prob, xq, xk, xv, outputs, as_operand(d_out), scale,
-                                    boundary=(T_Q, T_KV, False), rows=rows)
+                                    boundary=(T_Q, T_KV, False), rows=rows,
+                                    q_rank=sb.q_rank if sb.q_rank is not None and sb.k_rank is sb.q_rank else None)
     return outputs, dq, dk, dv, prob
 
 
