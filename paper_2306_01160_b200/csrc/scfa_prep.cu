@@ -233,7 +233,9 @@ __global__ void __launch_bounds__(kSortThreads) hash_sort_kernel(
 constexpr int kPrepMaxT = 16384;
 
 struct PrepSmem {
-  int cnt[256][32];  // per (digit, warp) counts, then exclusive offsets (digit-major)
+  int cnt[256][33];  // per (digit, warp) counts, then exclusive offsets (digit-major);
+                     // row padded to 33 so a warp's lanes (one warp column, many digits)
+                     // fall in different banks
   int red[33];
   long long mx;
 };
@@ -257,7 +259,7 @@ SCFA_DEVICE void radix_pass(PrepSmem& S, const int32_t* key, int T, int shift, c
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int seg = (((T + 31) / 32) + 31) & ~31;
   const int s0 = warp * seg, s1 = min(T, s0 + seg);
-  for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) (&S.cnt[0][0])[i] = 0;
+  for (int i = threadIdx.x; i < 256 * 33; i += blockDim.x) (&S.cnt[0][0])[i] = 0;
   __syncthreads();
   for (int base = s0; base < s1; base += 32) {
     const int s = base + lane;
@@ -269,10 +271,11 @@ SCFA_DEVICE void radix_pass(PrepSmem& S, const int32_t* key, int T, int shift, c
   __syncthreads();
   {  // exclusive scan of cnt in (digit, warp) order: 8 entries per thread
     int* flat = &S.cnt[0][0];
-    const int i0 = threadIdx.x * 8;
+    const int i0 = threadIdx.x * 8;  // flat (digit, warp) index; entry f lives at (f / 32) * 33 + f % 32
+    const int a0 = (i0 >> 5) * 33 + (i0 & 31);
     int loc[8], sum = 0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) { loc[i] = flat[i0 + i]; sum += loc[i]; }
+    for (int i = 0; i < 8; ++i) { loc[i] = flat[a0 + i]; sum += loc[i]; }
     int incl = sum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -294,7 +297,7 @@ SCFA_DEVICE void radix_pass(PrepSmem& S, const int32_t* key, int T, int shift, c
     __syncthreads();
     int acc = S.red[warp] + incl - sum;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) { flat[i0 + i] = acc; acc += loc[i]; }
+    for (int i = 0; i < 8; ++i) { flat[a0 + i] = acc; acc += loc[i]; }
   }
   __syncthreads();
   for (int base = s0; base < s1; base += 32) {
