@@ -79,7 +79,12 @@ struct Cfg {
   // S [0,64) and dP [64,128), with P / dS (bf16) written over them; accumulators at 256.
   static constexpr int TM_BUF = 128;
   // ALT: S / dP buffers in TMEM (tile t uses buffer t % NBUF, row warpgroup t % 2)
-  static constexpr int NBUF = (ALT && 3 * TM_BUF + ((kMode == MODE_DKDV) ? 2 * kD : kD) <= 512) ? 3 : 2;
+  // dK/dV at D = 64: the stationary K and V also live in TMEM (32 columns each, two
+  // buffers: item i uses buffer i % 2), so the S^T / dP^T MMAs read A from TMEM (TS mode:
+  // 32 instead of 48 clk per N = 64 MMA, scripts/mma_issue.cu) — which leaves room for
+  // two S / dP buffers, not three
+  static constexpr bool KV_TMEM = (kMode == MODE_DKDV && kD == 64);
+  static constexpr int NBUF = KV_TMEM ? 2 : ((ALT && 3 * TM_BUF + ((kMode == MODE_DKDV) ? 2 * kD : kD) <= 512) ? 3 : 2);
   static constexpr int TM_S = 0;
   static constexpr int TM_DP = (kMode == MODE_FWD) ? 0 : BN;
   static constexpr int TM_ACC = ALT ? NBUF * TM_BUF : 128;
@@ -89,6 +94,8 @@ struct Cfg {
   static constexpr int TM_P = OVERLAP ? TM_ACC + ACC_COLS : TM_S;                 // P | dS | P^T
   static constexpr int TM_P2 = OVERLAP ? TM_ACC + ACC_COLS + BN / 2 : TM_DP;      // dS^T (DKDV)
   static_assert(TM_ACC + ACC_COLS <= TM_STREAM, "TMEM budget");
+  static constexpr int TM_KV = TM_ACC + ACC_COLS;  // KV_TMEM buffer b: K [TM_KV + b*kD, +kD/2), V next
+  static_assert(!KV_TMEM || TM_KV + 2 * kD <= TM_STREAM, "TMEM budget (K / V)");
   // shared memory per stream (all TMA destinations 1024-aligned)
   static constexpr int OFF_X = 0;
   static constexpr int OFF_Y0 = OFF_X + NXS * XSLOT_BYTES;
@@ -729,6 +736,18 @@ __global__ void __launch_bounds__(512, 1)
           p_tg = -1;
         }
         mbar_wait_lazy(bar_x_full + xs, (ia / C::NXS) & 1);
+        if (C::KV_TMEM && elect_one()) {
+          // stationary K / V -> TMEM buffer ia % 2 (tcgen05.cp, 128 rows x 16 bf16 per copy);
+          // copies and MMAs execute in issue order, so the S^T / dP^T below see them
+          tc_fence_after();
+          const uint32_t kv = tmem + C::TM_KV + (ia & 1) * kD;
+#pragma unroll
+          for (int k = 0; k < kD / 16; ++k) {
+            tmem_cp_128x256b(kv + k * 8, make_sdesc_sw128(x0_addr + k * 32, 16, 1024));
+            tmem_cp_128x256b(kv + kD / 2 + k * 8, make_sdesc_sw128(x1_addr + k * 32, 16, 1024));
+          }
+        }
+        __syncwarp();
         if (lane == 0) { SCFA_STAMP_AT(tg, 9); }
         for (int t = 0; t < n; ++t, ++tg) {
           const int s0 = tg % C::NS0, s1 = tg % C::NS1;
@@ -757,13 +776,21 @@ __global__ void __launch_bounds__(512, 1)
               const uint32_t koff = (k & 3) * 32;
               const uint32_t a = x0_addr + (k >> 2) * (C::BM * 128) + koff;
               const uint32_t b = y0_addr + (k >> 2) * (C::BN * 128) + koff;
-              umma_ss(tmem + j * C::TM_BUF + C::TM_S, make_sdesc_sw128(a, 16, 1024), make_sdesc_sw128(b, 16, 1024),
-                      idesc_s, k > 0);
-              if (kMode != MODE_FWD) {
-                const uint32_t a1 = x1_addr + (k >> 2) * (C::BM * 128) + koff;
+              if (C::KV_TMEM) {  // A = K / V rows in TMEM (16 bf16 = 8 columns per K step)
+                const uint32_t kv = tmem + C::TM_KV + (ia & 1) * kD;
+                umma_ts(tmem + j * C::TM_BUF + C::TM_S, kv + k * 8, make_sdesc_sw128(b, 16, 1024), idesc_s, k > 0);
                 const uint32_t b1 = y1_addr + (k >> 2) * (C::BN * 128) + koff;
-                umma_ss(tmem + j * C::TM_BUF + C::TM_DP, make_sdesc_sw128(a1, 16, 1024), make_sdesc_sw128(b1, 16, 1024),
+                umma_ts(tmem + j * C::TM_BUF + C::TM_DP, kv + kD / 2 + k * 8, make_sdesc_sw128(b1, 16, 1024), idesc_s,
+                        k > 0);
+              } else {
+                umma_ss(tmem + j * C::TM_BUF + C::TM_S, make_sdesc_sw128(a, 16, 1024), make_sdesc_sw128(b, 16, 1024),
                         idesc_s, k > 0);
+                if (kMode != MODE_FWD) {
+                  const uint32_t a1 = x1_addr + (k >> 2) * (C::BM * 128) + koff;
+                  const uint32_t b1 = y1_addr + (k >> 2) * (C::BN * 128) + koff;
+                  umma_ss(tmem + j * C::TM_BUF + C::TM_DP, make_sdesc_sw128(a1, 16, 1024),
+                          make_sdesc_sw128(b1, 16, 1024), idesc_s, k > 0);
+                }
               }
             }
           umma_commit(bar_s_full + j);

@@ -290,6 +290,13 @@ SCFA_DEVICE void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
       : "memory");
 }
 
+// smem -> TMEM copy of a 128-row x 256-bit block (tcgen05.cp; source described by a
+// matrix descriptor, as an MMA operand), asynchronous, ordered with the issuing
+// thread's tcgen05.mma
+SCFA_DEVICE void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
+
 SCFA_DEVICE void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 SCFA_DEVICE void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
