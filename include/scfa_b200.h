@@ -258,6 +258,15 @@ int scfa_bwd_prep(const void* o, const void* d_out, const float* lse2_in, const 
 int scfa_bwd_prep_rank(const void* o, const void* d_out, int64_t B, int64_t T, int64_t H, int64_t D,
                        int64_t Tq_pad, const int32_t* rank, void* d_out_sorted, float* delta, void* stream);
 
+/* Zero the rows of dropped positions: for every (b, t, h) with keep[b*sb + t*st + h*sh]
+ * == 0 (dtype keep_dtype), the row of out0 (row_bytes0 bytes at row (b*T + t)*H + h) and
+ * of out1 (row_bytes1, may be NULL / 0) are set to 0.  With it the boundary-layout QK
+ * outputs need no full zero-fill: the attention epilogues write every kept row and the
+ * reference leaves dropped rows 0 (qk_postprocess, qk_sparse.py:214-225).              */
+int scfa_zero_dropped(const void* keep, int keep_dtype, int64_t B, int64_t T, int64_t H, int64_t sb,
+                      int64_t st, int64_t sh, void* out0, int64_t row_bytes0, void* out1,
+                      int64_t row_bytes1, void* stream);
+
 /* Backward pass 1 (dQ, query-block owner, _kernel.py:173-179).  q_runs, list_dq,
  * count_dq from scfa_build_schedule.  dq (B*H, T_q, D) f32, or (B, T_out, H, D)
  * scattered by q_idx when out_boundary (as scfa_attn_fwd), or the rows q_rows of a

@@ -1037,6 +1037,60 @@ extern "C" int scfa_bwd_prep_rank(const void* o, const void* d_out, int64_t B, i
   return check_launch("bwd_prep_rank");
 }
 
+// Zero the rows of dropped positions (keep == 0) of up to two (B, T, H, D) outputs:
+// the kernels write every kept row, so the outputs need no full zero-fill
+// (qk_postprocess / the backward scatter leave dropped rows 0, qk_sparse.py:214-225).
+// One warp per (b, t): the H rows of a position are contiguous, so the warp's 16-byte
+// stores walk them in order (coalesced), skipping the kept heads.
+__global__ void zero_dropped_kernel(const void* __restrict__ keep, int kdt, int T, int H, int64_t sb, int64_t st,
+                                    int64_t sh, uint8_t* __restrict__ out0, int row0, uint8_t* __restrict__ out1,
+                                    int row1, int64_t n_bt) {
+  const int64_t bt = blockIdx.x * static_cast<int64_t>(blockDim.x / 32) + (threadIdx.x >> 5);
+  if (bt >= n_bt) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t b = bt / T, t = bt - b * T;
+  const int64_t kbase = b * sb + t * st;
+  uint32_t dropped = 0;  // bit h: head h of this position is dropped (H <= 32 per pass)
+  for (int h0 = 0; h0 < H; h0 += 32) {
+    const int h = h0 + lane;
+    const bool d = h < H && load_num(keep, kdt, kbase + h * sh) == 0.0;
+    dropped = __ballot_sync(0xffffffffu, d);
+    if (!dropped) continue;
+    const int nh = min(32, H - h0);
+#pragma unroll
+    for (int o = 0; o < 2; ++o) {
+      uint8_t* out = o == 0 ? out0 : out1;
+      const int rb = o == 0 ? row0 : row1;
+      if (!out || rb == 0) continue;
+      const int pieces = rb / 16;
+      uint4* base = reinterpret_cast<uint4*>(out + (bt * H + h0) * static_cast<int64_t>(rb));
+      for (int p = lane; p < nh * pieces; p += 32)
+        if ((dropped >> (p / pieces)) & 1u) base[p] = make_uint4(0u, 0u, 0u, 0u);
+    }
+  }
+}
+
+extern "C" int scfa_zero_dropped(const void* keep, int keep_dtype, int64_t B, int64_t T, int64_t H, int64_t sb,
+                                 int64_t st, int64_t sh, void* out0, int64_t row_bytes0, void* out1,
+                                 int64_t row_bytes1, void* stream) {
+  if (row_bytes0 % 16 || row_bytes1 % 16 || (!out1 && row_bytes1)) {
+    set_error("zero_dropped: row bytes must be multiples of 16");
+    return SCFA_ERR_SHAPE;
+  }
+  if (T > 0x7fffffff || H > 0x7fffffff || row_bytes0 > 0x7fffffff || row_bytes1 > 0x7fffffff) {
+    set_error("zero_dropped: sizes out of range");
+    return SCFA_ERR_SHAPE;
+  }
+  const int64_t n_bt = B * T;
+  if (n_bt == 0 || H == 0) return SCFA_OK;
+  constexpr int kWarps = 8;
+  zero_dropped_kernel<<<static_cast<unsigned>((n_bt + kWarps - 1) / kWarps), 32 * kWarps, 0,
+                        static_cast<cudaStream_t>(stream)>>>(
+      keep, keep_dtype, static_cast<int>(T), static_cast<int>(H), sb, st, sh, static_cast<uint8_t*>(out0),
+      static_cast<int>(row_bytes0), static_cast<uint8_t*>(out1), static_cast<int>(row_bytes1), n_bt);
+  return check_launch("zero_dropped");
+}
+
 extern "C" int scfa_bwd_prep(const void* o, const void* d_out, const float* lse2_in, const float* m, const float* l,
                              int64_t BH, int64_t T_q, int64_t D, int64_t Tq_pad, const int32_t* q_idx, int64_t H,
                              int64_t T_out, void* d_out_sorted, float* delta, float* lse2_out, void* stream) {

@@ -273,10 +273,20 @@ def qk_sparse_attention_fwd_bwd(q, k, v, q_keep, k_keep, d_out, scale=None, row_
     prob = prep.problem
     prob.schedule("fwd", "dq", "dkdv")
     rows = prob.rows if row_tables else None
-    outputs = attention_forward(prob, prep.q_c, prep.k_c, prep.v_c, scale, boundary=(T_Q, True), rows=rows)
+    # the kernels write every kept row; only the dropped rows are zeroed (no full fill)
+    outputs = attention_forward(prob, prep.q_c, prep.k_c, prep.v_c, scale, boundary=(T_Q, False), rows=rows)
     dq, dk, dv = attention_backward(prob, prep.q_c, prep.k_c, prep.v_c, outputs, as_operand(d_out), scale,
-                                    boundary=(T_Q, T_KV, True), rows=rows)
+                                    boundary=(T_Q, T_KV, False), rows=rows)
+    _zero_dropped(q_keep, outputs.O, dq)
+    _zero_dropped(k_keep, dk, dv)
     return outputs.O, dq, dk, dv
+
+
+def _zero_dropped(keep, out0, out1):
+    B, T, H, D = out0.shape
+    keep = torch.as_tensor(keep, device=out0.device)
+    _lib.call("scfa_zero_dropped", _lib.ptr(keep), _lib.dtype_code(keep), B, T, H, *keep.stride(), _lib.ptr(out0),
+              D * out0.element_size(), _lib.ptr(out1), D * out1.element_size(), _lib.stream_ptr())
 
 
 def random_keep(B, T, H, drop_prob, seed):
