@@ -298,11 +298,12 @@ extern "C" int scfa_build_schedule(const int32_t* q_idx, const int32_t* q_hash, 
     set_error("schedule: padded vectors shorter than the block grid (or too many slices)");
     return SCFA_ERR_SHAPE;
   }
-  if ((list_fwd || list_dq) && q_runs == nullptr) {
+  // (no rows, no runs: an empty side of the problem — e.g. every query dropped — needs none)
+  if ((list_fwd || list_dq) && q_runs == nullptr && T_q > 0) {
     set_error("schedule: query-row lists need q_runs");
     return SCFA_ERR_PARAM;
   }
-  if (list_dkdv && k_runs == nullptr) {
+  if (list_dkdv && k_runs == nullptr && T_kv > 0) {
     set_error("schedule: key-row lists need k_runs");
     return SCFA_ERR_PARAM;
   }
