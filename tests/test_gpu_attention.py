@@ -136,3 +136,57 @@ def test_autograd_matches_fused_fwd_bwd(mode):
     assert torch.equal(o.detach().to(torch.bfloat16), o2)
     for name, a, b in (("dQ", q.grad, gq), ("dK", k.grad, gk), ("dV", v.grad, gv)):
         assert torch.equal(a, b), name
+
+
+def _hash_oracle(qb, kb, vb, dO, hq, hk, excl):
+    eng = lambda x: np.swapaxes(x, 1, 2)
+    T_Q, T_KV = qb.shape[1], kb.shape[1]
+    vis = orc.visibility(np.arange(T_Q), np.arange(T_KV), hq.transpose(0, 2, 1), hk.transpose(0, 2, 1),
+                         exclude_self=excl)
+    O, _, _ = orc.attention(eng(qb), eng(kb), eng(vb), vis)
+    dq, dk, dv = orc.attention_grads(eng(qb), eng(kb), eng(vb), vis, eng(dO))
+    return [eng(x) for x in (O, dq, dk, dv)]
+
+
+@pytest.mark.parametrize("T", [1, 2, 127, 129])
+@pytest.mark.parametrize("excl", [True, False])
+def test_hash_fwd_bwd_tiny_and_ragged_lengths(T, excl):
+    B, H, D = 2, 3, 64
+    qb, kb, vb = (np.swapaxes(x, 1, 2) for x in make_batch(B, H, T, D, seed=51))
+    dO = bf16_round(np.random.default_rng(52).standard_normal((B, T, H, D)))
+    hb = scfa.random_buckets(B, T, H, 3, 53)
+    want = _hash_oracle(qb, kb, vb, dO, hb, hb, excl)
+    got = scfa.hash_sparse_attention_fwd_bwd(_t(qb), _t(kb), _t(vb), _t(hb), _t(hb), _t(dO), exclude_self=excl)
+    for name, g, w in zip(("O", "dQ", "dK", "dV"), got, want):
+        _check(name, _np(g), w)
+
+
+def test_hash_fwd_bwd_distinct_query_and_key_ids():
+    """Separate query / key bucket ids (the general sort path, not the shared fast path)."""
+    B, H, T, D = 1, 2, 300, 64
+    qb, kb, vb = (np.swapaxes(x, 1, 2) for x in make_batch(B, H, T, D, seed=54))
+    dO = bf16_round(np.random.default_rng(55).standard_normal((B, T, H, D)))
+    hq = scfa.random_buckets(B, T, H, 4, 56)
+    hk = scfa.random_buckets(B, T, H, 4, 57)
+    want = _hash_oracle(qb, kb, vb, dO, hq, hk, False)
+    got = scfa.hash_sparse_attention_fwd_bwd(_t(qb), _t(kb), _t(vb), _t(hq), _t(hk), _t(dO), exclude_self=False)
+    for name, g, w in zip(("O", "dQ", "dK", "dV"), got, want):
+        _check(name, _np(g), w)
+
+
+@pytest.mark.parametrize("T", [1, 2, 129])
+def test_qk_fwd_bwd_tiny_and_ragged_lengths(T):
+    B, H, D = 2, 2, 64
+    qb, kb, vb = (np.swapaxes(x, 1, 2) for x in make_batch(B, H, T, D, seed=58))
+    dO = bf16_round(np.random.default_rng(59).standard_normal((B, T, H, D)))
+    qk = scfa.random_keep(B, T, H, 0.4, 60)
+    kk = scfa.random_keep(B, T, H, 0.4, 61)
+    eng = lambda x: np.swapaxes(x, 1, 2)
+    pos = np.arange(T)
+    vis = orc.visibility(pos, pos) & (qk.transpose(0, 2, 1)[..., :, None] > 0) & (kk.transpose(0, 2, 1)[..., None, :] > 0)
+    O, _, _ = orc.attention(eng(qb), eng(kb), eng(vb), vis)
+    dq, dk, dv = orc.attention_grads(eng(qb), eng(kb), eng(vb), vis, eng(dO))
+    # dropped queries: zero output / gradient; dropped keys: zero dK / dV
+    got = scfa.qk_sparse_attention_fwd_bwd(_t(qb), _t(kb), _t(vb), qk, kk, _t(dO))
+    for name, g, w in zip(("O", "dQ", "dK", "dV"), got, (O, dq, dk, dv)):
+        _check(name, _np(g), eng(w))
