@@ -16,28 +16,33 @@
 // (its bucket run cut at the causal boundary), precomputed per row, so the mask
 // costs two subtractions per tile.
 //
-// Roles (192 threads):
-//   warps 0-3  : one thread per stationary row == TMEM lane.  Online softmax (fwd)
-//                or P / dS recompute (bwd) with packed fp32x2 math, and the epilogue.
-//   warp 4     : TMA producer warp: stationary tiles, the y0 ring (K | K | Q with the
-//                per-column lse/delta of dK/dV) and the y1 ring (V | V | dO).  In
-//                gather mode every lane owns 4 rows of a tile and issues tile::gather4
-//                loads straight from the caller's (B, T, H, D) tensors (row tables), so
-//                no sorted / compacted copy of Q, K, V, dO is ever materialised.
-//   warp 5     : TMEM allocator + single-thread tcgen05.mma issuer.
+// One persistent CTA per SM (148 x 512 threads), items (slice, 128-row block) handed
+// out dynamically through an atomic counter and published in a shared-memory ring one
+// item ahead.  Roles (warpgroups):
+//   WG0, WG1  : row threads, one per stationary row == TMEM lane: online softmax (fwd)
+//               or P / dS recompute (bwd) with packed fp32x2 math.  FWD and dQ run two
+//               independent item streams per CTA (WG0 / WG1, each with its own producer,
+//               MMA issuer, smem slots and 256 TMEM columns); dK/dV runs one stream whose
+//               tiles alternate between WG0 and WG1 ("ALT") over two S / dP buffers.
+//   WG2       : epilogue: reads finished accumulators out of TMEM, releases them
+//               (o_free), stages the rows in the item's stationary slot and copies them
+//               out so each warp store covers whole rows, each row going straight to its
+//               original position (the inverse scatter fused in).
+//   WG3       : warps 12 / 14 TMA producers (tiled 128-B-swizzle boxes, or tile::gather4
+//               from the caller's (B, T, H, D) tensors through row tables), warps 13 / 15
+//               warp-uniform MMA issuers (one elected lane issues tcgen05.mma / .cp /
+//               .commit).  setmaxnreg gives the row warpgroups the register file.
 //
-// Epilogues stage the output rows in the item's (now idle) stationary slot and copy
-// them out so that each warp store covers whole rows, each row going straight to its
-// original position (the inverse scatter fused in).
-//
-// TMEM per CTA (256 columns at D = 64, two CTAs per SM; 512 at D = 128):
+// TMEM (512 columns per CTA; per stream at D = 64 with two streams):
 //   FWD   S fp32 [0,128)  O [128,128+D)  P bf16 [128+D, 192+D)
 //   DQ    S [0,64)  dP [64,128)  dQ [128,128+D)  dS bf16 [128+D, 160+D)
-//   DKDV  S^T [0,64)  dP^T [64,128)  dV [128,128+D)  dK [128+D,128+2D)
-//         P^T / dS^T bf16: own columns at D = 128, aliased onto S^T / dP^T at D = 64.
+//   DKDV  buffers j = 0, 1 at 128 j: S^T [0,64) dP^T [64,128) with P^T / dS^T bf16 written
+//         over them; dV, dK accumulators at 256; at D = 64 the stationary K / V rows
+//         (tcgen05.cp) at 384 in two buffers, read by the S^T / dP^T MMAs (TS mode).
 // With P (dS) in its own columns the S buffer is free as soon as the row threads
 // have loaded it, so the MMA warp issues the next tile's S while they work on
-// this one ("overlap"); aliased, S(t+1) waits for the accumulate MMAs of tile t.
+// this one ("overlap"); an item's last tile accumulates behind the next item's
+// first S when that item is already staged.
 #include "scfa_common.cuh"
 #include "scfa_internal.h"
 
