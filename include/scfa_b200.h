@@ -90,11 +90,15 @@ int scfa_hash_sort(const void* hash, int hash_dtype, int64_t B, int64_t T, int64
  * perm/rank (B*H, T); scratch (B*H, T + 257); q_idx/k_idx/q_hash/k_hash (B*H, T_pad) with the
  * same sentinels as scfa_build_aux; q_runs/k_runs (B*H, T_pad) int32 pairs as
  * scfa_build_schedule (pass runs_ready = 3 there); rows (optional, B*H x T_pad) the
- * scfa_row_map table of the sorted order for gather-mode attention.          */
+ * scfa_row_map table of the sorted order for gather-mode attention.
+ * sorted_event (optional cudaEvent_t) is recorded on `stream` as soon as perm and rank
+ * are final (between the sort and the finishing launch), so a caller can start the
+ * bucket-order row copies on another stream under the rest of the preparation.  */
 int scfa_hash_prepare(const void* hash, int hash_dtype, int64_t B, int64_t T, int64_t H, int64_t sb,
                       int64_t st, int64_t sh, int flags, int32_t* perm, int32_t* rank, int32_t* scratch,
                       int32_t* q_idx, int32_t* k_idx, int32_t* q_hash, int32_t* k_hash, int32_t* q_runs,
-                      int32_t* k_runs, int32_t* rows, int32_t* err_flag, void* stream);
+                      int32_t* k_runs, int32_t* rows, int32_t* err_flag, void* sorted_event,
+                      void* stream);
 
 /* Row tables for the gather-mode attention kernels: rows[bh, s] = (b * T_src + perm[bh, s])
  * * H + h, the row of slot s of slice bh = (b, h) in a (B, T_src, H, D) tensor viewed as

@@ -45,7 +45,7 @@ _SIGS = {
     "scfa_gather_rows": [_P, _I, _L, _L, _L, _L, _L, _L, _P, _L, _L, _P, _P],
     "scfa_gather_rows3": [_I, _P, _P, _P, _P, _I, _L, _L, _L, _P, _P, _P],
     "scfa_permute_rows3": [_I, _P, _P, _P, _P, _I, _L, _L, _L, _L, _P, _P],
-    "scfa_hash_prepare": [_P, _I, _L, _L, _L, _L, _L, _L, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "scfa_hash_prepare": [_P, _I, _L, _L, _L, _L, _L, _L, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "scfa_row_map": [_P, _L, _L, _L, _L, _L, _L, _P, _P],
     "scfa_scatter_rows": [_P, _I, _L, _L, _L, _L, _P, _L, _P, _I, _L, _L, _L, _P],
     "scfa_build_aux": [_P, _P, _L, _L, _L, _L, _L, ctypes.c_int32, ctypes.c_int32, _P, _I, _L, _L, _L,

@@ -255,7 +255,7 @@ SCFA_DEVICE int lower_bound_s(const int32_t* a, int n, int x) {
 //          earlier warps + this warp's running count + rank among equal lanes,
 // which is exactly argsort(kind="stable").  Two walks, three __syncthreads.
 SCFA_DEVICE void radix_pass(PrepSmem& S, const int32_t* key, int T, int shift, const int32_t* src, int32_t* dst,
-                           int32_t* sorted_key) {
+                           int32_t* sorted_key, int32_t* rank = nullptr) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int seg = (((T + 31) / 32) + 31) & ~31;
   const int s0 = warp * seg, s1 = min(T, s0 + seg);
@@ -313,6 +313,7 @@ SCFA_DEVICE void radix_pass(PrepSmem& S, const int32_t* key, int T, int shift, c
     if (act) {
       dst[off + below] = val;
       if (sorted_key) sorted_key[off + below] = key[val];
+      if (rank) rank[val] = off + below;
       if (below == 0) S.cnt[d][warp] = off + __popc(peers);
     }
     __syncwarp();
@@ -327,7 +328,7 @@ SCFA_DEVICE void radix_pass(PrepSmem& S, const int32_t* key, int T, int shift, c
 // flags a multi-pass sort (the finishing kernel then searches the sorted ids).
 __global__ void __launch_bounds__(kSortThreads) hash_prepare_sort_kernel(
     const void* hash, int hdt, int T, int T_pad, int64_t H, int64_t sb, int64_t st, int64_t sh, int32_t* perm,
-    int32_t* scratch, int32_t* sorted_hash, int32_t* err) {
+    int32_t* rank, int32_t* scratch, int32_t* sorted_hash, int32_t* err) {
   extern __shared__ __align__(16) uint8_t dsm[];
   PrepSmem& S = *reinterpret_cast<PrepSmem*>(dsm);
   int32_t* key = reinterpret_cast<int32_t*>(dsm + sizeof(PrepSmem));
@@ -367,14 +368,15 @@ __global__ void __launch_bounds__(kSortThreads) hash_prepare_sort_kernel(
   int32_t* bounds = X + T;
   int32_t* SH = sorted_hash + bh * T_pad;
   if (passes == 0) {
-    for (int s = threadIdx.x; s < T; s += blockDim.x) { P[s] = s; SH[s] = 0; }
+    for (int s = threadIdx.x; s < T; s += blockDim.x) { P[s] = s; SH[s] = 0; rank[bh * T + s] = s; }
     if (threadIdx.x <= 256) bounds[threadIdx.x] = (threadIdx.x == 0) ? 0 : T;
     return;
   }
   for (int p = 0; p < passes; ++p) {  // the final pass lands in perm; pass 0 reads the identity
     const bool last = p == passes - 1;
     const bool to_perm = ((passes - 1 - p) & 1) == 0;
-    radix_pass(S, key, T, 8 * p, p == 0 ? nullptr : (to_perm ? X : P), to_perm ? P : X, last ? SH : nullptr);
+    radix_pass(S, key, T, 8 * p, p == 0 ? nullptr : (to_perm ? X : P), to_perm ? P : X, last ? SH : nullptr,
+               last ? rank + bh * T : nullptr);
   }
   // radix_pass leaves each digit's end offset in S.cnt[d][31] (after the last walk)
   if (threadIdx.x < 256) {
@@ -423,7 +425,6 @@ __global__ void __launch_bounds__(256) hash_prepare_finish_kernel(int T, int T_p
     while (n > 0) { const int hh = n >> 1; if (sh[lo + hh] <= g) { lo += hh + 1; n -= hh + 1; } else n = hh; }
     e = lo;
   }
-  rank[bh * T + t] = s;
   q_idx[o] = t;
   k_idx[o] = t;
   k_hash[o] = g;
@@ -802,7 +803,8 @@ extern "C" int scfa_hash_sort(const void* hash, int hash_dtype, int64_t B, int64
 extern "C" int scfa_hash_prepare(const void* hash, int hash_dtype, int64_t B, int64_t T, int64_t H, int64_t sb,
                                  int64_t st, int64_t sh, int flags, int32_t* perm, int32_t* rank, int32_t* scratch,
                                  int32_t* q_idx, int32_t* k_idx, int32_t* q_hash, int32_t* k_hash, int32_t* q_runs,
-                                 int32_t* k_runs, int32_t* rows, int32_t* err_flag, void* stream) {
+                                 int32_t* k_runs, int32_t* rows, int32_t* err_flag, void* sorted_event,
+                                 void* stream) {
   if (T > kPrepMaxT) { set_error("hash_prepare: T > %d (use scfa_hash_sort)", kPrepMaxT); return SCFA_ERR_SHAPE; }
   if (B * H == 0 || T == 0) return SCFA_OK;
   if (B * H > 65535) { set_error("hash_prepare: too many (b, h) slices"); return SCFA_ERR_SHAPE; }
@@ -817,9 +819,13 @@ extern "C" int scfa_hash_prepare(const void* hash, int hash_dtype, int64_t B, in
     attr = true;
   }
   hash_prepare_sort_kernel<<<static_cast<unsigned>(B * H), kSortThreads, smem, s>>>(
-      hash, hash_dtype, static_cast<int>(T), T_pad, H, sb, st, sh, perm, scratch, q_hash, err_flag);
+      hash, hash_dtype, static_cast<int>(T), T_pad, H, sb, st, sh, perm, rank, scratch, q_hash, err_flag);
   int rc = check_launch("hash_prepare_sort");
   if (rc) return rc;
+  if (sorted_event) {  // perm / rank are final here: the caller may start the row copies
+    if (cudaEventRecord(static_cast<cudaEvent_t>(sorted_event), s) != cudaSuccess)
+      return check_launch("hash_prepare event");
+  }
   dim3 grid(static_cast<unsigned>((T_pad + 255) / 256), static_cast<unsigned>(B * H));
   hash_prepare_finish_kernel<<<grid, 256, 0, s>>>(static_cast<int>(T), T_pad, (flags & SCFA_FLAG_EXCLUDE_SELF) ? 1 : 0,
                                                   perm, scratch, rank, q_idx, k_idx, q_hash, k_hash,

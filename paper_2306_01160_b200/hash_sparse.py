@@ -7,6 +7,7 @@ a permutation that drives a fused gather+transpose of Q/K/V, the exact tile
 lists and the tcgen05 kernels; the inverse permutation routes outputs back.
 """
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -208,7 +209,16 @@ def _permute3(xs, ranks, T_perm):
 _PREP_MAX_T = 16384
 
 
-def _prepare_shared(hash_t, sb, st, sh, B, H, T, D, err, exclude_self):
+def _event_ptr(ev):
+    """The cudaEvent_t of a torch.cuda.Event (created by a first record if needed)."""
+    if ev is None:
+        return None
+    if not ev.cuda_event:
+        ev.record()
+    return ctypes.c_void_p(ev.cuda_event)
+
+
+def _prepare_shared(hash_t, sb, st, sh, B, H, T, D, err, exclude_self, sorted_event=None):
     """Fused sort + sorted vectors + visibility runs for shared bucket ids (scfa_hash_prepare)."""
     dev = hash_t.device
     BH, T_pad = B * H, pad128(T)
@@ -221,7 +231,7 @@ def _prepare_shared(hash_t, sb, st, sh, B, H, T, D, err, exclude_self):
     _lib.call("scfa_hash_prepare", _lib.ptr(hash_t), _lib.dtype_code(hash_t), B, T, H, sb, st, sh, flags,
               _lib.ptr(perm), _lib.ptr(rank), _lib.ptr(scratch), _lib.ptr(vec[0]), _lib.ptr(vec[1]),
               _lib.ptr(vec[2]), _lib.ptr(vec[3]), _lib.ptr(runs[0]), _lib.ptr(runs[1]), _lib.ptr(vec[4]),
-              _lib.ptr(err), _lib.stream_ptr())
+              _lib.ptr(err), _event_ptr(sorted_event), _lib.stream_ptr())
     problem = Problem(B, H, T, T, D, vec[0], vec[1], vec[2], vec[3], flags=flags)
     problem.set_runs(runs[0], runs[1])
     problem.rows = RowTables(vec[4], vec[4], B * T * H, B * T * H)
@@ -229,7 +239,7 @@ def _prepare_shared(hash_t, sb, st, sh, B, H, T, D, err, exclude_self):
 
 
 def _sort_batch(q, k, v, q_hash, k_hash, layout, q_pos=None, k_pos=None, check=True, exclude_self=True,
-                materialize=True):
+                materialize=True, sorted_event=None):
     """Shared by sort_by_bucket (engine layout) and hash_sparse_attention (boundary layout).
 
     materialize=False (boundary layout only): no sorted copies of q / k / v; the
@@ -256,7 +266,7 @@ def _sort_batch(q, k, v, q_hash, k_hash, layout, q_pos=None, k_pos=None, check=T
         kh, ksb, kst, ksh = _hash_view(torch.as_tensor(k_hash, device=dev), B, H, T_KV, hl)
     err = torch.zeros(1, dtype=torch.int32, device=dev)
     if same and 0 < T_Q <= _PREP_MAX_T:
-        q_perm, q_rank, problem = _prepare_shared(qh, qsb, qst, qsh, B, H, T_Q, D, err, exclude_self)
+        q_perm, q_rank, problem = _prepare_shared(qh, qsb, qst, qsh, B, H, T_Q, D, err, exclude_self, sorted_event)
         k_perm, k_rank = q_perm, q_rank
         if check and int(err.item()):
             raise ShapeError("bucket ids must be non-negative (and < 2**31)")
@@ -392,7 +402,9 @@ def _fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, exclude_self=True, row_
     caller's tensors through row tables (no copies at all).
     """
     q, k, v = as_operand(q), as_operand(k), as_operand(v)
-    sb = _sort_batch(q, k, v, q_hash, k_hash, "bthd", check=False, exclude_self=exclude_self, materialize=False)
+    sorted_ev = torch.cuda.Event() if not row_tables else None
+    sb = _sort_batch(q, k, v, q_hash, k_hash, "bthd", check=False, exclude_self=exclude_self, materialize=False,
+                     sorted_event=sorted_ev)
     prob = _problem_of(sb, exclude_self)
     T_Q, T_KV = q.shape[1], k.shape[1]
     rows = prob.rows if row_tables else None
@@ -404,7 +416,10 @@ def _fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, exclude_self=True, row_
         # independent: overlap them
         main = torch.cuda.current_stream(q.device)
         side = _copy_streams(q.device)[2]
-        side.wait_stream(main)
+        if sorted_ev is not None and sorted_ev.cuda_event and sb.k_rank is sb.q_rank:
+            side.wait_event(sorted_ev)  # perm / rank final: copy under the rest of the preparation
+        else:
+            side.wait_stream(main)
         with torch.cuda.stream(side):
             if sb.q_rank is not None and sb.k_rank is not None and T_Q == T_KV:
                 xq, xk, xv = _permute3([q, k, v], [sb.q_rank, sb.k_rank, sb.k_rank], T_Q)
