@@ -235,13 +235,16 @@ int scfa_ref_schedule(const int32_t* q_idx, const int32_t* q_hash, const int32_t
  * caller's (B, T, H, D) tensor, R_q = B*T*H) and slot s of slice bh is row q_rows[bh, s]
  * ((B*H, Tq_pad) int32, from scfa_row_map / scfa_hash_prepare); O is written to the same rows
  * of the [R_q, D] table `o` (this replaces out_boundary).  Likewise k_rows for k / v.  The
- * operands are then loaded with TMA tile::gather4: no compacted / sorted copies exist.  */
+ * operands are then loaded with TMA tile::gather4: no compacted / sorted copies exist.
+ * ABI 4: q_out (optional, needs q_rows) receives the gathered Q rows in kernel order as a
+ * (B*H, T_q, D) bf16 tensor — each stationary tile is stored back with a TMA store once
+ * loaded — so the backward passes can stream a sorted Q without a separate copy pass.  */
 int scfa_attn_fwd(const void* q, const void* k, const void* v, int64_t BH, int64_t T_q,
                   int64_t T_kv, int64_t D, const int32_t* q_idx, const int32_t* q_runs,
                   int64_t Tq_pad, int64_t Tkv_pad, const uint16_t* list, const int32_t* list_count,
                   int64_t list_stride, float scale, int64_t H, int64_t T_out, int out_boundary,
                   void* o, float* m, float* l, float* lse2, const int32_t* q_rows,
-                  const int32_t* k_rows, int64_t R_q, int64_t R_kv, void* stream);
+                  const int32_t* k_rows, int64_t R_q, int64_t R_kv, void* q_out, void* stream);
 
 /* delta = rowsum(dO * O) (qk_sparse.py:168, hash_sparse.py:194, dense.py:81);
  * lse2 rebuilt from (M, L) when lse2_in is NULL (m_hat/inv_l, _kernel.py:152-154).

@@ -237,7 +237,7 @@ class RowTables:
 _NO_ROWS = [None, None, 0, 0]
 
 
-def attention_forward(problem, q, k, v, scale=None, blocks=None, boundary=None, rows=None):
+def attention_forward(problem, q, k, v, scale=None, blocks=None, boundary=None, rows=None, q_out=None):
     """Launch the forward kernel over the exact tile list; returns FlashOutputs.
 
     boundary=None: O is engine layout (B, H, T_q, D) in kernel (sorted/compacted) order.
@@ -245,7 +245,9 @@ def attention_forward(problem, q, k, v, scale=None, blocks=None, boundary=None, 
     position of a (B, T_out, H, D) tensor (fused inverse scatter); positions no row maps
     to are zero-filled first when zero_fill (QK drops).  M, L stay in kernel order.
     rows=RowTables: q, k, v are the caller's (B, T, H, D) tensors, read by TMA gather4
-    through the row tables (no sorted copies); requires boundary.
+    through the row tables (no sorted copies); requires boundary.  With rows.k_rows None
+    the keys / values are kernel-order copies (tiled loads) and only Q is gathered;
+    q_out (B, H, T_q, D) bf16 then receives the gathered Q in kernel order.
     """
     if rows is not None:
         B, T_in, H, D = q.shape
@@ -273,7 +275,7 @@ def attention_forward(problem, q, k, v, scale=None, blocks=None, boundary=None, 
             _lib.ptr(problem.q_idx), _lib.ptr(sched["q_runs"]), problem.Tq_pad, problem.Tkv_pad,
             _lib.ptr(lst), _lib.ptr(cnt), stride, _scale(scale, D), H, T_out, out_b,
             _lib.ptr(O), _lib.ptr(M), _lib.ptr(L), _lib.ptr(lse2),
-            *(rows.args() if rows is not None else _NO_ROWS), _lib.stream_ptr(),
+            *(rows.args() if rows is not None else _NO_ROWS), _lib.ptr(q_out), _lib.stream_ptr(),
         )
     out = FlashOutputs(O, M, L, problem=problem, blocks=blocks, lse2=lse2)
     out._boundary = boundary

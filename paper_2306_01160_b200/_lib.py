@@ -59,7 +59,7 @@ _SIGS = {
     "scfa_ref_schedule": [_P, _P, _P, _P, _L, _L, _L, _L, _L, _L, _L, _I, _P, _P, _P, _P],
     "scfa_lsh_buckets": [_P, _I, _L, _L, _L, _L, _L, _L, _L, _L, _P, _I, _P, _L, _L, _L, _P],
     "scfa_attn_fwd": [_P, _P, _P, _L, _L, _L, _L, _P, _P, _L, _L, _P, _P, _L, _F, _L, _L, _I, _P, _P, _P, _P,
-                      _P, _P, _L, _L, _P],
+                      _P, _P, _L, _L, _P, _P],
     "scfa_zero_dropped": [_P, _I, _L, _L, _L, _L, _L, _L, _P, _L, _P, _L, _P],
     "scfa_bwd_prep_rank": [_P, _P, _L, _L, _L, _L, _L, _P, _P, _P, _P],
     "scfa_bwd_prep": [_P, _P, _P, _P, _P, _L, _L, _L, _L, _P, _L, _L, _P, _P, _P, _P],

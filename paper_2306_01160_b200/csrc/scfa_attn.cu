@@ -143,6 +143,7 @@ struct AttnArgs {
   const float* delta;          // (BH, Tq_pad)
   const int* x_rows;  // gather mode: global row per stationary slot (BH, T_rows_pad); null = tiled loads
   const int* y_rows;  // gather mode: global row per streamed slot (BH, T_cols_pad)
+  int x_writeout;              // FWD: write the gathered stationary tile out through tm_x1 (kernel order)
   const __nv_bfloat16* o_src;  // DQ: O rows (addressed like dO) for the fused delta
   float* delta_out;            // DQ: delta = rowsum(dO * O) per query slot (BH, T_rows_pad)
   const uint16_t* list;
@@ -686,6 +687,10 @@ __global__ void __launch_bounds__(512, 1)
         if (lane == 0) { SCFA_STAMP_AT(ptg, 13); }
         if (first && pia > 0) mbar_wait_lazy(B.o_free, (pia - 1) & 1);  // the epilogue has read the previous item
         tc_fence_after();
+        // the epilogue reuses the stationary slot once acc_full fires: the write-out must
+        // have read it by then
+        if (kMode == MODE_FWD && last && args.x_writeout && lane == 0) bulk_wait_read0();
+        __syncwarp();
         const uint32_t y0_addr = smem_u32(smem + C::OFF_Y0 + s0 * C::Y_BYTES);
         const uint32_t y1_addr = smem_u32(smem + C::OFF_Y1 + s1 * C::Y_BYTES);
         const uint32_t acc = tmem + C::TM_ACC;
@@ -741,6 +746,15 @@ __global__ void __launch_bounds__(512, 1)
           p_tg = -1;
         }
         mbar_wait_lazy(bar_x_full + xs, (ia / C::NXS) & 1);
+        if (kMode == MODE_FWD && args.x_writeout && lane == 0) {
+          // the gathered stationary rows, in kernel order, for the backward passes (the
+          // slot is read by TMA only: same proxy as its load; the wait is before acc_full)
+          const int wbh = item.x / args.n_row_blocks, wrb = item.x - wbh * args.n_row_blocks;
+          for (int c = 0; c < C::DCH; ++c)
+            tma_store_3d(&tm_x1, smem + C::OFF_X + xs * C::XSLOT_BYTES + c * C::BM * 128, c * 64, wrb * C::BM, wbh);
+          bulk_commit();
+        }
+        __syncwarp();
         if (C::KV_TMEM && elect_one()) {
           // stationary K / V -> TMEM buffer ia % 2 (tcgen05.cp, 128 rows x 16 bf16 per copy);
           // copies and MMAs execute in issue order, so the S^T / dP^T below see them
@@ -1259,7 +1273,10 @@ static int launch_mode(const AttnLaunch& L, cudaStream_t stream) {
   int rc = 0;
   if (L.x_rows) {
     rc |= make_row_map(&mx0, L.x0, L.x_nrows, kD, 2);
-    rc |= make_row_map(&mx1, L.x1 ? L.x1 : L.x0, L.x_nrows, kD, 2);
+    if (kMode == MODE_FWD && L.x_out)  // FWD has one stationary tensor: x1's map writes the tile out
+      rc |= make_map(&mx1, L.x_out, L.BH, L.T_rows, kD, C::BM);
+    else
+      rc |= make_row_map(&mx1, L.x1 ? L.x1 : L.x0, L.x_nrows, kD, 2);
   } else {
     rc |= make_map(&mx0, L.x0, L.BH, L.T_rows, kD, C::BM);
     rc |= make_map(&mx1, L.x1 ? L.x1 : L.x0, L.BH, L.T_rows, kD, C::BM);
@@ -1285,6 +1302,7 @@ static int launch_mode(const AttnLaunch& L, cudaStream_t stream) {
   a.row_runs = reinterpret_cast<const int2*>(L.row_runs);
   a.x_rows = L.x_rows;
   a.y_rows = L.y_rows;
+  a.x_writeout = (kMode == MODE_FWD && L.x_rows && L.x_out) ? 1 : 0;
   a.o_src = static_cast<const __nv_bfloat16*>(L.o_src);
   a.delta_out = L.delta_out;
   a.lse2 = L.lse2;

@@ -92,7 +92,7 @@ static int check_attn_args(int64_t BH, int64_t T_q, int64_t T_kv, int64_t D, int
 
 using namespace scfa;
 
-extern "C" int scfa_abi_version(void) { return 3; }
+extern "C" int scfa_abi_version(void) { return 4; }
 
 extern "C" const char* scfa_last_error(void) { return g_err; }
 
@@ -100,12 +100,18 @@ extern "C" int scfa_attn_fwd(const void* q, const void* k, const void* v, int64_
                              int64_t D, const int32_t* q_idx, const int32_t* q_runs, int64_t Tq_pad, int64_t Tkv_pad,
                              const uint16_t* list, const int32_t* list_count, int64_t list_stride, float scale,
                              int64_t H, int64_t T_out, int out_boundary, void* o, float* m, float* l, float* lse2,
-                             const int32_t* q_rows, const int32_t* k_rows, int64_t R_q, int64_t R_kv, void* stream) {
+                             const int32_t* q_rows, const int32_t* k_rows, int64_t R_q, int64_t R_kv, void* q_out,
+                             void* stream) {
   int rc = check_attn_args(BH, T_q, T_kv, D, Tq_pad, Tkv_pad, q, k, v);
   if (rc) return rc;
   if (BH == 0 || T_q == 0) return SCFA_OK;
+  if (q_out && !q_rows) {
+    set_error("attn_fwd: q_out needs row tables (it is the gathered Q in kernel order)");
+    return SCFA_ERR_PARAM;
+  }
   AttnLaunch L{};
   L.mode = 0;
+  L.x_out = q_out;
   L.D = static_cast<int>(D);
   L.BH = static_cast<int>(BH);
   L.H = static_cast<int>(H);

@@ -207,6 +207,7 @@ def _permute3(xs, ranks, T_perm):
 
 
 _PREP_MAX_T = 16384
+_Q_WRITEOUT = True  # forward gathers Q and writes the bucket-order copy (see _fwd_bwd)
 
 
 def _event_ptr(ev):
@@ -408,6 +409,7 @@ def _fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, exclude_self=True, row_
     prob = _problem_of(sb, exclude_self)
     T_Q, T_KV = q.shape[1], k.shape[1]
     rows = prob.rows if row_tables else None
+    q_writeout = False
     if row_tables:
         xq, xk, xv = q, k, v
         prob.schedule("fwd", "dq", "dkdv")  # runs + all three tile lists in one pass
@@ -420,16 +422,28 @@ def _fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, exclude_self=True, row_
             side.wait_event(sorted_ev)  # perm / rank final: copy under the rest of the preparation
         else:
             side.wait_stream(main)
+        # shared ids: only K / V are copied up front; the forward reads Q through the row
+        # table (once per 128-row item) and writes it back in bucket order for the backward
+        q_writeout = (prob.rows is not None and sb.k_rank is sb.q_rank and sb.q_rank is not None
+                      and T_Q == T_KV and _Q_WRITEOUT)
         with torch.cuda.stream(side):
-            if sb.q_rank is not None and sb.k_rank is not None and T_Q == T_KV:
+            if q_writeout:
+                xk, xv = _permute3([k, v], [sb.k_rank, sb.k_rank], T_KV)
+            elif sb.q_rank is not None and sb.k_rank is not None and T_Q == T_KV:
                 xq, xk, xv = _permute3([q, k, v], [sb.q_rank, sb.k_rank, sb.k_rank], T_Q)
             else:
                 xq, xk, xv = _gather3([q, k, v], [sb.q_perm, sb.k_perm, sb.k_perm], "bthd")
         prob.schedule("fwd", "dq", "dkdv")
         main.wait_stream(side)
-        for t in (xq, xk, xv):
+        for t in (xk, xv) if q_writeout else (xq, xk, xv):
             t.record_stream(main)
-    outputs = attention_forward(prob, xq, xk, xv, scale, boundary=(T_Q, False), rows=rows)
+        if q_writeout:
+            B, H, D = q.shape[0], q.shape[2], q.shape[3]
+            xq = torch.empty((B, H, T_Q, D), dtype=torch.bfloat16, device=q.device)
+            q_only = RowTables(prob.rows.q_rows, None, prob.rows.R_q, prob.rows.R_kv)
+            outputs = attention_forward(prob, q, xk, xv, scale, boundary=(T_Q, False), rows=q_only, q_out=xq)
+    if rows is not None or not q_writeout:
+        outputs = attention_forward(prob, xq, xk, xv, scale, boundary=(T_Q, False), rows=rows)
     dq, dk, dv = attention_backward(prob, xq, xk, xv, outputs, as_operand(d_out), scale,
                                     boundary=(T_Q, T_KV, False), rows=rows,
                                     q_rank=sb.q_rank if sb.q_rank is not None and sb.k_rank is sb.q_rank else None)
