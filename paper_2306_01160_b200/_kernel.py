@@ -355,7 +355,7 @@ def attention_backward(problem, q, k, v, outputs, d_out, scale=None, boundary=No
             _lib.ptr(problem.q_idx), _lib.ptr(sched["q_runs"]), problem.Tq_pad, problem.Tkv_pad,
             _lib.ptr(lse2), _lib.ptr(delta), _lib.ptr(lst), _lib.ptr(cnt), stride,
             _scale(scale, D), H, Tq_out, out_b, _lib.ptr(dq), *rargs,
-            _lib.ptr(O) if fuse else None, _lib.ptr(delta) if fuse else None, _lib.stream_ptr(),
+            _lib.ptr(O) if fuse else None, _lib.ptr(delta) if fuse else None, None, _lib.stream_ptr(),
         )
     if T_kv > 0:
         lst, cnt, stride = sched["dkdv"]
@@ -367,6 +367,56 @@ def attention_backward(problem, q, k, v, outputs, d_out, scale=None, boundary=No
             _scale(scale, D), H, Tkv_out, out_b, _lib.ptr(dk), _lib.ptr(dv), *rargs, _lib.stream_ptr(),
         )
     return dq, dk, dv
+
+
+def dq_backward_gathered(problem, q, k_sorted, v_sorted, outputs, d_out, rows, scale, T_out, do_out):
+    """dQ with the stationary Q / dO read through rows.q_rows from the caller's (B, T, H, D)
+    tensors (gather4, once per item) and streamed K / V from bucket-order copies; delta =
+    rowsum(dO * O) fused in (O read where the forward wrote it) and the gathered dO written
+    back in kernel order to do_out (B, H, T_q, D) for the dK/dV pass.
+    Returns (dQ (B, T_out, H, D) fp32, delta (BH, Tq_pad))."""
+    B, H, D = problem.B, problem.H, problem.D
+    T_q, T_kv = problem.T_q, problem.T_kv
+    dev = q.device
+    BH = B * H
+    dq = torch.empty((B, T_out, H, D), dtype=torch.float32, device=dev)
+    delta = torch.empty((BH, pad128(T_q)), dtype=torch.float32, device=dev)
+    if BH == 0 or T_q == 0:
+        return dq, delta
+    sched = problem.schedule("dq")
+    lst, cnt, stride = sched["dq"]
+    _lib.call(
+        "scfa_attn_bwd_dq",
+        _lib.ptr(q), _lib.ptr(k_sorted), _lib.ptr(v_sorted), _lib.ptr(d_out), BH, T_q, T_kv, D,
+        _lib.ptr(problem.q_idx), _lib.ptr(sched["q_runs"]), problem.Tq_pad, problem.Tkv_pad,
+        _lib.ptr(outputs._lse2), _lib.ptr(delta), _lib.ptr(lst), _lib.ptr(cnt), stride,
+        _scale(scale, D), H, T_out, 1, _lib.ptr(dq), *rows.args(),
+        _lib.ptr(as_operand(outputs.O, dev)), _lib.ptr(delta), _lib.ptr(do_out), _lib.stream_ptr(),
+    )
+    return dq, delta
+
+
+def dkdv_backward_sorted(problem, q_sorted, k_sorted, v_sorted, do_sorted, lse2, delta, scale, T_out):
+    """dK / dV from bucket-order (B, H, T, D) copies, written to their original positions of
+    (B, T_out, H, D) fp32 tensors."""
+    B, H, D = problem.B, problem.H, problem.D
+    T_q, T_kv = problem.T_q, problem.T_kv
+    dev = k_sorted.device
+    BH = B * H
+    dk = torch.empty((B, T_out, H, D), dtype=torch.float32, device=dev)
+    dv = torch.empty((B, T_out, H, D), dtype=torch.float32, device=dev)
+    if BH == 0 or T_kv == 0:
+        return dk, dv
+    sched = problem.schedule("dkdv")
+    lst, cnt, stride = sched["dkdv"]
+    _lib.call(
+        "scfa_attn_bwd_dkdv",
+        _lib.ptr(q_sorted), _lib.ptr(k_sorted), _lib.ptr(v_sorted), _lib.ptr(do_sorted), BH, T_q, T_kv, D,
+        _lib.ptr(problem.k_idx), _lib.ptr(sched["k_runs"]), problem.Tq_pad, problem.Tkv_pad,
+        _lib.ptr(lse2), _lib.ptr(delta), _lib.ptr(lst), _lib.ptr(cnt), stride,
+        _scale(scale, D), H, T_out, 1, _lib.ptr(dk), _lib.ptr(dv), *_NO_ROWS, _lib.stream_ptr(),
+    )
+    return dk, dv
 
 
 def make_row_tables(q_perm, k_perm, B, H, T_q_slots, T_kv_slots, T_Q, T_KV, Tq_pad, Tkv_pad, shared=False):

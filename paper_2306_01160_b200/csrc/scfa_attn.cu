@@ -143,7 +143,8 @@ struct AttnArgs {
   const float* delta;          // (BH, Tq_pad)
   const int* x_rows;  // gather mode: global row per stationary slot (BH, T_rows_pad); null = tiled loads
   const int* y_rows;  // gather mode: global row per streamed slot (BH, T_cols_pad)
-  int x_writeout;              // FWD: write the gathered stationary tile out through tm_x1 (kernel order)
+  int x_writeout;              // gather mode: write a gathered stationary tile out through tm_xo (kernel
+                               // order): FWD its Q, DQ its dO (the tensors dK/dV streams)
   const __nv_bfloat16* o_src;  // DQ: O rows (addressed like dO) for the fused delta
   float* delta_out;            // DQ: delta = rowsum(dO * O) per query slot (BH, T_rows_pad)
   const uint16_t* list;
@@ -488,7 +489,7 @@ template <int kMode, int kD>
 __global__ void __launch_bounds__(512, 1)
     scfa_attn_kernel(const __grid_constant__ CUtensorMap tm_x0, const __grid_constant__ CUtensorMap tm_x1,
                      const __grid_constant__ CUtensorMap tm_y0, const __grid_constant__ CUtensorMap tm_y1,
-                     const AttnArgs args) {
+                     const __grid_constant__ CUtensorMap tm_xo, const AttnArgs args) {
   using C = Cfg<kMode, kD>;
   extern __shared__ __align__(1024) uint8_t smem_base[];
 
@@ -689,7 +690,7 @@ __global__ void __launch_bounds__(512, 1)
         tc_fence_after();
         // the epilogue reuses the stationary slot once acc_full fires: the write-out must
         // have read it by then
-        if (kMode == MODE_FWD && last && args.x_writeout && lane == 0) bulk_wait_read0();
+        if (kMode != MODE_DKDV && last && args.x_writeout && lane == 0) bulk_wait_read0();
         __syncwarp();
         const uint32_t y0_addr = smem_u32(smem + C::OFF_Y0 + s0 * C::Y_BYTES);
         const uint32_t y1_addr = smem_u32(smem + C::OFF_Y1 + s1 * C::Y_BYTES);
@@ -746,12 +747,13 @@ __global__ void __launch_bounds__(512, 1)
           p_tg = -1;
         }
         mbar_wait_lazy(bar_x_full + xs, (ia / C::NXS) & 1);
-        if (kMode == MODE_FWD && args.x_writeout && lane == 0) {
-          // the gathered stationary rows, in kernel order, for the backward passes (the
-          // slot is read by TMA only: same proxy as its load; the wait is before acc_full)
+        if (kMode != MODE_DKDV && args.x_writeout && lane == 0) {
+          // the gathered stationary rows (FWD: Q, DQ: dO), in kernel order, for the dK/dV
+          // pass (the slot is read by TMA only, the proxy of its load; the wait is before
+          // acc_full, after which the epilogue reuses the slot)
           const int wbh = item.x / args.n_row_blocks, wrb = item.x - wbh * args.n_row_blocks;
-          for (int c = 0; c < C::DCH; ++c)
-            tma_store_3d(&tm_x1, smem + C::OFF_X + xs * C::XSLOT_BYTES + c * C::BM * 128, c * 64, wrb * C::BM, wbh);
+          const uint8_t* src = smem + C::OFF_X + xs * C::XSLOT_BYTES + ((kMode == MODE_DQ) ? C::X_BYTES : 0);
+          for (int c = 0; c < C::DCH; ++c) tma_store_3d(&tm_xo, src + c * C::BM * 128, c * 64, wrb * C::BM, wbh);
           bulk_commit();
         }
         __syncwarp();
@@ -828,6 +830,8 @@ __global__ void __launch_bounds__(512, 1)
         ++ia;
       }
       if (p_tg >= 0) flush(p_tg, p_first, p_last, p_ia);
+      if (kMode != MODE_DKDV && args.x_writeout && lane == 0) bulk_wait0();  // write-outs complete
+      __syncwarp();
     }
    }
   } else if (wg == 2) {
@@ -1074,8 +1078,11 @@ __global__ void __launch_bounds__(512, 1)
           my_nlse = -args.lse2[roff];
           if (args.delta_out) {
             // fused delta = rowsum(dO * O) (qk_sparse.py:168): O row from global, dO row
-            // from the stationary tile in shared memory
+            // from the stationary tile in shared memory.  Summed as the delta passes do
+            // (scfa_bwd_prep*: one partial per 16-byte piece, then an xor-butterfly), so
+            // every path gives the same bits.
             float dl = 0.f;
+            float part[kD / 8];
             if (n > 0 && row < args.T_rows) {
               const size_t orow_o = args.x_rows ? static_cast<size_t>(my_idx)
                                                 : static_cast<size_t>(bh) * args.T_rows + row;
@@ -1095,14 +1102,22 @@ __global__ void __launch_bounds__(512, 1)
                              : "r"(addr));
                 const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&ov[j]);
                 const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&dv4);
+                float acc = 0.f;
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                   const float2 x = __bfloat1622float2(a2[e]);
                   const float2 y = __bfloat1622float2(b2[e]);
-                  dl = fmaf(x.x, y.x, dl);
-                  dl = fmaf(x.y, y.y, dl);
+                  acc = fmaf(x.x, y.x, acc);
+                  acc = fmaf(x.y, y.y, acc);
                 }
+                part[j] = acc;
               }
+#pragma unroll
+              for (int w = kD / 16; w >= 1; w >>= 1) {
+#pragma unroll
+                for (int i = 0; i < w; ++i) part[i] = part[i] + part[i + w];
+              }
+              dl = part[0];
             }
             args.delta_out[roff] = dl;
             my_ndelta = -dl;
@@ -1269,14 +1284,11 @@ static int sm_count() {
 template <int kMode, int kD>
 static int launch_mode(const AttnLaunch& L, cudaStream_t stream) {
   using C = Cfg<kMode, kD>;
-  CUtensorMap mx0, mx1, my0, my1;
+  CUtensorMap mx0, mx1, my0, my1, mxo;
   int rc = 0;
   if (L.x_rows) {
     rc |= make_row_map(&mx0, L.x0, L.x_nrows, kD, 2);
-    if (kMode == MODE_FWD && L.x_out)  // FWD has one stationary tensor: x1's map writes the tile out
-      rc |= make_map(&mx1, L.x_out, L.BH, L.T_rows, kD, C::BM);
-    else
-      rc |= make_row_map(&mx1, L.x1 ? L.x1 : L.x0, L.x_nrows, kD, 2);
+    rc |= make_row_map(&mx1, L.x1 ? L.x1 : L.x0, L.x_nrows, kD, 2);
   } else {
     rc |= make_map(&mx0, L.x0, L.BH, L.T_rows, kD, C::BM);
     rc |= make_map(&mx1, L.x1 ? L.x1 : L.x0, L.BH, L.T_rows, kD, C::BM);
@@ -1288,6 +1300,8 @@ static int launch_mode(const AttnLaunch& L, cudaStream_t stream) {
     rc |= make_map(&my0, L.y0, L.BH, L.T_cols, kD, C::BN);
     rc |= make_map(&my1, L.y1, L.BH, L.T_cols, kD, C::BN);
   }
+  const bool writeout = L.x_rows && L.x_out && (kMode == MODE_FWD || kMode == MODE_DQ);
+  rc |= writeout ? make_map(&mxo, L.x_out, L.BH, L.T_rows, kD, C::BM) : make_map(&mxo, L.x0, 1, 1, kD, C::BM);
   if (rc) return SCFA_ERR_CUDA;
   AttnArgs a;
   a.BH = L.BH;
@@ -1302,7 +1316,7 @@ static int launch_mode(const AttnLaunch& L, cudaStream_t stream) {
   a.row_runs = reinterpret_cast<const int2*>(L.row_runs);
   a.x_rows = L.x_rows;
   a.y_rows = L.y_rows;
-  a.x_writeout = (kMode == MODE_FWD && L.x_rows && L.x_out) ? 1 : 0;
+  a.x_writeout = writeout ? 1 : 0;
   a.o_src = static_cast<const __nv_bfloat16*>(L.o_src);
   a.delta_out = L.delta_out;
   a.lse2 = L.lse2;
@@ -1331,7 +1345,7 @@ static int launch_mode(const AttnLaunch& L, cudaStream_t stream) {
   if (a.n_items == 0) return SCFA_OK;
   int grid = sm_count();
   if (grid * C::NSTREAM > a.n_items) grid = (a.n_items + C::NSTREAM - 1) / C::NSTREAM;
-  kern<<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(mx0, mx1, my0, my1, a);
+  kern<<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(mx0, mx1, my0, my1, mxo, a);
   return cudaGetLastError() == cudaSuccess ? SCFA_OK : SCFA_ERR_CUDA;
 }
 

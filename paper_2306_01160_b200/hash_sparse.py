@@ -208,6 +208,7 @@ def _permute3(xs, ranks, T_perm):
 
 _PREP_MAX_T = 16384
 _Q_WRITEOUT = True  # forward gathers Q and writes the bucket-order copy (see _fwd_bwd)
+_DO_WRITEOUT = True  # dQ gathers Q / dO, fuses delta, writes the bucket-order dO copy
 
 
 def _event_ptr(ev):
@@ -438,10 +439,20 @@ def _fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, exclude_self=True, row_
         for t in (xk, xv) if q_writeout else (xq, xk, xv):
             t.record_stream(main)
         if q_writeout:
+            from ._kernel import dkdv_backward_sorted, dq_backward_gathered
+
             B, H, D = q.shape[0], q.shape[2], q.shape[3]
             xq = torch.empty((B, H, T_Q, D), dtype=torch.bfloat16, device=q.device)
             q_only = RowTables(prob.rows.q_rows, None, prob.rows.R_q, prob.rows.R_kv)
             outputs = attention_forward(prob, q, xk, xv, scale, boundary=(T_Q, False), rows=q_only, q_out=xq)
+            if _DO_WRITEOUT:
+                # dQ gathers Q / dO the same way, fuses delta and writes dO back in bucket
+                # order: no separate delta / dO pass
+                xdo = torch.empty((B, H, T_Q, D), dtype=torch.bfloat16, device=q.device)
+                dq, delta = dq_backward_gathered(prob, q, xk, xv, outputs, as_operand(d_out), q_only, scale, T_Q,
+                                                 xdo)
+                dk, dv = dkdv_backward_sorted(prob, xq, xk, xv, xdo, outputs._lse2, delta, scale, T_KV)
+                return outputs, dq, dk, dv, prob
     if rows is not None or not q_writeout:
         outputs = attention_forward(prob, xq, xk, xv, scale, boundary=(T_Q, False), rows=rows)
     dq, dk, dv = attention_backward(prob, xq, xk, xv, outputs, as_operand(d_out), scale,
