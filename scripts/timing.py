@@ -64,8 +64,11 @@ def hook(name, phase):
 
 
 _lib.EVENT_HOOK = hook
-out = attention_forward(prob, sb.q, sb.k, sb.v, boundary=bnd_f)
-g = attention_backward(prob, sb.q, sb.k, sb.v, out, dO, boundary=bnd_b)
+if MODE == "fused":  # the fused hash fwd+bwd (gathered stationary Q / dO, write-outs, fused delta)
+    hs._fwd_bwd(q, k, v, hb, hb, dO)
+else:
+    out = attention_forward(prob, sb.q, sb.k, sb.v, boundary=bnd_f)
+    g = attention_backward(prob, sb.q, sb.k, sb.v, out, dO, boundary=bnd_b)
 torch.cuda.synchronize()
 _lib.EVENT_HOOK = None
 print("ctas/sm", [lib.scfa_debug_ctas_per_sm(m, 64) for m in range(3)])
