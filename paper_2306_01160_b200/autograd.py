@@ -11,6 +11,7 @@ epilogues write each gradient row straight back to its original position.
 import torch
 
 from ._kernel import as_operand, attention_backward, attention_forward
+from ._headdim import padded_call
 
 __all__ = ["dense_causal_attention_autograd", "hash_sparse_attention_autograd", "qk_sparse_attention_autograd"]
 
@@ -58,6 +59,7 @@ class _QkSparseAttention(torch.autograd.Function):
         return dq.to(qt), dk.to(kt), dv.to(vt), None, None, None
 
 
+@padded_call("attn")
 def hash_sparse_attention_autograd(q, k, v, q_hash, k_hash, scale=None, exclude_self=True, check=True):
     """hash_sparse_attention (hash_sparse.py:223-238) with gradients w.r.t. q, k, v.
 
@@ -67,6 +69,7 @@ def hash_sparse_attention_autograd(q, k, v, q_hash, k_hash, scale=None, exclude_
     return _HashSparseAttention.apply(q, k, v, q_hash, k_hash, scale, exclude_self, check)
 
 
+@padded_call("attn")
 def qk_sparse_attention_autograd(q, k, v, q_keep, k_keep, scale=None):
     """qk_sparse_attention (qk_sparse.py:228-239) with gradients w.r.t. q, k, v."""
     return _QkSparseAttention.apply(q, k, v, q_keep, k_keep, scale)
@@ -103,6 +106,7 @@ class _DenseCausalAttention(torch.autograd.Function):
         return dq.to(qt), dk.to(kt), dv.to(vt), None
 
 
+@padded_call("attn")
 def dense_causal_attention_autograd(q, k, v, scale=None):
     """Dense causal attention on (B, T, H, D) operands with gradients (dense.py:33-93)."""
     return _DenseCausalAttention.apply(q, k, v, scale)

@@ -12,6 +12,7 @@ from . import _lib
 from ._kernel import Problem, as_operand, attention_backward, attention_forward, check_forward_operands
 from .errors import ShapeError
 from .tensors import BlockSpec, pad128
+from ._headdim import padded_call
 
 
 def dense_tile_count(T, blocks=BlockSpec()):
@@ -44,6 +45,7 @@ def causal_problem(B, H, T, D, device):
     return Problem(B, H, T, T, D, _arange_aux(B, H, T, -1, device), _arange_aux(B, H, T, 0x7FFFFFFF, device))
 
 
+@padded_call("flash_fwd")
 def flash_forward(q, k, v, blocks=BlockSpec(), scale=None, workers=None):
     """Tiled causal attention over (B, H, T, D) operands (dense.py:33-63)."""
     q, k, v = as_operand(q), as_operand(k), as_operand(v)
@@ -54,6 +56,7 @@ def flash_forward(q, k, v, blocks=BlockSpec(), scale=None, workers=None):
     return attention_forward(causal_problem(B, H, T, D, q.device), q, k, v, scale, blocks)
 
 
+@padded_call("flash_bwd")
 def flash_backward(q, k, v, outputs, d_out, blocks=BlockSpec(), scale=None, workers=None):
     """Gradients of <O, dO> w.r.t. (Q, K, V), fp32 (dense.py:66-93)."""
     q, k, v = as_operand(q), as_operand(k), as_operand(v)

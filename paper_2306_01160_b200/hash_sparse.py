@@ -27,6 +27,7 @@ from ._kernel import (
 )
 from .errors import NumericError, ParameterError, ShapeError
 from .tensors import DOMAIN_BUCKETS, DOMAIN_PROJECTIONS, BlockSpec, pad128, stream
+from ._headdim import padded_call
 
 _OOB_QI, _OOB_KI = -1, 0x7FFFFFFF
 _OOB_QH, _OOB_KH = -3, -2
@@ -305,6 +306,7 @@ def _sort_batch(q, k, v, q_hash, k_hash, layout, q_pos=None, k_pos=None, check=T
     )
 
 
+@padded_call("sort")
 def sort_by_bucket(q, k, v, q_hash, k_hash, q_idx=None, k_idx=None):
     """Reorder engine-layout operands by (bucket, position) (hash_sparse.py:97-133)."""
     q, k, v = as_operand(q), as_operand(k), as_operand(v)
@@ -345,6 +347,7 @@ def _problem_of(sb, exclude_self, validate=True):
     return prob
 
 
+@padded_call("hash_fwd")
 def hash_forward_kernel(sorted_batch, scale=None, blocks=BlockSpec(), exclude_self=True, workers=None):
     """Banded forward over a SortedBatch (hash_sparse.py:145-179)."""
     sb = sorted_batch
@@ -354,6 +357,7 @@ def hash_forward_kernel(sorted_batch, scale=None, blocks=BlockSpec(), exclude_se
     return attention_forward(prob, sb.q, sb.k, sb.v, scale, blocks)
 
 
+@padded_call("hash_bwd")
 def hash_backward_kernel(sorted_batch, outputs, d_out_sorted, scale=None, blocks=BlockSpec(), exclude_self=True,
                          workers=None):
     """Gradients w.r.t. the sorted operands, fp32 (hash_sparse.py:182-213)."""
@@ -382,6 +386,7 @@ def hash_scatter(o_sorted, q_idx):
     return _scatter(o_sorted, rank, "bhtd")
 
 
+@padded_call("attn")
 def hash_sparse_attention(q, k, v, q_hash, k_hash, scale=None, blocks=BlockSpec(), exclude_self=True,
                           workers=None):
     """End-to-end hash-sparse attention in boundary layout (hash_sparse.py:223-238).
@@ -461,6 +466,7 @@ def _fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, exclude_self=True, row_
     return outputs, dq, dk, dv, prob
 
 
+@padded_call("fwd_bwd")
 def hash_sparse_attention_fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, exclude_self=True, row_tables=False,
                                   out=None):
     """Forward + backward through the whole hash path, boundary layout in and out.

@@ -31,6 +31,7 @@ from ._kernel import (
 )
 from .errors import ShapeError
 from .tensors import DOMAIN_KEEP, KEY_PAD, QUERY_PAD, BlockSpec, pad128, stream
+from ._headdim import padded_call
 
 _OOB_Q = QUERY_PAD
 _OOB_K = 0x7FFFFFFF
@@ -138,6 +139,7 @@ def qk_tile_schedule(q_idx, k_idx, blocks=BlockSpec()):
     return causal_j_stops(q_idx, k_idx, blocks)
 
 
+@padded_call("prep")
 def qk_preprocess(q, k, v, q_keep, k_keep, materialize=True):
     """Compact, pad and transpose boundary-layout inputs (qk_sparse.py:196-211).
 
@@ -195,6 +197,7 @@ def _problem_from(q_c, k_c, q_idx, k_idx, validate=True):
     return prob
 
 
+@padded_call("qk_fwd")
 def qk_forward_kernel(q_c, k_c, v_c, q_idx, k_idx, scale=None, blocks=BlockSpec(), workers=None):
     """Irregular-causal forward over compacted operands (qk_sparse.py:120-148)."""
     q_c, k_c, v_c = as_operand(q_c), as_operand(k_c), as_operand(v_c)
@@ -207,6 +210,7 @@ def qk_forward_kernel(q_c, k_c, v_c, q_idx, k_idx, scale=None, blocks=BlockSpec(
     return attention_forward(prob, q_c, k_c, v_c, scale, blocks)
 
 
+@padded_call("qk_bwd")
 def qk_backward_kernel(q_c, k_c, v_c, outputs, d_out_c, q_idx, k_idx, scale=None, blocks=BlockSpec(),
                        workers=None):
     """Gradients w.r.t. compacted operands, fp32 (qk_sparse.py:151-183)."""
@@ -250,6 +254,7 @@ def qk_postprocess(o_kernel, scatter_index, T_Q, rank=None):
     return _scatter(o_kernel, rank, T_Q)
 
 
+@padded_call("attn")
 def qk_sparse_attention(q, k, v, q_keep, k_keep, scale=None, blocks=BlockSpec(), workers=None):
     """End-to-end QK-sparse attention in boundary layout (qk_sparse.py:228-239).
 
@@ -261,6 +266,7 @@ def qk_sparse_attention(q, k, v, q_keep, k_keep, scale=None, blocks=BlockSpec(),
                              boundary=(prep.T_Q, True)).O
 
 
+@padded_call("fwd_bwd")
 def qk_sparse_attention_fwd_bwd(q, k, v, q_keep, k_keep, d_out, scale=None, row_tables=False):
     """Forward + backward through the whole QK path in boundary layout.
 

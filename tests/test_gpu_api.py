@@ -1,6 +1,7 @@
 """The reference's own kernel-level and end-to-end tests (pkg/tests/test_qk.py,
-test_hash.py), restated on the CUDA path at D = 64 (the engine's head dims are 64 /
-128; the reference tests use D = 3..8 on its NumPy loop).
+test_hash.py), restated on the CUDA path, mostly at D = 64 (the engine's tile head dims
+are 64 / 128; other D <= 128 are zero-padded by the public calls — tested at the end,
+including the reference's own D = 4).
 
 Exact-equality tests (`bitwise dense`, `zero upstream`, `all dropped`, `collision
 pattern`) keep the reference's exactness; numeric comparisons use the bf16 tolerance
@@ -207,3 +208,61 @@ def test_nan_safety_large_logits():  # test_acceptance.py:203+
     hb = scfa.random_buckets(1, 256, 2, 4, 49)
     o, gq, gk, gv = scfa.hash_sparse_attention_fwd_bwd(_t(qb), _t(kb), _t(vb), hb, hb, _t(qb))
     assert all(bool(torch.isfinite(x).all()) for x in (o, gq, gk, gv))
+
+
+# ------------------------------------------------------------------ head dims other than 64 / 128
+
+@pytest.mark.parametrize("D", [4, 8, 32, 96])
+def test_small_and_odd_head_dims_match_oracle(D):
+    """The engine zero-pads D up to 64 / 128 (scale stays 1/sqrt(D)): same results as the
+    oracle at the caller's D, for the end-to-end hash and QK fwd+bwd and the dense path."""
+    B, H, T = 1, 2, 200
+    qb, kb, vb = (_boundary(x) for x in make_batch(B, H, T, D, seed=91))
+    dO = bf16_round(np.random.default_rng(92).standard_normal((B, T, H, D)))
+    eng = lambda x: np.swapaxes(x, 1, 2)
+    hb = scfa.random_buckets(B, T, H, 4, 93)
+    hh = hb.transpose(0, 2, 1)
+    pos = np.arange(T)
+    vis = orc.visibility(pos, pos, hh, hh, exclude_self=True)
+    O, _, _ = orc.attention(eng(qb), eng(kb), eng(vb), vis)
+    grads = orc.attention_grads(eng(qb), eng(kb), eng(vb), vis, eng(dO))
+    got = scfa.hash_sparse_attention_fwd_bwd(_t(qb), _t(kb), _t(vb), _t(hb, torch.int64), _t(hb, torch.int64),
+                                             _t(dO))
+    for g, w in zip(got, (O,) + tuple(grads)):
+        assert g.shape[-1] == D
+        assert np.max(np.abs(_np(g) - eng(w))) <= 2e-2
+    o = scfa.hash_sparse_attention(_t(qb), _t(kb), _t(vb), hb, hb)
+    assert tuple(o.shape) == (B, T, H, D) and np.max(np.abs(_np(o) - eng(O))) <= 2e-2
+    # dense comparator, kernel level
+    q, k, v = (_t(eng(x)) for x in (qb, kb, vb))
+    out = scfa.flash_forward(q, k, v)
+    Od, _, _ = orc.attention(eng(qb), eng(kb), eng(vb), orc.visibility(pos, pos))
+    assert out.O.shape[-1] == D and np.max(np.abs(_np(out.O) - Od)) <= 2e-2
+    gd = scfa.flash_backward(q, k, v, out, _t(eng(dO)))
+    wd = orc.attention_grads(eng(qb), eng(kb), eng(vb), orc.visibility(pos, pos), eng(dO))
+    for g, w in zip(gd, wd):
+        assert g.shape[-1] == D and np.max(np.abs(_np(g) - w)) <= 2e-2
+
+
+def test_reference_style_tiny_head_dim_bitwise_dense():  # test_qk.py:137-146 at its own D = 4
+    q, k, v = (_t(x) for x in make_batch(2, 2, 48, 4, seed=5))
+    dense = scfa.flash_forward(q, k, v)
+    idx = torch.arange(48).expand(2, 2, 48)
+    sparse = scfa.qk_forward_kernel(q, k, v, idx, idx)
+    assert sparse.O.shape[-1] == 4
+    assert torch.equal(sparse.O, dense.O) and torch.equal(sparse.M, dense.M)
+
+
+def test_autograd_with_padded_head_dim():
+    B, T, H, D = 1, 256, 2, 40
+    rng = np.random.default_rng(94)
+    x = [torch.from_numpy(rng.standard_normal((B, T, H, D)).astype(np.float32)).cuda().requires_grad_()
+         for _ in range(3)]
+    ids = torch.from_numpy(scfa.random_buckets(B, T, H, 4, 95)).cuda()
+    o = scfa.dynamic_sparse_attention(x[0], x[1], x[2], ids, ids)
+    assert o.shape[-1] == D
+    o.sum().backward()
+    assert all(t.grad is not None and t.grad.shape[-1] == D and bool(torch.isfinite(t.grad).all()) for t in x)
+    with pytest.raises(scfa.ShapeError):
+        scfa.hash_sparse_attention(torch.zeros(1, 8, 1, 160), torch.zeros(1, 8, 1, 160), torch.zeros(1, 8, 1, 160),
+                                   ids[:, :8, :1], ids[:, :8, :1])
