@@ -9,12 +9,13 @@ layout is (B, H, T, D), the boundary layout (B, T, H, D).
 """
 
 import os
+import struct
 from dataclasses import dataclass
 
 import numpy as np
 import torch
 
-from .errors import ParameterError, ShapeError
+from .errors import FormatError, ParameterError, ShapeError
 
 KEY_PAD = 10**9
 QUERY_PAD = -1
@@ -109,3 +110,57 @@ def worker_count():
 
 def pad128(T):
     return ((int(T) + 127) // 128) * 128
+
+
+# ---------------------------------------------------------------- SCFA tensor files
+
+MAGIC = b"SCFA"
+VERSION = 1
+_HEADER = struct.Struct("<4sIB4Q")
+
+
+def save_tensor(path, x):
+    """Write a (B, H, T, D) float32 / float64 tensor in the reference's container format
+    (tensors.py:110-125): magic "SCFA", u32 version 1, u8 bytes per element, four u64
+    extents, then the little-endian values in row-major order.  Torch tensors (any device)
+    are written from their host copy."""
+    if isinstance(x, torch.Tensor):
+        x = x.detach().cpu().numpy()
+    x = np.asarray(x)
+    if x.ndim != 4:
+        raise ShapeError(f"tensor must be 4-D (B, H, T, D), got ndim={x.ndim}")
+    if x.dtype not in (np.float32, np.float64):
+        raise ShapeError(f"tensor must be float32 or float64, got {x.dtype}")
+    if not np.isfinite(x).all():
+        raise ShapeError("tensor must be finite")
+    with open(path, "wb") as f:
+        f.write(_HEADER.pack(MAGIC, VERSION, x.dtype.itemsize, *x.shape))
+        f.write(np.ascontiguousarray(x, dtype=x.dtype.newbyteorder("<")).tobytes())
+
+
+def load_tensor(path):
+    """Read a file written by save_tensor (either implementation); FormatError with the
+    byte offset of the first defect otherwise (tensors.py:128-154)."""
+    with open(path, "rb") as f:
+        raw = f.read()
+    if len(raw) < _HEADER.size:
+        raise FormatError("file truncated inside header", len(raw))
+    magic, version, itemsize, B, H, T, D = _HEADER.unpack_from(raw, 0)
+    if magic != MAGIC:
+        raise FormatError(f"bad magic {magic!r}", 0)
+    if version != VERSION:
+        raise FormatError(f"unsupported version {version}", 4)
+    if itemsize not in (4, 8):
+        raise FormatError(f"bad precision byte {itemsize}", 8)
+    for i, e in enumerate((B, H, T, D)):
+        if e < 1:
+            raise FormatError(f"extent {i} is {e}", 9 + 8 * i)
+    count = B * H * T * D
+    expected = _HEADER.size + count * itemsize
+    if len(raw) != expected:
+        raise FormatError(f"payload has {len(raw) - _HEADER.size} bytes, expected {count * itemsize}",
+                          min(len(raw), expected))
+    dtype = np.dtype("<f4" if itemsize == 4 else "<f8")
+    data = np.frombuffer(raw, dtype=dtype, count=count, offset=_HEADER.size)
+    return data.reshape(B, H, T, D).astype(dtype.newbyteorder("="))
+

@@ -20,6 +20,8 @@ reference's public functions in float64:
   dense: flash_forward / flash_backward (dense.py:33-93).
   lsh:   lsh_buckets (hash_sparse.py:34-52) at several bucket counts (lsh_small.npz;
          `--lsh-only` regenerates just that file).
+  files: tensor_f32.scfa / tensor_f64.scfa written by the reference's save_tensor
+         (tensors.py:110-125) with their arrays in tensor_files.npz.
 
 Stored per case (one .npz): the integer provenance (compaction indices,
 counts, sorted positions / buckets, reference schedules at BlockSpec(64,64)),
@@ -204,11 +206,25 @@ def lsh_case():
     return arrays, {"seed": 31, "nbs": [2, 6, 16, 64]}
 
 
+def tensor_files():
+    """Two files written by the reference's save_tensor (tensors.py:110-125), and the arrays."""
+    from scfa import save_tensor
+
+    x = np.random.default_rng(7).standard_normal((2, 3, 5, 4)).astype(np.float32)
+    y = np.random.default_rng(8).standard_normal((1, 2, 3, 8))
+    save_tensor(os.path.join(HERE, "tensor_f32.scfa"), x)
+    save_tensor(os.path.join(HERE, "tensor_f64.scfa"), y)
+    np.savez_compressed(os.path.join(HERE, "tensor_files.npz"), f32=x, f64=y)
+
+
 def main():
     try:
         import scfa  # noqa: F401
     except ImportError:
         sys.exit("run with PYTHONPATH=/root/reference/pkg/src (the reference package)")
+    if "--tensor-files-only" in sys.argv:
+        tensor_files()
+        return
     if "--lsh-only" in sys.argv:
         arrays, meta = lsh_case()
         np.savez_compressed(os.path.join(HERE, "lsh_small.npz"), **arrays)
@@ -228,6 +244,7 @@ def main():
     arrays, meta = lsh_case()
     np.savez_compressed(os.path.join(HERE, "lsh_small.npz"), **arrays)
     print("lsh_small", meta)
+    tensor_files()
 
 
 if __name__ == "__main__":
