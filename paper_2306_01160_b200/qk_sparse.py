@@ -145,6 +145,7 @@ def qk_preprocess(q, k, v, q_keep, k_keep, materialize=True):
 
     materialize=False: no compacted copies; q_c / k_c / v_c are the (B, T, H, D) inputs
     and problem.rows holds the row tables the gather-mode kernels read them through.
+    materialize="kv": compacted K / V only (q_c is the input Q, problem.rows set).
     """
     q, k, v = as_operand(q), as_operand(k), as_operand(v)
     if q.dim() != 4 or k.dim() != 4 or k.shape != v.shape:
@@ -168,7 +169,10 @@ def qk_preprocess(q, k, v, q_keep, k_keep, materialize=True):
     q_aux = _aux(q_perm, cnt[:BH], B, H, T_cq, QUERY_PAD, _OOB_Q)
     k_aux = _aux(k_perm, cnt[BH: 2 * BH], B, H, T_ck, KEY_PAD, _OOB_K)
     problem = Problem(B, H, T_cq, T_ck, D, q_aux, k_aux)
-    if materialize:
+    if materialize == "kv":  # compacted K / V; Q stays in place behind the row tables
+        q_c, k_c, v_c = q, _gather(k, k_perm, T_ck), _gather(v, k_perm, T_ck)
+        problem.rows = make_row_tables(q_perm, k_perm, B, H, T_cq, T_ck, T_Q, T_KV, problem.Tq_pad, problem.Tkv_pad)
+    elif materialize:
         q_c = _gather(q, q_perm, T_cq)
         k_c = _gather(k, k_perm, T_ck)
         v_c = _gather(v, k_perm, T_ck)
@@ -274,10 +278,32 @@ def qk_sparse_attention_fwd_bwd(q, k, v, q_keep, k_keep, d_out, scale=None, row_
     zero outputs and zero gradients.  The reference composes the same thing
     from qk_preprocess -> qk_forward_kernel -> qk_backward_kernel.
     """
-    prep = qk_preprocess(q, k, v, q_keep, k_keep, materialize=not row_tables)
+    prep = qk_preprocess(q, k, v, q_keep, k_keep, materialize=False if row_tables else "kv")
     T_Q, T_KV = q.shape[1], k.shape[1]
     prob = prep.problem
     prob.schedule("fwd", "dq", "dkdv")
+    if not row_tables and prob.rows is not None and prob.T_q > 0:
+        # as the hash path: Q is read through the row table and written back compacted by
+        # the forward, dQ reads Q / dO the same way, fuses delta and writes dO back, and
+        # dK/dV streams both copies — only K / V are copied up front
+        from ._kernel import RowTables, dkdv_backward_sorted, dq_backward_gathered
+
+        B, H, D = prob.B, prob.H, prob.D
+        q_b, d_b = as_operand(q), as_operand(d_out)
+        xq = torch.empty((B, H, prob.T_q, D), dtype=torch.bfloat16, device=q_b.device)
+        xdo = torch.empty_like(xq)
+        q_only = RowTables(prob.rows.q_rows, None, prob.rows.R_q, prob.rows.R_kv)
+        outputs = attention_forward(prob, q_b, prep.k_c, prep.v_c, scale, boundary=(T_Q, False), rows=q_only,
+                                    q_out=xq)
+        dq, delta = dq_backward_gathered(prob, q_b, prep.k_c, prep.v_c, outputs, d_b, q_only, scale, T_Q, xdo)
+        dk, dv = dkdv_backward_sorted(prob, xq, prep.k_c, prep.v_c, xdo, outputs._lse2, delta, scale, T_KV)
+        _zero_dropped(q_keep, outputs.O, dq)
+        _zero_dropped(k_keep, dk, dv)
+        return outputs.O, dq, dk, dv
+    if not row_tables:  # degenerate sizes: the materialised path
+        prep = qk_preprocess(q, k, v, q_keep, k_keep)
+        prob = prep.problem
+        prob.schedule("fwd", "dq", "dkdv")
     rows = prob.rows if row_tables else None
     # the kernels write every kept row; only the dropped rows are zeroed (no full fill)
     outputs = attention_forward(prob, prep.q_c, prep.k_c, prep.v_c, scale, boundary=(T_Q, False), rows=rows)
