@@ -19,21 +19,19 @@ __all__ = ["dense_causal_attention_autograd", "hash_sparse_attention_autograd", 
 class _HashSparseAttention(torch.autograd.Function):
     @staticmethod
     def forward(ctx, q, k, v, q_hash, k_hash, scale, exclude_self, check):
-        from .hash_sparse import _problem_of, _sort_batch
+        # the same stages as hash_sparse_attention_fwd_bwd (copy-free bucket order for Q / dO)
+        from .hash_sparse import _hash_forward_stage
 
-        qb, kb, vb = as_operand(q), as_operand(k), as_operand(v)
-        sb = _sort_batch(qb, kb, vb, q_hash, k_hash, "bthd", exclude_self=exclude_self, check=check)
-        prob = _problem_of(sb, exclude_self)
-        prob.schedule("fwd", "dq", "dkdv")
-        out = attention_forward(prob, sb.q, sb.k, sb.v, scale, boundary=(q.shape[1], False))
-        ctx.state = (prob, sb, out, scale, q.shape[1], k.shape[1], q.dtype, k.dtype, v.dtype)
-        return out.O.to(q.dtype)
+        st = _hash_forward_stage(q, k, v, q_hash, k_hash, scale, exclude_self, check=check)
+        ctx.state = (st, q.dtype, k.dtype, v.dtype)
+        return st.outputs.O.to(q.dtype)
 
     @staticmethod
     def backward(ctx, d_out):
-        prob, sb, out, scale, T_Q, T_KV, qt, kt, vt = ctx.state
-        dq, dk, dv = attention_backward(prob, sb.q, sb.k, sb.v, out, as_operand(d_out.contiguous()), scale,
-                                        boundary=(T_Q, T_KV, False))
+        from .hash_sparse import _hash_backward_stage
+
+        st, qt, kt, vt = ctx.state
+        dq, dk, dv = _hash_backward_stage(st, d_out.contiguous())
         ctx.state = None
         return dq.to(qt), dk.to(kt), dv.to(vt), None, None, None, None, None
 

@@ -400,70 +400,93 @@ def hash_sparse_attention(q, k, v, q_hash, k_hash, scale=None, blocks=BlockSpec(
     return attention_forward(prob, sb.q, sb.k, sb.v, scale, blocks, boundary=(q.shape[1], False)).O
 
 
-def _fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, exclude_self=True, row_tables=False):
-    """The fused boundary-layout fwd + bwd; returns (FlashOutputs, dq, dk, dv, problem).
+class _HashState:
+    """What the backward stage needs from the forward stage."""
 
-    row_tables=False (default): Q / K / V are gathered once into bucket order and the
-    kernels stream them with tiled TMA loads (the fast path: tile::gather4 sustains only
-    ~1.6 TB/s chip-wide, scripts/gather_bw.cu).  row_tables=True: the kernels read the
-    caller's tensors through row tables (no copies at all).
+    __slots__ = ("prob", "sb", "q", "xq", "xk", "xv", "outputs", "rows", "q_only", "scale", "T_Q", "T_KV")
+
+
+def _hash_forward_stage(q, k, v, q_hash, k_hash, scale=None, exclude_self=True, row_tables=False, check=False):
+    """Preparation + forward of the boundary-layout hash path; returns a _HashState.
+
+    Default (shared ids): Q / K / V are put in bucket order without copy passes for Q:
+    K / V are permuted up front (`scfa_permute_rows3`, on a side stream started as soon as
+    the sort is final, under the finishing / tile-list kernels), the forward reads Q
+    through the row table (tile::gather4, once per 128-row item) and writes the
+    bucket-order Q copy back with TMA stores.  Separate query / key ids: Q / K / V are
+    copied (tiled loads everywhere).  row_tables=True: every load goes through the row
+    tables (no copies at all; tile::gather4 sustains only ~1.6 TB/s, scripts/gather_bw.cu).
     """
     q, k, v = as_operand(q), as_operand(k), as_operand(v)
     sorted_ev = torch.cuda.Event() if not row_tables else None
-    sb = _sort_batch(q, k, v, q_hash, k_hash, "bthd", check=False, exclude_self=exclude_self, materialize=False,
+    sb = _sort_batch(q, k, v, q_hash, k_hash, "bthd", check=check, exclude_self=exclude_self, materialize=False,
                      sorted_event=sorted_ev)
     prob = _problem_of(sb, exclude_self)
-    T_Q, T_KV = q.shape[1], k.shape[1]
-    rows = prob.rows if row_tables else None
-    q_writeout = False
+    st = _HashState()
+    st.prob, st.sb, st.q, st.scale = prob, sb, q, scale
+    st.T_Q, st.T_KV = q.shape[1], k.shape[1]
+    st.rows, st.q_only = (prob.rows if row_tables else None), None
     if row_tables:
-        xq, xk, xv = q, k, v
+        st.xq, st.xk, st.xv = q, k, v
         prob.schedule("fwd", "dq", "dkdv")  # runs + all three tile lists in one pass
+        st.outputs = attention_forward(prob, q, k, v, scale, boundary=(st.T_Q, False), rows=st.rows)
+        return st
+    main = torch.cuda.current_stream(q.device)
+    side = _copy_streams(q.device)[2]
+    shared = sb.q_rank is not None and sb.k_rank is sb.q_rank
+    if sorted_ev.cuda_event and shared:
+        side.wait_event(sorted_ev)  # perm / rank final: copy under the rest of the preparation
     else:
-        # the bucket-ordered copies (side stream) and the tile lists (this stream) are
-        # independent: overlap them
-        main = torch.cuda.current_stream(q.device)
-        side = _copy_streams(q.device)[2]
-        if sorted_ev is not None and sorted_ev.cuda_event and sb.k_rank is sb.q_rank:
-            side.wait_event(sorted_ev)  # perm / rank final: copy under the rest of the preparation
-        else:
-            side.wait_stream(main)
-        # shared ids: only K / V are copied up front; the forward reads Q through the row
-        # table (once per 128-row item) and writes it back in bucket order for the backward
-        q_writeout = (prob.rows is not None and sb.k_rank is sb.q_rank and sb.q_rank is not None
-                      and T_Q == T_KV and _Q_WRITEOUT)
-        with torch.cuda.stream(side):
-            if q_writeout:
-                xk, xv = _permute3([k, v], [sb.k_rank, sb.k_rank], T_KV)
-            elif sb.q_rank is not None and sb.k_rank is not None and T_Q == T_KV:
-                xq, xk, xv = _permute3([q, k, v], [sb.q_rank, sb.k_rank, sb.k_rank], T_Q)
-            else:
-                xq, xk, xv = _gather3([q, k, v], [sb.q_perm, sb.k_perm, sb.k_perm], "bthd")
-        prob.schedule("fwd", "dq", "dkdv")
-        main.wait_stream(side)
-        for t in (xk, xv) if q_writeout else (xq, xk, xv):
-            t.record_stream(main)
+        side.wait_stream(main)
+    q_writeout = prob.rows is not None and shared and st.T_Q == st.T_KV and _Q_WRITEOUT
+    with torch.cuda.stream(side):
         if q_writeout:
-            from ._kernel import dkdv_backward_sorted, dq_backward_gathered
+            xk, xv = _permute3([k, v], [sb.k_rank, sb.k_rank], st.T_KV)
+            xq = None
+        elif sb.q_rank is not None and sb.k_rank is not None and st.T_Q == st.T_KV:
+            xq, xk, xv = _permute3([q, k, v], [sb.q_rank, sb.k_rank, sb.k_rank], st.T_Q)
+        else:
+            xq, xk, xv = _gather3([q, k, v], [sb.q_perm, sb.k_perm, sb.k_perm], "bthd")
+    prob.schedule("fwd", "dq", "dkdv")  # overlaps the copies
+    main.wait_stream(side)
+    for t in (xq, xk, xv):
+        if t is not None:
+            t.record_stream(main)
+    if q_writeout:
+        B, H, D = q.shape[0], q.shape[2], q.shape[3]
+        xq = torch.empty((B, H, st.T_Q, D), dtype=torch.bfloat16, device=q.device)
+        st.q_only = RowTables(prob.rows.q_rows, None, prob.rows.R_q, prob.rows.R_kv)
+        st.outputs = attention_forward(prob, q, xk, xv, scale, boundary=(st.T_Q, False), rows=st.q_only, q_out=xq)
+    else:
+        st.outputs = attention_forward(prob, xq, xk, xv, scale, boundary=(st.T_Q, False))
+    st.xq, st.xk, st.xv = xq, xk, xv
+    return st
 
-            B, H, D = q.shape[0], q.shape[2], q.shape[3]
-            xq = torch.empty((B, H, T_Q, D), dtype=torch.bfloat16, device=q.device)
-            q_only = RowTables(prob.rows.q_rows, None, prob.rows.R_q, prob.rows.R_kv)
-            outputs = attention_forward(prob, q, xk, xv, scale, boundary=(T_Q, False), rows=q_only, q_out=xq)
-            if _DO_WRITEOUT:
-                # dQ gathers Q / dO the same way, fuses delta and writes dO back in bucket
-                # order: no separate delta / dO pass
-                xdo = torch.empty((B, H, T_Q, D), dtype=torch.bfloat16, device=q.device)
-                dq, delta = dq_backward_gathered(prob, q, xk, xv, outputs, as_operand(d_out), q_only, scale, T_Q,
-                                                 xdo)
-                dk, dv = dkdv_backward_sorted(prob, xq, xk, xv, xdo, outputs._lse2, delta, scale, T_KV)
-                return outputs, dq, dk, dv, prob
-    if rows is not None or not q_writeout:
-        outputs = attention_forward(prob, xq, xk, xv, scale, boundary=(T_Q, False), rows=rows)
-    dq, dk, dv = attention_backward(prob, xq, xk, xv, outputs, as_operand(d_out), scale,
-                                    boundary=(T_Q, T_KV, False), rows=rows,
-                                    q_rank=sb.q_rank if sb.q_rank is not None and sb.k_rank is sb.q_rank else None)
-    return outputs, dq, dk, dv, prob
+
+def _hash_backward_stage(st, d_out):
+    """dQ, dK, dV (fp32, boundary layout) for a _HashState and the output gradient."""
+    from ._kernel import dkdv_backward_sorted, dq_backward_gathered
+
+    d_out = as_operand(d_out)
+    prob, sb = st.prob, st.sb
+    if st.q_only is not None and _DO_WRITEOUT:
+        # dQ gathers Q / dO through the row table, fuses delta and writes dO back in
+        # bucket order for dK/dV: no separate delta / dO pass
+        xdo = torch.empty_like(st.xq)
+        dq, delta = dq_backward_gathered(prob, st.q, st.xk, st.xv, st.outputs, d_out, st.q_only, st.scale, st.T_Q,
+                                         xdo)
+        dk, dv = dkdv_backward_sorted(prob, st.xq, st.xk, st.xv, xdo, st.outputs._lse2, delta, st.scale, st.T_KV)
+        return dq, dk, dv
+    shared = sb.q_rank is not None and sb.k_rank is sb.q_rank
+    return attention_backward(prob, st.xq, st.xk, st.xv, st.outputs, d_out, st.scale,
+                              boundary=(st.T_Q, st.T_KV, False), rows=st.rows, q_rank=sb.q_rank if shared else None)
+
+
+def _fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, exclude_self=True, row_tables=False):
+    """The fused boundary-layout fwd + bwd; returns (FlashOutputs, dq, dk, dv, problem)."""
+    st = _hash_forward_stage(q, k, v, q_hash, k_hash, scale, exclude_self, row_tables)
+    dq, dk, dv = _hash_backward_stage(st, d_out)
+    return st.outputs, dq, dk, dv, st.prob
 
 
 @padded_call("fwd_bwd")
