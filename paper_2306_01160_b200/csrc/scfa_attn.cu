@@ -58,7 +58,9 @@ struct Cfg {
   // Backward ("ALT"): one stream per CTA whose tiles alternate between the two row
   // warpgroups (a tile's P / dS depend only on that tile), each with its own S / dP TMEM
   // buffer, so S(t+1) runs while P(t) is computed and both warpgroups work at once.
-  static constexpr bool ALT = (kMode == MODE_DKDV);  // measured: dK/dV gains, dQ loses (one MMA issuer paces it)
+  // measured: dK/dV gains; dQ loses at D = 64 (two streams beat one MMA issuer) but gains at
+  // D = 128, where TMEM holds only one dQ stream anyway
+  static constexpr bool ALT = (kMode == MODE_DKDV) || (kMode == MODE_DQ && kD == 128);
   static constexpr int NSTREAM = ALT ? 1 : ((kD == 64) ? 2 : 1);
   static constexpr int THREADS = 512;
   static constexpr int BM = 128;                             // stationary rows per work item
