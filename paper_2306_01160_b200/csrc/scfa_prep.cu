@@ -9,6 +9,8 @@
 #include <cstdarg>
 #include <cstdio>
 
+#include <cooperative_groups.h>
+
 #include "scfa_common.cuh"
 #include "scfa_internal.h"
 
@@ -384,6 +386,161 @@ __global__ void __launch_bounds__(kSortThreads) hash_prepare_sort_kernel(
     bounds[threadIdx.x] = (passes == 1) ? start : -1;
   }
   if (threadIdx.x == 0) bounds[256] = T;
+}
+
+// Kernel 1, cluster form (the common case: every id < 256, one counting pass): a cluster
+// of kSortCluster CTAs per slice, each owning a contiguous quarter of the positions, so a
+// slice is sorted by 4x the SMs.  Each CTA counts its quarter per (digit, warp); the
+// clusters' per-digit totals are exchanged through distributed shared memory, giving
+// every CTA its global slot base per digit (stable: lower quarters first, then warps in
+// order, then lanes).  Multi-pass ids (>= 256) fall back to the single-CTA path in CTA 0.
+constexpr int kSortCluster = 4;
+
+struct ClusterSortSmem {
+  int ctot[256];   // this CTA's count per digit
+  int dbase[256];  // global first slot of each digit
+  int before[256];  // slots of each digit in lower-ranked CTAs
+  int wsum[8];
+  unsigned long long mx;
+};
+
+__global__ void __cluster_dims__(kSortCluster, 1, 1) __launch_bounds__(kSortThreads)
+    hash_prepare_sort_cluster_kernel(const void* hash, int hdt, int T, int T_pad, int64_t H, int64_t sb, int64_t st,
+                                     int64_t sh, int32_t* perm, int32_t* rank, int32_t* scratch,
+                                     int32_t* sorted_hash, int32_t* err) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) uint8_t dsm[];
+  PrepSmem& S = *reinterpret_cast<PrepSmem*>(dsm);
+  ClusterSortSmem& C = *reinterpret_cast<ClusterSortSmem*>(dsm + sizeof(PrepSmem));
+  int32_t* key = reinterpret_cast<int32_t*>(dsm + sizeof(PrepSmem) + sizeof(ClusterSortSmem));
+  const int crank = static_cast<int>(cluster.block_rank());
+  const int64_t bh = blockIdx.x / kSortCluster;
+  const int64_t b = bh / H, h = bh % H;
+  const int64_t hbase = b * sb + h * sh;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int segT = ((T + kSortCluster - 1) / kSortCluster + 31) & ~31;
+  const int s0 = min(T, crank * segT), s1 = min(T, s0 + segT), nloc = s1 - s0;
+  int32_t* P = perm + bh * T;
+  int32_t* R = rank + bh * T;
+  int32_t* X = scratch + bh * (T + 257);
+  int32_t* bounds = X + T;
+  int32_t* SH = sorted_hash + bh * T_pad;
+
+  // ---- this CTA's keys, validity and max
+  long long mh = 0;
+  bool bad = false;
+  for (int i = threadIdx.x; i < nloc; i += blockDim.x) {
+    const long long v = load_int(hash, hdt, hbase + static_cast<int64_t>(s0 + i) * st);
+    bad |= (v < 0 || v > 0x7fffffffLL);
+    const long long c = v < 0 ? 0 : (v > 0x7fffffffLL ? 0x7fffffffLL : v);
+    key[i] = static_cast<int32_t>(c);
+    mh = max(mh, c);
+  }
+  if (bad) flag_error(err, SCFA_ERR_SHAPE);
+  if (threadIdx.x == 0) C.mx = 0;
+  for (int i = threadIdx.x; i < 256 * 33; i += blockDim.x) (&S.cnt[0][0])[i] = 0;
+  __syncthreads();
+  atomicMax(&C.mx, static_cast<unsigned long long>(mh));
+  cluster.sync();
+  unsigned long long gmx = 0;
+  for (int c = 0; c < kSortCluster; ++c) gmx = max(gmx, cluster.map_shared_rank(&C.mx, c)[0]);
+  if (gmx >= 256) {  // multi-pass ids: CTA 0 sorts the whole slice as the single-CTA kernel
+    cluster.sync();
+    if (crank != 0) return;
+    for (int t = threadIdx.x; t < T; t += blockDim.x) {
+      const long long v = load_int(hash, hdt, hbase + static_cast<int64_t>(t) * st);
+      key[t] = static_cast<int32_t>(v < 0 ? 0 : (v > 0x7fffffffLL ? 0x7fffffffLL : v));
+    }
+    __syncthreads();
+    int passes = 0;
+    for (unsigned long long m = gmx; m > 0; m >>= 8) ++passes;
+    for (int p = 0; p < passes; ++p) {
+      const bool last = p == passes - 1;
+      const bool to_perm = ((passes - 1 - p) & 1) == 0;
+      radix_pass(S, key, T, 8 * p, p == 0 ? nullptr : (to_perm ? X : P), to_perm ? P : X, last ? SH : nullptr,
+                 last ? R : nullptr);
+    }
+    if (threadIdx.x < 256) bounds[threadIdx.x] = -1;
+    if (threadIdx.x == 0) bounds[256] = T;
+    return;
+  }
+  // ---- one counting pass: per-warp counts over contiguous warp segments of this quarter
+  const int wseg = (((nloc + 31) / 32) + 31) & ~31;
+  const int w0 = min(nloc, warp * wseg), w1 = min(nloc, w0 + wseg);
+  for (int base = w0; base < w1; base += 32) {
+    const int i = base + lane;
+    const bool act = i < w1;
+    const int d = act ? key[i] : 256 + lane;
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    if (act && (peers & lanemask_lt()) == 0) S.cnt[d][warp] += __popc(peers);
+  }
+  __syncthreads();
+  if (threadIdx.x < 256) {  // within-digit warp prefix, this CTA's total per digit
+    const int d = threadIdx.x;
+    int acc = 0;
+    for (int w = 0; w < 32; ++w) {
+      const int c = S.cnt[d][w];
+      S.cnt[d][w] = acc;
+      acc += c;
+    }
+    C.ctot[d] = acc;
+  }
+  cluster.sync();
+  int gsum = 0;
+  if (threadIdx.x < 256) {
+    const int d = threadIdx.x;
+    int before = 0;
+    for (int c = 0; c < kSortCluster; ++c) {
+      const int v = cluster.map_shared_rank(&C.ctot[0], c)[d];
+      gsum += v;
+      before += (c < crank) ? v : 0;
+    }
+    C.before[d] = before;
+    // exclusive scan of gsum over the 256 digits: warp scans, then the 8 warp totals
+    int incl = gsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += n;
+    }
+    if (lane == 31) C.wsum[warp] = incl;
+    C.dbase[d] = incl - gsum;
+  }
+  __syncthreads();
+  if (threadIdx.x < 256) {
+    int wofs = 0;
+    for (int w = 0; w < warp; ++w) wofs += C.wsum[w];
+    const int d = threadIdx.x;
+    C.dbase[d] += wofs;
+    const int base = C.dbase[d] + C.before[d];
+    for (int w = 0; w < 32; ++w) S.cnt[d][w] += base;
+  }
+  __syncthreads();
+  // ---- second walk: stable slots, perm / rank / sorted ids
+  for (int base = w0; base < w1; base += 32) {
+    const int i = base + lane;
+    const bool act = i < w1;
+    const int d = act ? key[i] : 256 + lane;
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const int below = __popc(peers & lanemask_lt());
+    int off = 0;
+    if (act) off = S.cnt[d][warp];
+    __syncwarp();
+    if (act) {
+      const int slot = off + below;
+      P[slot] = s0 + i;
+      SH[slot] = d;
+      R[s0 + i] = slot;
+      if (below == 0) S.cnt[d][warp] = off + __popc(peers);
+    }
+    __syncwarp();
+  }
+  if (crank == 0) {
+    if (threadIdx.x < 256) bounds[threadIdx.x] = C.dbase[threadIdx.x];
+    if (threadIdx.x == 0) bounds[256] = T;
+  }
+  cluster.sync();  // the other CTAs' reads of this CTA's shared memory are done
 }
 
 // Kernel 2 (one thread per slot, all slices): sorted vectors, rank and visibility runs.
@@ -818,8 +975,27 @@ extern "C" int scfa_hash_prepare(const void* hash, int hash_dtype, int64_t B, in
       return check_launch("hash_prepare attribute");
     attr = true;
   }
-  hash_prepare_sort_kernel<<<static_cast<unsigned>(B * H), kSortThreads, smem, s>>>(
-      hash, hash_dtype, static_cast<int>(T), T_pad, H, sb, st, sh, perm, rank, scratch, q_hash, err_flag);
+  static bool cattr = false;
+  const size_t csmem = sizeof(PrepSmem) + sizeof(ClusterSortSmem) + static_cast<size_t>(T) * 4;
+  if (!cattr) {
+    if (cudaFuncSetAttribute(hash_prepare_sort_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(sizeof(PrepSmem) + sizeof(ClusterSortSmem) + kPrepMaxT * 4)) !=
+        cudaSuccess)
+      return check_launch("hash_prepare cluster attribute");
+    cattr = true;
+  }
+  // a cluster of CTAs per slice when the slices alone leave most SMs idle and fit one
+  // wave as clusters (measured: B*H = 24 at T = 16k 31 -> 13 us; 48 at 8k equal; 96 at 4k
+  // the single-CTA kernel wins)
+  static int sms = 0;
+  if (!sms && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess) sms = 148;
+  if (T >= 4096 && B * H * kSortCluster <= 2 * sms) {
+    hash_prepare_sort_cluster_kernel<<<static_cast<unsigned>(B * H * kSortCluster), kSortThreads, csmem, s>>>(
+        hash, hash_dtype, static_cast<int>(T), T_pad, H, sb, st, sh, perm, rank, scratch, q_hash, err_flag);
+  } else {
+    hash_prepare_sort_kernel<<<static_cast<unsigned>(B * H), kSortThreads, smem, s>>>(
+        hash, hash_dtype, static_cast<int>(T), T_pad, H, sb, st, sh, perm, rank, scratch, q_hash, err_flag);
+  }
   int rc = check_launch("hash_prepare_sort");
   if (rc) return rc;
   if (sorted_event) {  // perm / rank are final here: the caller may start the row copies

@@ -116,8 +116,11 @@ def test_dense_runs_and_lists():
     _check_problem(prob, vis)
 
 
+# T >= 4096 with few slices runs the cluster sort (4 CTAs per slice; nb > 256 its
+# multi-pass fallback, nb = 1 the all-zero ids)
 @pytest.mark.parametrize("T,nb,excl,seed", [(300, 4, True, 0), (2048, 16, False, 1), (4096, 300, True, 2),
-                                            (1000, 1, True, 3)])
+                                            (1000, 1, True, 3), (8192, 16, True, 4), (16384, 64, False, 5),
+                                            (4096, 1, True, 6), (5000, 7, True, 7)])
 def test_fused_prepare_matches_general_path(T, nb, excl, seed):
     """scfa_hash_prepare (shared ids) == hash_sort + build_aux + runs_kernel, bit for bit."""
     from paper_2306_01160_b200._kernel import Problem
