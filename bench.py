@@ -203,6 +203,57 @@ def measure_qk_cfg3(args, dev, barrier, max_over_ranks, T=16384, drop=0.5):
             "timing": "CUDA events, eager (QK prep reads the kept counts back once per call, qk_sparse.py:58)"}
 
 
+def measure_hash_t16k(args, dev, barrier, max_over_ranks, B=4, H=12, T=16384, D=64, nb=16):
+    """The north-star target shape for hash sparsity: fwd+bwd at T=16k with 16 buckets
+    (B=4 H=12 D=64, as cfg3), next to the dense causal comparator at the same shape;
+    CUDA-graph replay as the headline step (extra field of the bench line)."""
+    import torch
+
+    import paper_2306_01160_b200 as scfa
+    from paper_2306_01160_b200 import hash_sparse as hs
+
+    gen = torch.Generator(device=dev).manual_seed(17)
+    q, k, v, dO = (torch.randn((B, T, H, D), device=dev, generator=gen).to(torch.bfloat16) for _ in range(4))
+    ids = torch.randint(0, nb, (B, T, H), device=dev, generator=gen)
+    c = torch.nn.functional.one_hot(ids, nb).sum(1).to(torch.int64)
+    p_live = int((c * (c - 1) // 2).sum())
+    stream = torch.cuda.current_stream()
+
+    def graphed(fn):
+        fn()
+        side = torch.cuda.Stream()
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            fn()
+        stream.wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        for _ in range(args.warmup):
+            g.replay()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            g.replay()
+        e1.record(stream)
+        barrier()
+        return max_over_ranks(e0.elapsed_time(e1) / args.steps)
+
+    ms = graphed(lambda: hs._fwd_bwd(q, k, v, ids, ids, dO, exclude_self=True))
+    qe, ke, ve, de = (x.transpose(1, 2).contiguous() for x in (q, k, v, dO))
+
+    def dense():
+        o = scfa.flash_forward(qe, ke, ve)
+        scfa.flash_backward(qe, ke, ve, o, de)
+
+    dense_ms = graphed(dense)
+    return {"workload": f"hash-sparse SCFA fwd+bwd, B={B} H={H} T={T} D={D}, {nb} buckets (north-star target)",
+            "ms_per_step": ms, "effective_tflops": 14.0 * D * p_live / (ms * 1e-3) / 1e12, "p_live": p_live,
+            "dense_causal_ms": dense_ms, "speedup_vs_dense": dense_ms / ms,
+            "timing": "CUDA events over CUDA-graph replays, inputs resident"}
+
+
 # ---------------------------------------------------------------- GPU arm
 
 def run_ours(args, cfg):
@@ -361,6 +412,7 @@ def run_ours(args, cfg):
     del qe, ke, ve, de, o
 
     cfg3 = None if args.no_cfg3 else measure_qk_cfg3(args, dev, barrier, max_over_ranks)
+    t16k = None if args.no_cfg3 else measure_hash_t16k(args, dev, barrier, max_over_ranks)
 
     # end to end through the public API with host buffers: H2D inputs, D2H outputs + gradients
     outs_host = [torch.empty(r.shape, dtype=r.dtype, pin_memory=True) for r in res]
@@ -415,6 +467,8 @@ def run_ours(args, cfg):
     }
     if cfg3 is not None:
         line["cfg3_qk"] = cfg3
+    if t16k is not None:
+        line["hash_t16k"] = t16k
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(qkvd, buckets, cfg)
     if rank == 0:
