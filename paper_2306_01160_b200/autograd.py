@@ -39,20 +39,19 @@ class _HashSparseAttention(torch.autograd.Function):
 class _QkSparseAttention(torch.autograd.Function):
     @staticmethod
     def forward(ctx, q, k, v, q_keep, k_keep, scale):
-        from .qk_sparse import qk_preprocess
+        # the same stages as qk_sparse_attention_fwd_bwd
+        from .qk_sparse import _qk_forward_stage
 
-        prep = qk_preprocess(q, k, v, q_keep, k_keep)
-        prob = prep.problem
-        prob.schedule("fwd", "dq", "dkdv")
-        out = attention_forward(prob, prep.q_c, prep.k_c, prep.v_c, scale, boundary=(q.shape[1], True))
-        ctx.state = (prob, prep, out, scale, q.shape[1], k.shape[1], q.dtype, k.dtype, v.dtype)
-        return out.O.to(q.dtype)
+        st = _qk_forward_stage(q, k, v, q_keep, k_keep, scale)
+        ctx.state = (st, q.dtype, k.dtype, v.dtype)
+        return st.outputs.O.to(q.dtype)
 
     @staticmethod
     def backward(ctx, d_out):
-        prob, prep, out, scale, T_Q, T_KV, qt, kt, vt = ctx.state
-        dq, dk, dv = attention_backward(prob, prep.q_c, prep.k_c, prep.v_c, out, as_operand(d_out.contiguous()),
-                                        scale, boundary=(T_Q, T_KV, True))
+        from .qk_sparse import _qk_backward_stage
+
+        st, qt, kt, vt = ctx.state
+        dq, dk, dv = _qk_backward_stage(st, d_out.contiguous())
         ctx.state = None
         return dq.to(qt), dk.to(kt), dv.to(vt), None, None, None
 

@@ -20,6 +20,7 @@ import torch
 
 from . import _lib
 from ._kernel import (
+    RowTables,
     FlashOutputs,
     Problem,
     as_operand,
@@ -270,6 +271,64 @@ def qk_sparse_attention(q, k, v, q_keep, k_keep, scale=None, blocks=BlockSpec(),
                              boundary=(prep.T_Q, True)).O
 
 
+class _QkState:
+    """What the QK backward stage needs from the forward stage."""
+
+    __slots__ = ("prob", "prep", "q", "xq", "outputs", "rows", "q_only", "scale", "T_Q", "T_KV", "q_keep", "k_keep")
+
+
+def _qk_forward_stage(q, k, v, q_keep, k_keep, scale=None, row_tables=False):
+    """Preparation + forward of the boundary-layout QK path; returns a _QkState.
+
+    Default: only K / V are compacted up front; the forward reads Q through the row table
+    and writes the compacted Q back (as the hash path).  row_tables=True: every load goes
+    through the row tables.  Dropped rows of O are zeroed here (not zero-filled up front).
+    """
+    st = _QkState()
+    st.T_Q, st.T_KV, st.scale, st.q_keep, st.k_keep = q.shape[1], k.shape[1], scale, q_keep, k_keep
+    st.q_only, st.xq, st.rows = None, None, None
+    if row_tables:
+        st.prep, mode = qk_preprocess(q, k, v, q_keep, k_keep, materialize=False), "rows"
+    else:
+        st.prep, mode = qk_preprocess(q, k, v, q_keep, k_keep, materialize="kv"), "gathered"
+        if st.prep.problem.rows is None or st.prep.problem.T_q == 0:  # degenerate: every query dropped
+            st.prep, mode = qk_preprocess(q, k, v, q_keep, k_keep), "sorted"
+    st.prob = prob = st.prep.problem
+    prob.schedule("fwd", "dq", "dkdv")
+    st.q = as_operand(q)
+    if mode == "gathered":
+        st.q_only = RowTables(prob.rows.q_rows, None, prob.rows.R_q, prob.rows.R_kv)
+        st.xq = torch.empty((prob.B, prob.H, prob.T_q, prob.D), dtype=torch.bfloat16, device=st.q.device)
+        st.outputs = attention_forward(prob, st.q, st.prep.k_c, st.prep.v_c, scale, boundary=(st.T_Q, False),
+                                       rows=st.q_only, q_out=st.xq)
+    else:
+        st.rows = prob.rows if mode == "rows" else None
+        st.outputs = attention_forward(prob, st.prep.q_c, st.prep.k_c, st.prep.v_c, scale,
+                                       boundary=(st.T_Q, False), rows=st.rows)
+    _zero_dropped_rows(q_keep, st.outputs.O)
+    return st
+
+
+def _qk_backward_stage(st, d_out):
+    """dQ, dK, dV (fp32, boundary layout; dropped rows zero) for a _QkState."""
+    from ._kernel import dkdv_backward_sorted, dq_backward_gathered
+
+    prob, prep = st.prob, st.prep
+    d_b = as_operand(d_out)
+    if st.q_only is not None:
+        xdo = torch.empty_like(st.xq)
+        dq, delta = dq_backward_gathered(prob, st.q, prep.k_c, prep.v_c, st.outputs, d_b, st.q_only, st.scale,
+                                         st.T_Q, xdo)
+        dk, dv = dkdv_backward_sorted(prob, st.xq, prep.k_c, prep.v_c, xdo, st.outputs._lse2, delta, st.scale,
+                                      st.T_KV)
+    else:
+        dq, dk, dv = attention_backward(prob, prep.q_c, prep.k_c, prep.v_c, st.outputs, d_b, st.scale,
+                                        boundary=(st.T_Q, st.T_KV, False), rows=st.rows)
+    _zero_dropped_rows(st.q_keep, dq)
+    _zero_dropped(st.k_keep, dk, dv)
+    return dq, dk, dv
+
+
 @padded_call("fwd_bwd")
 def qk_sparse_attention_fwd_bwd(q, k, v, q_keep, k_keep, d_out, scale=None, row_tables=False):
     """Forward + backward through the whole QK path in boundary layout.
@@ -278,40 +337,16 @@ def qk_sparse_attention_fwd_bwd(q, k, v, q_keep, k_keep, d_out, scale=None, row_
     zero outputs and zero gradients.  The reference composes the same thing
     from qk_preprocess -> qk_forward_kernel -> qk_backward_kernel.
     """
-    prep = qk_preprocess(q, k, v, q_keep, k_keep, materialize=False if row_tables else "kv")
-    T_Q, T_KV = q.shape[1], k.shape[1]
-    prob = prep.problem
-    prob.schedule("fwd", "dq", "dkdv")
-    if not row_tables and prob.rows is not None and prob.T_q > 0:
-        # as the hash path: Q is read through the row table and written back compacted by
-        # the forward, dQ reads Q / dO the same way, fuses delta and writes dO back, and
-        # dK/dV streams both copies — only K / V are copied up front
-        from ._kernel import RowTables, dkdv_backward_sorted, dq_backward_gathered
+    st = _qk_forward_stage(q, k, v, q_keep, k_keep, scale, row_tables)
+    dq, dk, dv = _qk_backward_stage(st, d_out)
+    return st.outputs.O, dq, dk, dv
 
-        B, H, D = prob.B, prob.H, prob.D
-        q_b, d_b = as_operand(q), as_operand(d_out)
-        xq = torch.empty((B, H, prob.T_q, D), dtype=torch.bfloat16, device=q_b.device)
-        xdo = torch.empty_like(xq)
-        q_only = RowTables(prob.rows.q_rows, None, prob.rows.R_q, prob.rows.R_kv)
-        outputs = attention_forward(prob, q_b, prep.k_c, prep.v_c, scale, boundary=(T_Q, False), rows=q_only,
-                                    q_out=xq)
-        dq, delta = dq_backward_gathered(prob, q_b, prep.k_c, prep.v_c, outputs, d_b, q_only, scale, T_Q, xdo)
-        dk, dv = dkdv_backward_sorted(prob, xq, prep.k_c, prep.v_c, xdo, outputs._lse2, delta, scale, T_KV)
-        _zero_dropped(q_keep, outputs.O, dq)
-        _zero_dropped(k_keep, dk, dv)
-        return outputs.O, dq, dk, dv
-    if not row_tables:  # degenerate sizes: the materialised path
-        prep = qk_preprocess(q, k, v, q_keep, k_keep)
-        prob = prep.problem
-        prob.schedule("fwd", "dq", "dkdv")
-    rows = prob.rows if row_tables else None
-    # the kernels write every kept row; only the dropped rows are zeroed (no full fill)
-    outputs = attention_forward(prob, prep.q_c, prep.k_c, prep.v_c, scale, boundary=(T_Q, False), rows=rows)
-    dq, dk, dv = attention_backward(prob, prep.q_c, prep.k_c, prep.v_c, outputs, as_operand(d_out), scale,
-                                    boundary=(T_Q, T_KV, False), rows=rows)
-    _zero_dropped(q_keep, outputs.O, dq)
-    _zero_dropped(k_keep, dk, dv)
-    return outputs.O, dq, dk, dv
+
+def _zero_dropped_rows(keep, out):
+    B, T, H, D = out.shape
+    keep = torch.as_tensor(keep, device=out.device)
+    _lib.call("scfa_zero_dropped", _lib.ptr(keep), _lib.dtype_code(keep), B, T, H, *keep.stride(), _lib.ptr(out),
+              D * out.element_size(), None, 0, _lib.stream_ptr())
 
 
 def _zero_dropped(keep, out0, out1):
