@@ -190,3 +190,51 @@ def test_qk_fwd_bwd_tiny_and_ragged_lengths(T):
     got = scfa.qk_sparse_attention_fwd_bwd(_t(qb), _t(kb), _t(vb), qk, kk, _t(dO))
     for name, g, w in zip(("O", "dQ", "dK", "dV"), got, (O, dq, dk, dv)):
         _check(name, _np(g), eng(w))
+
+
+def _torch_masked_reference(q, k, v, dO, vis):
+    """fp32 torch attention + gradients for one head: q, k, v, dO (T, D); vis (T, T) bool."""
+    q, k, v = (x.float().requires_grad_() for x in (q, k, v))
+    s = (q @ k.T) / q.shape[-1] ** 0.5
+    s = s.masked_fill(~vis, float("-inf"))
+    p = torch.softmax(s, dim=-1).nan_to_num(0.0)
+    o = p @ v
+    o.backward(dO.float())
+    return o.detach(), q.grad, k.grad, v.grad
+
+
+def test_hash_full_cfg2_size_against_torch_fp32():
+    """BASELINE configs[1] at full size (B=4 H=12 T=8192 D=64, 16 buckets): the fused
+    fwd+bwd against an fp32 torch reference on a sample of heads (same bf16 inputs)."""
+    B, H, T, D, nb = 4, 12, 8192, 64, 16
+    g = torch.Generator(device="cuda").manual_seed(123)
+    q, k, v, dO = (torch.randn((B, T, H, D), device="cuda", generator=g).to(torch.bfloat16) for _ in range(4))
+    ids = torch.randint(0, nb, (B, T, H), device="cuda", generator=g)
+    o, dq, dk, dv = scfa.hash_sparse_attention_fwd_bwd(q, k, v, ids, ids, dO)
+    pos = torch.arange(T, device="cuda")
+    causal = pos[:, None] > pos[None, :]  # exclude_self
+    for b, h in ((0, 0), (1, 5), (3, 11)):
+        same = ids[b, :, h][:, None] == ids[b, :, h][None, :]
+        want = _torch_masked_reference(q[b, :, h], k[b, :, h], v[b, :, h], dO[b, :, h], causal & same)
+        for name, got, w in zip(("O", "dQ", "dK", "dV"), (o[b, :, h], dq[b, :, h], dk[b, :, h], dv[b, :, h]), want):
+            err = float((got.float() - w).abs().max())
+            assert err <= TOL, f"{name} (b={b}, h={h}): max-abs {err:.3e}"
+
+
+def test_qk_full_cfg3_size_against_torch_fp32():
+    """BASELINE configs[2] at full size (B=4 H=12 T=16384 D=64, half of the queries and keys
+    dropped): the fused fwd+bwd against an fp32 torch reference on a sample of heads."""
+    B, H, T, D = 4, 12, 16384, 64
+    g = torch.Generator(device="cuda").manual_seed(321)
+    q, k, v, dO = (torch.randn((B, T, H, D), device="cuda", generator=g).to(torch.bfloat16) for _ in range(4))
+    qk = torch.from_numpy(scfa.random_keep(B, T, H, 0.5, 6)).cuda()
+    kk = torch.from_numpy(scfa.random_keep(B, T, H, 0.5, 7)).cuda()
+    o, dq, dk, dv = scfa.qk_sparse_attention_fwd_bwd(q, k, v, qk, kk, dO)
+    pos = torch.arange(T, device="cuda")
+    causal = pos[:, None] >= pos[None, :]
+    for b, h in ((0, 3), (2, 9)):
+        vis = causal & (qk[b, :, h] > 0)[:, None] & (kk[b, :, h] > 0)[None, :]
+        want = _torch_masked_reference(q[b, :, h], k[b, :, h], v[b, :, h], dO[b, :, h], vis)
+        for name, got, w in zip(("O", "dQ", "dK", "dV"), (o[b, :, h], dq[b, :, h], dk[b, :, h], dv[b, :, h]), want):
+            err = float((got.float() - w).abs().max())
+            assert err <= TOL, f"{name} (b={b}, h={h}): max-abs {err:.3e}"
