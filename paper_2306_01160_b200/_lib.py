@@ -23,6 +23,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # SCFA_LIB overrides the path (A/B timing of two builds); the default is the in-tree build
 LIB_PATH = os.environ.get("SCFA_LIB") or os.path.join(_HERE, "lib", "libscfa_b200.so")
 
+ABI_VERSION = 4  # include/scfa_b200.h / scfa_abi_version()
 OK = 0
 ERR_SHAPE, ERR_FORMAT, ERR_PARAM, ERR_NUMERIC, ERR_CONTRACT, ERR_CUDA = 1, 2, 3, 4, 5, 6
 DT_F32, DT_F64, DT_U8, DT_I32, DT_I64, DT_BF16 = 0, 1, 2, 3, 4, 5
@@ -93,6 +94,8 @@ def load():
     lib.scfa_last_error.argtypes = []
     lib.scfa_abi_version.restype = ctypes.c_int
     lib.scfa_abi_version.argtypes = []
+    if lib.scfa_abi_version() != ABI_VERSION:  # a stale build: fail loudly, not with bad arguments
+        raise ScfaError(f"{LIB_PATH}: ABI {lib.scfa_abi_version()}, this package needs {ABI_VERSION} (rebuild it)")
     _lib = lib
     return lib
 

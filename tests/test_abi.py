@@ -51,3 +51,9 @@ def test_error_codes_map_to_reference_taxonomy():
         _lib.raise_for(_lib.ERR_SHAPE, "x")
     with pytest.raises(ContractError):
         _lib.raise_for(_lib.ERR_CONTRACT, "x")
+
+
+def test_abi_version_matches_the_package():
+    from paper_2306_01160_b200 import _lib
+
+    assert _lib.load().scfa_abi_version() == _lib.ABI_VERSION
