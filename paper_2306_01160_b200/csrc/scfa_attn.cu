@@ -50,6 +50,28 @@ namespace scfa {
 
 enum Mode : int { MODE_FWD = 0, MODE_DQ = 1, MODE_DKDV = 2 };
 
+#ifndef SCFA_TUNE_NS0_FWD
+#define SCFA_TUNE_NS0_FWD 2
+#endif
+#ifndef SCFA_TUNE_NS1_FWD
+#define SCFA_TUNE_NS1_FWD 3
+#endif
+#ifndef SCFA_TUNE_NS0_DQ
+#define SCFA_TUNE_NS0_DQ 3
+#endif
+#ifndef SCFA_TUNE_NS1_DQ
+#define SCFA_TUNE_NS1_DQ 2
+#endif
+#ifndef SCFA_TUNE_NS0_ALT
+#define SCFA_TUNE_NS0_ALT 6
+#endif
+#ifndef SCFA_TUNE_NS1_ALT
+#define SCFA_TUNE_NS1_ALT 5
+#endif
+#ifndef SCFA_TUNE_QE
+#define SCFA_TUNE_QE 3
+#endif
+
 template <int kMode, int kD>
 struct Cfg {
   // One CTA per SM runs NSTREAM independent item streams (two at D = 64: each has its
@@ -77,8 +99,15 @@ struct Cfg {
   // accumulate MMAs: K feeds only S in the forward, V feeds only dP in dQ.
   static constexpr bool Y0_EARLY = (kMode == MODE_FWD);
   static constexpr bool Y1_EARLY = (kMode == MODE_DQ);
-  static constexpr int NS0 = (kMode == MODE_FWD) ? 2 : ((ALT && kD == 64) ? 6 : 3);
-  static constexpr int NS1 = (kMode == MODE_FWD) ? ((kD == 64) ? 3 : 2) : ((ALT && kD == 64) ? 5 : 2);
+  // ring depths (SCFA_TUNE_* build-time overrides for tuning sweeps, scripts/tune.py)
+  static constexpr int NS0 = (kMode == MODE_FWD)   ? ((kD == 64) ? SCFA_TUNE_NS0_FWD : 2)
+                             : (ALT && kD == 64)   ? SCFA_TUNE_NS0_ALT
+                             : (kMode == MODE_DQ && kD == 64) ? SCFA_TUNE_NS0_DQ
+                                                   : 3;
+  static constexpr int NS1 = (kMode == MODE_FWD)   ? ((kD == 64) ? SCFA_TUNE_NS1_FWD : 2)
+                             : (ALT && kD == 64)   ? SCFA_TUNE_NS1_ALT
+                             : (kMode == MODE_DQ && kD == 64) ? SCFA_TUNE_NS1_DQ
+                                                   : 2;
   // TMEM (per stream)
   static constexpr int TM_COLS = 512;  // allocated once per CTA
   static constexpr int TM_STREAM = TM_COLS / NSTREAM;
@@ -121,7 +150,7 @@ struct Cfg {
   // epilogue queues, one per TMEM lane quadrant (row warp q of either stream -> epilogue
   // warp q), entries taken in ticket order: per quadrant eq_full[QE], eq_empty[QE], a
   // ticket, entries {int4 info, float inv_l[32]}
-  static constexpr int QE = 3;
+  static constexpr int QE = SCFA_TUNE_QE;
   static constexpr int OFF_EQ = OFF_CTRL + NSTREAM * CTRL_BYTES;
   static constexpr int EQ_ENTRY = 16 + 4 * 32;
   static constexpr int EQQ_BYTES = 16 * QE + 16 + QE * EQ_ENTRY;  // one quadrant
