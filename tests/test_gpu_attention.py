@@ -115,6 +115,26 @@ def test_hash_host_streaming_matches_device():
         assert torch.equal(a, b.cpu())
 
 
+@pytest.mark.parametrize("D,pinned", [(48, True), (64, False)])
+def test_hash_host_streaming_out_buffers(D, pinned):
+    """Host inputs with caller-given result buffers (`out=`, the bench's e2e call), padded
+    head dims and pageable memory: the same bits as the device call, in the caller's buffers."""
+    B, H, T, nb = 2, 3, 520, 4
+    rng = np.random.default_rng(22)
+    x = [torch.from_numpy(rng.standard_normal((B, T, H, D)).astype(np.float32)).to(torch.bfloat16) for _ in range(4)]
+    h = torch.from_numpy(scfa.random_buckets(B, T, H, nb, 4))
+    dev = [t.cuda() for t in x]
+    want = scfa.hash_sparse_attention_fwd_bwd(dev[0], dev[1], dev[2], h.cuda(), h.cuda(), dev[3])
+    host = [t.pin_memory() for t in x] if pinned else x
+    out = [torch.full(w.shape, float("nan"), dtype=w.dtype, pin_memory=pinned) for w in want]
+    got = scfa.hash_sparse_attention_fwd_bwd(host[0], host[1], host[2], h, h, host[3], out=out)
+    torch.cuda.synchronize()
+    for a, o, b in zip(got, out, want):
+        assert a.data_ptr() == o.data_ptr()
+        assert a.shape == (B, T, H, D)
+        assert torch.equal(a, b.cpu())
+
+
 @pytest.mark.parametrize("mode", ["hash", "qk"])
 def test_autograd_matches_fused_fwd_bwd(mode):
     """dynamic_sparse_attention under autograd: same O and gradients as the *_fwd_bwd calls."""
