@@ -256,6 +256,30 @@ def measure_hash_t16k(args, dev, barrier, max_over_ranks, B=4, H=12, T=16384, D=
 
 # ---------------------------------------------------------------- GPU arm
 
+def gpu_local_cpus(index):
+    """Pin this process to the CPUs NVML reports as local to GPU `index` (the host buffers
+    of the end-to-end leg are then allocated on the GPU's NUMA node: device<->host copies
+    do not cross the socket link).  Returns (previous affinity, local CPU count) or None."""
+    try:
+        import pynvml
+
+        pynvml.nvmlInit()
+        try:
+            h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        finally:
+            pynvml.nvmlShutdown()
+        cpus = {64 * w + b for w, m in enumerate(words) for b in range(64) if (int(m) >> b) & 1}
+        prev = os.sched_getaffinity(0)
+        cpus &= prev
+        if not cpus or cpus == prev:
+            return None
+        os.sched_setaffinity(0, cpus)
+        return prev, len(cpus)
+    except Exception:
+        return None
+
+
 def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
@@ -273,6 +297,9 @@ def run_ours(args, cfg):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     _lib.require_cuda()
+    visible = (os.environ.get("CUDA_VISIBLE_DEVICES") or "").split(",")
+    nvml_index = int(visible[local]) if local < len(visible) and visible[local].strip().isdigit() else local
+    affinity = gpu_local_cpus(nvml_index)
 
     qkvd, buckets = make_inputs(cfg)
     B, H, T, D = cfg["B"], cfg["H"], cfg["T"], cfg["D"]
@@ -453,6 +480,7 @@ def run_ours(args, cfg):
                    "exclude_self": cfg["exclude_self"], "global_batch": B * world,
                    "parallelism": f"(b,h)-sharded, 1 batch per rank x{world}",
                    "l2": "inputs > L2 (q,k,v,dO 4 x 48 MiB bf16 + sorted copies), no flush",
+                   "host_affinity": f"{affinity[1]} GPU-local CPUs" if affinity else "unchanged",
                    "p_live_per_rank": p_live},
         "e2e": {"value": world * flops_step / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
@@ -470,6 +498,8 @@ def run_ours(args, cfg):
     if t16k is not None:
         line["hash_t16k"] = t16k
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        if affinity is not None:
+            os.sched_setaffinity(0, affinity[0])  # the CPU baseline gets every core again
         line["cpu_baseline"] = cpu_baseline(qkvd, buckets, cfg)
     if rank == 0:
         print(json.dumps(line), flush=True)
