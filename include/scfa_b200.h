@@ -238,13 +238,17 @@ int scfa_ref_schedule(const int32_t* q_idx, const int32_t* q_hash, const int32_t
  * operands are then loaded with TMA tile::gather4: no compacted / sorted copies exist.
  * ABI 4: q_out (optional, needs q_rows) receives the gathered Q rows in kernel order as a
  * (B*H, T_q, D) bf16 tensor — each stationary tile is stored back with a TMA store once
- * loaded — so the backward passes can stream a sorted Q without a separate copy pass.  */
+ * loaded — so the backward passes can stream a sorted Q without a separate copy pass.
+ * ABI 5: err_flag (optional, int32 device word) is set to SCFA_ERR_NUMERIC when a row's
+ * output or softmax denominator is non-finite — the reference raises NumericError when o
+ * turns non-finite inside update_stats (softmax.py:63-64).  First error code wins.     */
 int scfa_attn_fwd(const void* q, const void* k, const void* v, int64_t BH, int64_t T_q,
                   int64_t T_kv, int64_t D, const int32_t* q_idx, const int32_t* q_runs,
                   int64_t Tq_pad, int64_t Tkv_pad, const uint16_t* list, const int32_t* list_count,
                   int64_t list_stride, float scale, int64_t H, int64_t T_out, int out_boundary,
                   void* o, float* m, float* l, float* lse2, const int32_t* q_rows,
-                  const int32_t* k_rows, int64_t R_q, int64_t R_kv, void* q_out, void* stream);
+                  const int32_t* k_rows, int64_t R_q, int64_t R_kv, void* q_out, int32_t* err_flag,
+                  void* stream);
 
 /* delta = rowsum(dO * O) (qk_sparse.py:168, hash_sparse.py:194, dense.py:81);
  * lse2 rebuilt from (M, L) when lse2_in is NULL (m_hat/inv_l, _kernel.py:152-154).

@@ -237,7 +237,25 @@ class RowTables:
 _NO_ROWS = [None, None, 0, 0]
 
 
-def attention_forward(problem, q, k, v, scale=None, blocks=None, boundary=None, rows=None, q_out=None):
+def check_status(err, what="attention"):
+    """Raise the reference error class for a device status word (int32, 0 = ok).
+
+    The engine's kernels report data-dependent failures through one device word instead
+    of aborting: SCFA_ERR_SHAPE for bad bucket ids / keep entries (hash_sparse.py:112-113,
+    qk_sparse.py:54-55), SCFA_ERR_NUMERIC for a non-finite output (softmax.py:63-64).
+    Reading it synchronises with the stream, so the public calls read it once, after
+    every launch of the call is queued."""
+    if err is None:
+        return
+    code = int(err.item())
+    if code:
+        msgs = {_lib.ERR_SHAPE: "bucket ids must be non-negative (and < 2**31)",
+                _lib.ERR_NUMERIC: "non-finite values in attention output (update_stats, softmax.py:63-64)"}
+        _lib.raise_for_status(code, msgs.get(code, what))
+
+
+def attention_forward(problem, q, k, v, scale=None, blocks=None, boundary=None, rows=None, q_out=None, err=None,
+                      check=False):
     """Launch the forward kernel over the exact tile list; returns FlashOutputs.
 
     boundary=None: O is engine layout (B, H, T_q, D) in kernel (sorted/compacted) order.
@@ -248,6 +266,8 @@ def attention_forward(problem, q, k, v, scale=None, blocks=None, boundary=None, 
     through the row tables (no sorted copies); requires boundary.  With rows.k_rows None
     the keys / values are kernel-order copies (tiled loads) and only Q is gathered;
     q_out (B, H, T_q, D) bf16 then receives the gathered Q in kernel order.
+    err: int32 device status word the kernel flags SCFA_ERR_NUMERIC in; check=True reads
+    it after the launch and raises NumericError (reference update_stats, softmax.py:63-64).
     """
     if rows is not None:
         B, T_in, H, D = q.shape
@@ -266,6 +286,8 @@ def attention_forward(problem, q, k, v, scale=None, blocks=None, boundary=None, 
     M = torch.empty((B, H, T_q), dtype=torch.float32, device=dev)
     L = torch.empty((B, H, T_q), dtype=torch.float32, device=dev)
     lse2 = torch.empty((B * H, pad128(T_q)), dtype=torch.float32, device=dev)
+    if check and err is None:
+        err = torch.zeros(1, dtype=torch.int32, device=dev)
     if B * H > 0 and T_q > 0:
         sched = problem.schedule("fwd")
         lst, cnt, stride = sched["fwd"]
@@ -275,10 +297,12 @@ def attention_forward(problem, q, k, v, scale=None, blocks=None, boundary=None, 
             _lib.ptr(problem.q_idx), _lib.ptr(sched["q_runs"]), problem.Tq_pad, problem.Tkv_pad,
             _lib.ptr(lst), _lib.ptr(cnt), stride, _scale(scale, D), H, T_out, out_b,
             _lib.ptr(O), _lib.ptr(M), _lib.ptr(L), _lib.ptr(lse2),
-            *(rows.args() if rows is not None else _NO_ROWS), _lib.ptr(q_out), _lib.stream_ptr(),
+            *(rows.args() if rows is not None else _NO_ROWS), _lib.ptr(q_out), _lib.ptr(err), _lib.stream_ptr(),
         )
     out = FlashOutputs(O, M, L, problem=problem, blocks=blocks, lse2=lse2)
     out._boundary = boundary
+    if check:
+        check_status(err)
     return out
 
 

@@ -23,7 +23,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # SCFA_LIB overrides the path (A/B timing of two builds); the default is the in-tree build
 LIB_PATH = os.environ.get("SCFA_LIB") or os.path.join(_HERE, "lib", "libscfa_b200.so")
 
-ABI_VERSION = 4  # include/scfa_b200.h / scfa_abi_version()
+ABI_VERSION = 5  # include/scfa_b200.h / scfa_abi_version()
 OK = 0
 ERR_SHAPE, ERR_FORMAT, ERR_PARAM, ERR_NUMERIC, ERR_CONTRACT, ERR_CUDA = 1, 2, 3, 4, 5, 6
 DT_F32, DT_F64, DT_U8, DT_I32, DT_I64, DT_BF16 = 0, 1, 2, 3, 4, 5
@@ -60,7 +60,7 @@ _SIGS = {
     "scfa_ref_schedule": [_P, _P, _P, _P, _L, _L, _L, _L, _L, _L, _L, _I, _P, _P, _P, _P],
     "scfa_lsh_buckets": [_P, _I, _L, _L, _L, _L, _L, _L, _L, _L, _P, _I, _P, _L, _L, _L, _P],
     "scfa_attn_fwd": [_P, _P, _P, _L, _L, _L, _L, _P, _P, _L, _L, _P, _P, _L, _F, _L, _L, _I, _P, _P, _P, _P,
-                      _P, _P, _L, _L, _P, _P],
+                      _P, _P, _L, _L, _P, _P, _P],
     "scfa_zero_dropped": [_P, _I, _L, _L, _L, _L, _L, _L, _P, _L, _P, _L, _P],
     "scfa_bwd_prep_rank": [_P, _P, _L, _L, _L, _L, _L, _P, _P, _P, _P],
     "scfa_bwd_prep": [_P, _P, _P, _P, _P, _L, _L, _L, _L, _P, _L, _L, _P, _P, _P, _P],
@@ -112,6 +112,14 @@ def raise_for(code, what=""):
     if cls is None:
         raise ScfaError(f"{what}: CUDA engine failure: {msg}")
     raise cls(f"{what}: {msg}" if what else msg)
+
+
+def raise_for_status(code, msg):
+    """A device status word (SCFA_ERR_*) -> the reference exception class."""
+    cls = _ERRORS.get(code)
+    if cls is None:
+        raise ScfaError(f"engine status {code}: {msg}")
+    raise cls(msg)
 
 
 # kernels launched per successful call (for launch accounting in bench.py)

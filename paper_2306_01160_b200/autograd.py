@@ -10,7 +10,7 @@ epilogues write each gradient row straight back to its original position.
 
 import torch
 
-from ._kernel import as_operand, attention_backward, attention_forward
+from ._kernel import as_operand, attention_backward, attention_forward, check_status
 from ._headdim import padded_call
 
 __all__ = ["dense_causal_attention_autograd", "hash_sparse_attention_autograd", "qk_sparse_attention_autograd"]
@@ -22,7 +22,9 @@ class _HashSparseAttention(torch.autograd.Function):
         # the same stages as hash_sparse_attention_fwd_bwd (copy-free bucket order for Q / dO)
         from .hash_sparse import _hash_forward_stage
 
-        st = _hash_forward_stage(q, k, v, q_hash, k_hash, scale, exclude_self, check=check)
+        st = _hash_forward_stage(q, k, v, q_hash, k_hash, scale, exclude_self)
+        if check:  # bucket ids (hash_sparse.py:112-113) and a non-finite output (softmax.py:63-64)
+            check_status(st.err)
         ctx.state = (st, q.dtype, k.dtype, v.dtype)
         return st.outputs.O.to(q.dtype)
 
@@ -60,8 +62,9 @@ class _QkSparseAttention(torch.autograd.Function):
 def hash_sparse_attention_autograd(q, k, v, q_hash, k_hash, scale=None, exclude_self=True, check=True):
     """hash_sparse_attention (hash_sparse.py:223-238) with gradients w.r.t. q, k, v.
 
-    check=False skips the bucket-id validation read-back (one host sync per call) for
-    callers whose ids are valid by construction, e.g. an argmax over LSH projections.
+    check=False skips the status read-back (one host sync per call: bucket ids, non-finite
+    output) for callers whose ids are valid by construction, e.g. an argmax over LSH
+    projections.
     """
     return _HashSparseAttention.apply(q, k, v, q_hash, k_hash, scale, exclude_self, check)
 

@@ -189,6 +189,7 @@ struct AttnArgs {
   float* out_lse2;       // FWD
   float scale_log2;
   float scale;
+  int* err_flag;  // FWD: SCFA_ERR_NUMERIC on a non-finite output (update_stats, softmax.py:63-64)
   long long* dbg;  // optional per-tile timestamps (diagnostics)
   int dbg_tiles;
 };
@@ -434,6 +435,7 @@ SCFA_DEVICE void epilogue_wg(const AttnArgs& args, uint8_t* smem_base, uint32_t 
       tc_fence_after();
       if (kMode == MODE_FWD) {
         constexpr int RB = kD * 2;  // bf16 output row
+        bool finite_ok = true;
 #pragma unroll
         for (int c = 0; c < kD; c += 32) {
           uint32_t v[32];
@@ -441,13 +443,19 @@ SCFA_DEVICE void epilogue_wg(const AttnArgs& args, uint8_t* smem_base, uint32_t 
           tmem_wait_ld();
           uint32_t w[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            w[i] = pack_bf16(__uint_as_float(v[2 * i]) * inv_l, __uint_as_float(v[2 * i + 1]) * inv_l);
+          for (int i = 0; i < 16; ++i) {
+            const float o0 = __uint_as_float(v[2 * i]) * inv_l, o1 = __uint_as_float(v[2 * i + 1]) * inv_l;
+            finite_ok &= (fabsf(o0) <= FLT_MAX) & (fabsf(o1) <= FLT_MAX);
+            w[i] = pack_bf16(o0, o1);
+          }
 #pragma unroll
           for (int i = 0; i < 4; ++i) stage_put<RB>(stage, r, c / 8 + i, w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
         }
         tc_fence_before();
         mbar_arrive(B.o_free);
+        // the reference raises NumericError when o turns non-finite (softmax.py:63-64)
+        if (__any_sync(0xffffffffu, live && !finite_ok) && args.err_flag && lane == 0)
+          atomicCAS(args.err_flag, 0, SCFA_ERR_NUMERIC);
         stage_copy_out<RB>(stage, warp & 3, lane, reinterpret_cast<uint8_t*>(args.out_o), static_cast<long long>(orow) * RB,
                            live);
       } else if (kMode == MODE_DQ) {
@@ -1095,6 +1103,7 @@ __global__ void __launch_bounds__(512, 1)
           const size_t so = static_cast<size_t>(bh) * args.T_rows + row;
           const float LN2 = 0.6931471805599453f;
           const bool dead = !(l_run > 0.f);
+          if (!(l_run <= FLT_MAX) && args.err_flag) atomicCAS(args.err_flag, 0, SCFA_ERR_NUMERIC);  // inf / NaN
           const float m_use = (m_run == NEG_INF) ? 0.f : m_run;
           args.out0[so] = dead ? NEG_INF : m_true * LN2;             // M
           args.out1[so] = dead ? 0.f : l_run * ex2(m_use - m_true);  // L relative to M
@@ -1363,6 +1372,7 @@ static int launch_mode(const AttnLaunch& L, cudaStream_t stream) {
   a.out_lse2 = L.out_lse2;
   a.scale_log2 = L.scale * 1.4426950408889634f;
   a.scale = L.scale;
+  a.err_flag = L.err_flag;
   a.dbg = g_dbg_buf;
   a.dbg_tiles = g_dbg_tiles;
   auto kern = scfa_attn_kernel<kMode, kD>;

@@ -92,7 +92,7 @@ static int check_attn_args(int64_t BH, int64_t T_q, int64_t T_kv, int64_t D, int
 
 using namespace scfa;
 
-extern "C" int scfa_abi_version(void) { return 4; }
+extern "C" int scfa_abi_version(void) { return 5; }
 
 extern "C" const char* scfa_last_error(void) { return g_err; }
 
@@ -101,7 +101,7 @@ extern "C" int scfa_attn_fwd(const void* q, const void* k, const void* v, int64_
                              const uint16_t* list, const int32_t* list_count, int64_t list_stride, float scale,
                              int64_t H, int64_t T_out, int out_boundary, void* o, float* m, float* l, float* lse2,
                              const int32_t* q_rows, const int32_t* k_rows, int64_t R_q, int64_t R_kv, void* q_out,
-                             void* stream) {
+                             int32_t* err_flag, void* stream) {
   int rc = check_attn_args(BH, T_q, T_kv, D, Tq_pad, Tkv_pad, q, k, v);
   if (rc) return rc;
   if (BH == 0 || T_q == 0) return SCFA_OK;
@@ -112,6 +112,7 @@ extern "C" int scfa_attn_fwd(const void* q, const void* k, const void* v, int64_
   AttnLaunch L{};
   L.mode = 0;
   L.x_out = q_out;
+  L.err_flag = err_flag;
   L.D = static_cast<int>(D);
   L.BH = static_cast<int>(BH);
   L.H = static_cast<int>(H);

@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cfloat>
+
 #ifndef SCFA_DEVICE
 #define SCFA_DEVICE __device__ __forceinline__
 #endif

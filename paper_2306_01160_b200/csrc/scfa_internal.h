@@ -48,6 +48,7 @@ struct AttnLaunch {
   float* out1;
   float* out_lse2;
   float scale;
+  int32_t* err_flag;  // FWD: SCFA_ERR_NUMERIC when an output row or its l is non-finite (softmax.py:63-64)
 };
 
 int launch_attention(const AttnLaunch& L, cudaStream_t stream);

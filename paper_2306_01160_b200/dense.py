@@ -53,7 +53,7 @@ def flash_forward(q, k, v, blocks=BlockSpec(), scale=None, workers=None):
     B, H, T, D = q.shape
     if T != k.shape[2]:
         raise ShapeError("dense causal attention requires T_Q == T_KV")
-    return attention_forward(causal_problem(B, H, T, D, q.device), q, k, v, scale, blocks)
+    return attention_forward(causal_problem(B, H, T, D, q.device), q, k, v, scale, blocks, check=True)
 
 
 @padded_call("flash_bwd")

@@ -23,6 +23,7 @@ from ._kernel import (
     attention_backward,
     attention_forward,
     check_forward_operands,
+    check_status,
     pack_index,
 )
 from .errors import NumericError, ParameterError, ShapeError
@@ -242,7 +243,7 @@ def _prepare_shared(hash_t, sb, st, sh, B, H, T, D, err, exclude_self, sorted_ev
 
 
 def _sort_batch(q, k, v, q_hash, k_hash, layout, q_pos=None, k_pos=None, check=True, exclude_self=True,
-                materialize=True, sorted_event=None):
+                materialize=True, sorted_event=None, err=None):
     """Shared by sort_by_bucket (engine layout) and hash_sparse_attention (boundary layout).
 
     materialize=False (boundary layout only): no sorted copies of q / k / v; the
@@ -267,7 +268,8 @@ def _sort_batch(q, k, v, q_hash, k_hash, layout, q_pos=None, k_pos=None, check=T
         kh, ksb, kst, ksh = qh, qsb, qst, qsh
     else:
         kh, ksb, kst, ksh = _hash_view(torch.as_tensor(k_hash, device=dev), B, H, T_KV, hl)
-    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    if err is None:
+        err = torch.zeros(1, dtype=torch.int32, device=dev)
     if same and 0 < T_Q <= _PREP_MAX_T:
         q_perm, q_rank, problem = _prepare_shared(qh, qsb, qst, qsh, B, H, T_Q, D, err, exclude_self, sorted_event)
         k_perm, k_rank = q_perm, q_rank
@@ -320,9 +322,19 @@ def sort_by_bucket(q, k, v, q_hash, k_hash, q_idx=None, k_idx=None):
     return _sort_batch(q, k, v, q_hash, k_hash, "bhtd", qp, kp)
 
 
+def _own_views(sb, prob):
+    """Whether the batch's index / bucket vectors are still the ones its cached Problem was
+    built from (a caller may replace them, e.g. dataclasses.replace(sb, q_hash=...))."""
+    pairs = ((sb.q_idx, prob.q_idx), (sb.k_idx, prob.k_idx), (sb.q_hash, prob.q_hash), (sb.k_hash, prob.k_hash))
+    return all(isinstance(a, torch.Tensor) and b is not None and a.is_cuda and a.dtype == torch.int32
+               and a.data_ptr() == b.data_ptr() for a, b in pairs)
+
+
 def _problem_of(sb, exclude_self, validate=True):
     flags = _lib.FLAG_HASH | (_lib.FLAG_EXCLUDE_SELF if exclude_self else 0)
     prob = sb.problem
+    if prob is not None and not _own_views(sb, prob):
+        prob = None  # rebuilt from the batch and validated (_check_sorted, hash_sparse.py:136-142)
     if prob is not None and prob.rows is not None:  # operands stayed in (B, T, H, D)
         B, H, T_Q, D = prob.B, prob.H, prob.T_q, prob.D
         T_KV = prob.T_kv
@@ -354,7 +366,7 @@ def hash_forward_kernel(sorted_batch, scale=None, blocks=BlockSpec(), exclude_se
     sb.q, sb.k, sb.v = as_operand(sb.q), as_operand(sb.k), as_operand(sb.v)
     check_forward_operands(sb.q, sb.k, sb.v)
     prob = _problem_of(sb, exclude_self)
-    return attention_forward(prob, sb.q, sb.k, sb.v, scale, blocks)
+    return attention_forward(prob, sb.q, sb.k, sb.v, scale, blocks, check=True)
 
 
 @padded_call("hash_bwd")
@@ -367,7 +379,7 @@ def hash_backward_kernel(sorted_batch, outputs, d_out_sorted, scale=None, blocks
         raise ShapeError(f"dO shape {tuple(d_out_sorted.shape)} != {tuple(sb.q.shape)}")
     prob = getattr(outputs, "_problem", None)
     want = _lib.FLAG_HASH | (_lib.FLAG_EXCLUDE_SELF if exclude_self else 0)
-    if prob is None or prob.flags != want or prob.T_q != sb.q.shape[2]:
+    if prob is None or prob.flags != want or prob.T_q != sb.q.shape[2] or not _own_views(sb, prob):
         prob = _problem_of(sb, exclude_self)
     return attention_backward(prob, as_operand(sb.q), as_operand(sb.k), as_operand(sb.v), outputs, d_out_sorted,
                               scale)
@@ -397,16 +409,16 @@ def hash_sparse_attention(q, k, v, q_hash, k_hash, scale=None, blocks=BlockSpec(
     q, k, v = as_operand(q), as_operand(k), as_operand(v)
     sb = _sort_batch(q, k, v, q_hash, k_hash, "bthd", exclude_self=exclude_self)
     prob = _problem_of(sb, exclude_self)
-    return attention_forward(prob, sb.q, sb.k, sb.v, scale, blocks, boundary=(q.shape[1], False)).O
+    return attention_forward(prob, sb.q, sb.k, sb.v, scale, blocks, boundary=(q.shape[1], False), check=True).O
 
 
 class _HashState:
     """What the backward stage needs from the forward stage."""
 
-    __slots__ = ("prob", "sb", "q", "xq", "xk", "xv", "outputs", "rows", "q_only", "scale", "T_Q", "T_KV")
+    __slots__ = ("prob", "sb", "q", "xq", "xk", "xv", "outputs", "rows", "q_only", "scale", "T_Q", "T_KV", "err")
 
 
-def _hash_forward_stage(q, k, v, q_hash, k_hash, scale=None, exclude_self=True, row_tables=False, check=False):
+def _hash_forward_stage(q, k, v, q_hash, k_hash, scale=None, exclude_self=True, row_tables=False):
     """Preparation + forward of the boundary-layout hash path; returns a _HashState.
 
     Default (shared ids): Q / K / V are put in bucket order without copy passes for Q:
@@ -416,20 +428,24 @@ def _hash_forward_stage(q, k, v, q_hash, k_hash, scale=None, exclude_self=True, 
     bucket-order Q copy back with TMA stores.  Separate query / key ids: Q / K / V are
     copied (tiled loads everywhere).  row_tables=True: every load goes through the row
     tables (no copies at all; tile::gather4 sustains only ~1.6 TB/s, scripts/gather_bw.cu).
+    Nothing here synchronises with the host: bad bucket ids (sort kernels) and non-finite
+    outputs (forward) are flagged in the device word st.err, which the caller reads once
+    its launches are queued (check_status).
     """
     q, k, v = as_operand(q), as_operand(k), as_operand(v)
     sorted_ev = torch.cuda.Event() if not row_tables else None
-    sb = _sort_batch(q, k, v, q_hash, k_hash, "bthd", check=check, exclude_self=exclude_self, materialize=False,
-                     sorted_event=sorted_ev)
+    err = torch.zeros(1, dtype=torch.int32, device=q.device)
+    sb = _sort_batch(q, k, v, q_hash, k_hash, "bthd", check=False, exclude_self=exclude_self, materialize=False,
+                     sorted_event=sorted_ev, err=err)
     prob = _problem_of(sb, exclude_self)
     st = _HashState()
     st.prob, st.sb, st.q, st.scale = prob, sb, q, scale
     st.T_Q, st.T_KV = q.shape[1], k.shape[1]
-    st.rows, st.q_only = (prob.rows if row_tables else None), None
+    st.rows, st.q_only, st.err = (prob.rows if row_tables else None), None, err
     if row_tables:
         st.xq, st.xk, st.xv = q, k, v
         prob.schedule("fwd", "dq", "dkdv")  # runs + all three tile lists in one pass
-        st.outputs = attention_forward(prob, q, k, v, scale, boundary=(st.T_Q, False), rows=st.rows)
+        st.outputs = attention_forward(prob, q, k, v, scale, boundary=(st.T_Q, False), rows=st.rows, err=err)
         return st
     main = torch.cuda.current_stream(q.device)
     side = _copy_streams(q.device)[2]
@@ -456,9 +472,10 @@ def _hash_forward_stage(q, k, v, q_hash, k_hash, scale=None, exclude_self=True, 
         B, H, D = q.shape[0], q.shape[2], q.shape[3]
         xq = torch.empty((B, H, st.T_Q, D), dtype=torch.bfloat16, device=q.device)
         st.q_only = RowTables(prob.rows.q_rows, None, prob.rows.R_q, prob.rows.R_kv)
-        st.outputs = attention_forward(prob, q, xk, xv, scale, boundary=(st.T_Q, False), rows=st.q_only, q_out=xq)
+        st.outputs = attention_forward(prob, q, xk, xv, scale, boundary=(st.T_Q, False), rows=st.q_only, q_out=xq,
+                                       err=err)
     else:
-        st.outputs = attention_forward(prob, xq, xk, xv, scale, boundary=(st.T_Q, False))
+        st.outputs = attention_forward(prob, xq, xk, xv, scale, boundary=(st.T_Q, False), err=err)
     st.xq, st.xk, st.xv = xq, xk, xv
     return st
 
@@ -469,6 +486,8 @@ def _hash_backward_stage(st, d_out):
 
     d_out = as_operand(d_out)
     prob, sb = st.prob, st.sb
+    if tuple(d_out.shape) != tuple(st.q.shape):  # dO rows are addressed like Q's (hash_sparse.py:182-213)
+        raise ShapeError(f"dO shape {tuple(d_out.shape)} != Q shape {tuple(st.q.shape)}")
     if st.q_only is not None and _DO_WRITEOUT:
         # dQ gathers Q / dO through the row table, fuses delta and writes dO back in
         # bucket order for dK/dV: no separate delta / dO pass
@@ -482,16 +501,22 @@ def _hash_backward_stage(st, d_out):
                               boundary=(st.T_Q, st.T_KV, False), rows=st.rows, q_rank=sb.q_rank if shared else None)
 
 
-def _fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, exclude_self=True, row_tables=False):
-    """The fused boundary-layout fwd + bwd; returns (FlashOutputs, dq, dk, dv, problem)."""
+def _fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, exclude_self=True, row_tables=False, check=False):
+    """The fused boundary-layout fwd + bwd; returns (FlashOutputs, dq, dk, dv, problem).
+
+    check=False (graph capture, the bench's device-resident step) leaves the status word
+    unread; check=True reads it once after the backward is queued."""
     st = _hash_forward_stage(q, k, v, q_hash, k_hash, scale, exclude_self, row_tables)
     dq, dk, dv = _hash_backward_stage(st, d_out)
+    if check:
+        check_status(st.err)
+    st.outputs._err = st.err
     return st.outputs, dq, dk, dv, st.prob
 
 
 @padded_call("fwd_bwd")
 def hash_sparse_attention_fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, exclude_self=True, row_tables=False,
-                                  out=None):
+                                  out=None, check=True):
     """Forward + backward through the whole hash path, boundary layout in and out.
 
     Returns (O bf16, dQ, dK, dV fp32), each (B, T, H, D).  The reference
@@ -505,12 +530,18 @@ def hash_sparse_attention_fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, ex
     the attention and device->host copies of consecutive batch elements overlap on
     three CUDA streams (every (b, h) slice is independent, hash_sparse.py:223-238, so
     the results are those of one call).  `out` may give the four host result tensors
-    (pinned memory keeps the copies asynchronous).
+    (pinned memory keeps the copies asynchronous).  Host results are complete when the
+    call returns.
+
+    check=True (the reference's behaviour): negative bucket ids raise ShapeError
+    (hash_sparse.py:112-113) and a non-finite output NumericError (softmax.py:63-64).
+    Both are flagged on the device and read once, after every launch of the call is
+    queued, so the check adds no bubble to the GPU timeline.
     """
     if not (isinstance(q, torch.Tensor) and not q.is_cuda):
-        outputs, dq, dk, dv, _ = _fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale, exclude_self, row_tables)
+        outputs, dq, dk, dv, _ = _fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale, exclude_self, row_tables, check)
         return outputs.O, dq, dk, dv
-    return _fwd_bwd_host(q, k, v, q_hash, k_hash, d_out, scale, exclude_self, out)
+    return _fwd_bwd_host(q, k, v, q_hash, k_hash, d_out, scale, exclude_self, out, check)
 
 
 _COPY_STREAMS = {}
@@ -524,7 +555,7 @@ def _copy_streams(dev):
     return _COPY_STREAMS[dev]
 
 
-def _fwd_bwd_host(q, k, v, q_hash, k_hash, d_out, scale, exclude_self, out):
+def _fwd_bwd_host(q, k, v, q_hash, k_hash, d_out, scale, exclude_self, out, check=True):
     dev = torch.device("cuda", torch.cuda.current_device())
     B, T, H, D = q.shape
     same = k_hash is q_hash
@@ -537,7 +568,7 @@ def _fwd_bwd_host(q, k, v, q_hash, k_hash, d_out, scale, exclude_self, out):
     h2d, d2h, _ = _copy_streams(dev)
     h2d.wait_stream(comp)
     d2h.wait_stream(comp)
-    keep = []
+    keep, errs = [], []
     for b in range(B):
         sl = slice(b, b + 1)
         with torch.cuda.stream(h2d):
@@ -549,6 +580,7 @@ def _fwd_bwd_host(q, k, v, q_hash, k_hash, d_out, scale, exclude_self, out):
         for t in xs + [kh]:
             t.record_stream(comp)
         outputs, dq, dk, dv, _ = _fwd_bwd(xs[0], xs[1], xs[2], xs[4], kh, xs[3], scale, exclude_self)
+        errs.append(outputs._err)
         done = torch.cuda.Event()
         done.record(comp)
         with torch.cuda.stream(d2h):
@@ -557,5 +589,10 @@ def _fwd_bwd_host(q, k, v, q_hash, k_hash, d_out, scale, exclude_self, out):
                 dst[sl].copy_(src, non_blocking=True)
                 src.record_stream(d2h)
         keep.append((xs, kh, outputs, dq, dk, dv))
-    comp.wait_stream(d2h)  # results are on the host once the caller's stream reaches here
+    comp.wait_stream(d2h)
+    # the reference API is synchronous: the host results are complete on return
+    comp.synchronize()
+    if check:
+        for e in errs:
+            check_status(e)
     return tuple(out)

@@ -27,6 +27,7 @@ from ._kernel import (
     attention_backward,
     attention_forward,
     check_forward_operands,
+    check_status,
     pack_index,
     make_row_tables,
 )
@@ -212,7 +213,7 @@ def qk_forward_kernel(q_c, k_c, v_c, q_idx, k_idx, scale=None, blocks=BlockSpec(
             B, H, k_c.shape[2]):
         raise ShapeError("index tensors do not match the compacted operands")
     prob = _problem_from(q_c, k_c, q_idx, k_idx)
-    return attention_forward(prob, q_c, k_c, v_c, scale, blocks)
+    return attention_forward(prob, q_c, k_c, v_c, scale, blocks, check=True)
 
 
 @padded_call("qk_bwd")
@@ -268,13 +269,14 @@ def qk_sparse_attention(q, k, v, q_keep, k_keep, scale=None, blocks=BlockSpec(),
     """
     prep = qk_preprocess(q, k, v, q_keep, k_keep)
     return attention_forward(prep.problem, prep.q_c, prep.k_c, prep.v_c, scale, blocks,
-                             boundary=(prep.T_Q, True)).O
+                             boundary=(prep.T_Q, True), check=True).O
 
 
 class _QkState:
     """What the QK backward stage needs from the forward stage."""
 
-    __slots__ = ("prob", "prep", "q", "xq", "outputs", "rows", "q_only", "scale", "T_Q", "T_KV", "q_keep", "k_keep")
+    __slots__ = ("prob", "prep", "q", "xq", "outputs", "rows", "q_only", "scale", "T_Q", "T_KV", "q_keep", "k_keep",
+                 "err")
 
 
 def _qk_forward_stage(q, k, v, q_keep, k_keep, scale=None, row_tables=False):
@@ -296,15 +298,16 @@ def _qk_forward_stage(q, k, v, q_keep, k_keep, scale=None, row_tables=False):
     st.prob = prob = st.prep.problem
     prob.schedule("fwd", "dq", "dkdv")
     st.q = as_operand(q)
+    st.err = torch.zeros(1, dtype=torch.int32, device=st.q.device)
     if mode == "gathered":
         st.q_only = RowTables(prob.rows.q_rows, None, prob.rows.R_q, prob.rows.R_kv)
         st.xq = torch.empty((prob.B, prob.H, prob.T_q, prob.D), dtype=torch.bfloat16, device=st.q.device)
         st.outputs = attention_forward(prob, st.q, st.prep.k_c, st.prep.v_c, scale, boundary=(st.T_Q, False),
-                                       rows=st.q_only, q_out=st.xq)
+                                       rows=st.q_only, q_out=st.xq, err=st.err)
     else:
         st.rows = prob.rows if mode == "rows" else None
         st.outputs = attention_forward(prob, st.prep.q_c, st.prep.k_c, st.prep.v_c, scale,
-                                       boundary=(st.T_Q, False), rows=st.rows)
+                                       boundary=(st.T_Q, False), rows=st.rows, err=st.err)
     _zero_dropped_rows(q_keep, st.outputs.O)
     return st
 
@@ -315,6 +318,8 @@ def _qk_backward_stage(st, d_out):
 
     prob, prep = st.prob, st.prep
     d_b = as_operand(d_out)
+    if tuple(d_b.shape) != tuple(st.q.shape):  # the kernels address dO like Q (qk_sparse.py:151-183)
+        raise ShapeError(f"dO shape {tuple(d_b.shape)} != Q shape {tuple(st.q.shape)}")
     if st.q_only is not None:
         xdo = torch.empty_like(st.xq)
         dq, delta = dq_backward_gathered(prob, st.q, prep.k_c, prep.v_c, st.outputs, d_b, st.q_only, st.scale,
@@ -330,15 +335,19 @@ def _qk_backward_stage(st, d_out):
 
 
 @padded_call("fwd_bwd")
-def qk_sparse_attention_fwd_bwd(q, k, v, q_keep, k_keep, d_out, scale=None, row_tables=False):
+def qk_sparse_attention_fwd_bwd(q, k, v, q_keep, k_keep, d_out, scale=None, row_tables=False, check=True):
     """Forward + backward through the whole QK path in boundary layout.
 
     Returns (O bf16, dQ, dK, dV fp32), all (B, T, H, D); dropped positions get
     zero outputs and zero gradients.  The reference composes the same thing
-    from qk_preprocess -> qk_forward_kernel -> qk_backward_kernel.
+    from qk_preprocess -> qk_forward_kernel -> qk_backward_kernel.  check=True reads
+    the device status word once, after every launch is queued, and raises
+    NumericError for a non-finite output (softmax.py:63-64).
     """
     st = _qk_forward_stage(q, k, v, q_keep, k_keep, scale, row_tables)
     dq, dk, dv = _qk_backward_stage(st, d_out)
+    if check:
+        check_status(st.err)
     return st.outputs.O, dq, dk, dv
 
 

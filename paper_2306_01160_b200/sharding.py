@@ -60,7 +60,8 @@ def gather_segments(results, shape, dtype, group=None, dst=0):
     dist.all_gather_object(everything, payload, group=group)
     if dist.get_rank(group) != dst:
         return None
-    n_out = len(payload[0][1]) if payload else len(everything[0][0][1])
+    # a rank may own no segment (B*H < world): take the output count from any non-empty part
+    n_out = next((len(part[0][1]) for part in everything if part), 0)
     full = [torch.zeros(shape, dtype=dtype) for _ in range(n_out)]
     for part in everything:
         for (b, h0, h1), outs in part:

@@ -15,6 +15,8 @@ g = torch.Generator().manual_seed(0)
 t_end = time.time() + seconds
 n = 0
 worst = {}
+worst_abs = {}
+over_abs = []
 while time.time() < t_end:
     r = lambda lo, hi: int(torch.randint(lo, hi + 1, (1,), generator=g))
     B, H = r(1, 4), r(1, 12)
@@ -52,6 +54,9 @@ while time.time() < t_end:
         err = float((got.float() - want.detach()).abs().max()) if T else 0.0
         scale_ = max(1.0, float(want.detach().abs().max())) if T else 1.0
         worst[name] = max(worst.get(name, 0.0), err / scale_)
+        worst_abs[name] = max(worst_abs.get(name, 0.0), err)
+        if err > 2e-2:
+            over_abs.append((name, kind, B, H, T, D, err, scale_))
         if err > 2e-2 * scale_:  # bf16 P / dS: error grows with the gradient's magnitude
             print("MISMATCH", name, kind, B, H, T, D, err, "max|ref|", scale_, flush=True)
             sys.exit(1)
@@ -66,3 +71,7 @@ while time.time() < t_end:
 torch.cuda.synchronize()
 print(f"stress ok: {n} random calls, each twice, bit-identical, finite; one head per call against fp32 torch, "
       f"worst max-abs / max(1, max|ref|): " + ", ".join(f"{k} {v:.2e}" for k, v in worst.items()), flush=True)
+print("worst absolute max-abs: " + ", ".join(f"{k} {v:.2e}" for k, v in worst_abs.items())
+      + f"; {len(over_abs)} of {4 * n} checks above the absolute 2e-2", flush=True)
+for r in over_abs[:20]:
+    print("  above 2e-2 (name, kind, B, H, T, D, err, max|ref|):", r, flush=True)

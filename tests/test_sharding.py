@@ -69,3 +69,26 @@ def test_two_rank_gloo_matches_single_process():
                                               hsh[b:b + 1, :, h:h + 1])[0] for h in range(H)], dim=2)
                       for b in range(B)])
     assert torch.allclose(out, want, atol=1e-12)
+
+
+def _worker_few(rank, world, port, q, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        res = run_sharded(lambda x: (2.0 * x,), [q], rank, world)
+        full = gather_segments(res, q.shape, torch.float64)
+        if rank == 0:
+            out.copy_(full[0])
+        else:
+            assert full is None
+    finally:
+        dist.destroy_process_group()
+
+
+def test_more_ranks_than_units_gathers():
+    """B*H < world: some ranks own no segment, rank 0 among them possibly."""
+    q = torch.arange(1 * 5 * 1 * 2, dtype=torch.float64).reshape(1, 5, 1, 2)
+    out = torch.zeros_like(q).share_memory_()
+    mp.start_processes(_worker_few, args=(3, _free_port(), q, out), nprocs=3, join=True, start_method="fork")
+    assert torch.equal(out, 2.0 * q)
