@@ -46,14 +46,16 @@ def causal_problem(B, H, T, D, device):
 
 
 @padded_call("flash_fwd")
-def flash_forward(q, k, v, blocks=BlockSpec(), scale=None, workers=None):
-    """Tiled causal attention over (B, H, T, D) operands (dense.py:33-63)."""
+def flash_forward(q, k, v, blocks=BlockSpec(), scale=None, workers=None, check=True):
+    """Tiled causal attention over (B, H, T, D) operands (dense.py:33-63).
+
+    check=False skips the read of the NumericError status word (graph capture)."""
     q, k, v = as_operand(q), as_operand(k), as_operand(v)
     check_forward_operands(q, k, v)
     B, H, T, D = q.shape
     if T != k.shape[2]:
         raise ShapeError("dense causal attention requires T_Q == T_KV")
-    return attention_forward(causal_problem(B, H, T, D, q.device), q, k, v, scale, blocks, check=True)
+    return attention_forward(causal_problem(B, H, T, D, q.device), q, k, v, scale, blocks, check=check)
 
 
 @padded_call("flash_bwd")

@@ -92,3 +92,46 @@ def test_more_ranks_than_units_gathers():
     out = torch.zeros_like(q).share_memory_()
     mp.start_processes(_worker_few, args=(3, _free_port(), q, out), nprocs=3, join=True, start_method="fork")
     assert torch.equal(out, 2.0 * q)
+
+
+@pytest.mark.parametrize("B,H,world", [(4, 12, 1), (4, 12, 2), (4, 12, 3), (4, 12, 8), (3, 5, 4), (2, 3, 7)])
+def test_blocks_cover_the_same_units(B, H, world):
+    from paper_2306_01160_b200.sharding import shard_blocks
+
+    for r in range(world):
+        units = [b * H + h for b, h0, h1 in shard_segments(B, H, r, world) for h in range(h0, h1)]
+        got = [b * H + h for b0, b1, h0, h1 in shard_blocks(B, H, r, world) for b in range(b0, b1) for h in range(h0, h1)]
+        assert got == units
+    if (B, H, world) == (4, 12, 2):
+        assert shard_blocks(B, H, 0, world) == [(0, 2, 0, 12)]
+
+
+def _worker_units(rank, world, port, x, out):
+    from paper_2306_01160_b200.sharding import gather_units, shard_blocks, slice_block
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        B, T, H = x.shape[:3]
+        res = [(blk, (slice_block(x, blk) * 3.0, slice_block(x, blk)[..., :1].to(torch.float32)))
+               for blk in shard_blocks(B, H, rank, world)]
+        full = gather_units(res, B, H)
+        if rank == 0:
+            out[0].copy_(full[0])
+            out[1].copy_(full[1])
+        else:
+            assert full is None
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("B,H,world", [(4, 12, 2), (2, 3, 4), (1, 2, 3)])
+def test_gather_units_collective(B, H, world):
+    """The bench's verification gather (all_gather of packed units) over gloo, uneven counts."""
+    x = torch.randn((B, 7, H, 4), dtype=torch.float64)
+    out = [torch.zeros_like(x).share_memory_(), torch.zeros((B, 7, H, 1), dtype=torch.float32).share_memory_()]
+    mp.start_processes(_worker_units, args=(world, _free_port(), x, out), nprocs=world, join=True,
+                       start_method="fork")
+    assert torch.equal(out[0], 3.0 * x)
+    assert torch.equal(out[1], x[..., :1].float())
