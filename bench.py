@@ -608,6 +608,14 @@ def run_ours(args, cfg):
             prep[n] = {"us": kern_ms[n] * 1e3, "bytes": byt, "gbs": gbs, "frac_of_hbm": gbs / hbm}
     prep["_peak_gbs"] = hbm
 
+    # the single-pass backward variant (scfa_attn_bwd: one key-stationary sweep, dQ reduced in
+    # fp32) of the same step, for comparison with the default two-pass backward
+    def step_single():
+        for (q, k, v, dO), h in zip(dv_in, dv_h):
+            hs._fwd_bwd(q, k, v, h, h, dO, exclude_self=cfg["exclude_self"], single_pass=True)
+
+    sp_ms = timed(ctx, step_single, args.steps, args.warmup)
+
     # dense causal comparator at the same shape (our own kernels, engine layout, same fwd+bwd, same units)
     eng = [[x.transpose(1, 2).contiguous() for x in xs] for xs in dv_in]
 
@@ -666,6 +674,10 @@ def run_ours(args, cfg):
         "prep": prep,
         "stages_ms": {n: round(v, 4) for n, v in sorted(kern_ms.items(), key=lambda kv: -kv[1])},
         "tiles": tiles,
+        "single_pass_backward": {"ms_per_step": sp_ms, "value": flops_step / (sp_ms * 1e-3) / 1e12,
+                                 "note": "same step with scfa_attn_bwd (dQ, dK, dV in one sweep; dQ by fp32 "
+                                         "reductions, not bitwise reproducible); the headline uses the two-pass "
+                                         "backward"},
         "dense_causal": {"ms_per_step": dense_ms, "effective_tflops": dense_flops / (dense_ms * 1e-3) / 1e12,
                          "speedup_of_scfa": dense_ms / ms},
         "clocks": sampler.summary(),

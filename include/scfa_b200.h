@@ -307,6 +307,20 @@ int scfa_attn_bwd_dkdv(const void* q, const void* k, const void* v, const void* 
                        float* dk, float* dv, const int32_t* q_rows, const int32_t* k_rows,
                        int64_t R_q, int64_t R_kv, void* stream);
 
+/* Single-pass backward (ABI 5): dQ, dK, dV in one key-stationary sweep over the dK/dV
+ * schedule (_kernel.py:139-193 with both of its passes fused).  Arguments as
+ * scfa_attn_bwd_dkdv (engine-layout / kernel-order operands, no row tables) plus q_idx
+ * (padded query positions, the dQ routing) and dq.  Each pair of 64-query tiles of a key
+ * block issues dQ += scale * dS K on the tensor cores; the epilogue reduces it (fp32 add)
+ * into dq, which the caller must zero-fill: (B*H, T_q, D) f32, or (B, Tq_out, H, D) at
+ * the original positions when out_boundary.  dK / dV as scfa_attn_bwd_dkdv (Tkv_out).
+ * D = 64 only.  dQ is not bitwise reproducible (the reduction order varies); dK / dV are. */
+int scfa_attn_bwd(const void* q, const void* k, const void* v, const void* d_out, int64_t BH, int64_t T_q,
+                  int64_t T_kv, int64_t D, const int32_t* q_idx, const int32_t* k_idx, const int32_t* k_runs,
+                  int64_t Tq_pad, int64_t Tkv_pad, const float* lse2, const float* delta, const uint16_t* list,
+                  const int32_t* list_count, int64_t list_stride, float scale, int64_t H, int64_t Tq_out,
+                  int64_t Tkv_out, int out_boundary, float* dq, float* dk, float* dv, void* stream);
+
 /* ---------------------------------------------------------------- diagnostics
  * Route per-tile clock64 stamps of subsequent attention launches into `buf`
  * (grid * tiles_per_cta * 8 int64; NULL disables).  Not part of the reference API. */

@@ -443,6 +443,44 @@ def dkdv_backward_sorted(problem, q_sorted, k_sorted, v_sorted, do_sorted, lse2,
     return dk, dv
 
 
+def backward_single_pass(problem, q_sorted, k_sorted, v_sorted, do_sorted, lse2, delta, scale, Tq_out, Tkv_out,
+                         boundary=True):
+    """dQ, dK, dV in one key-stationary sweep (scfa_attn_bwd, D = 64): kernel-order operands,
+    the dK/dV schedule; dQ is reduced per tile pair into a zero-filled fp32 tensor.
+
+    boundary=True: gradients at their original positions of (B, T_*_out, H, D) fp32 tensors
+    (the inverse scatter fused); else engine layout (B, H, T, D) in kernel order.
+    Not bitwise reproducible in dQ (fp32 reduction order); attention_backward is."""
+    B, H, D = problem.B, problem.H, problem.D
+    T_q, T_kv = problem.T_q, problem.T_kv
+    dev = k_sorted.device
+    BH = B * H
+    if boundary:
+        dq = torch.zeros((B, Tq_out, H, D), dtype=torch.float32, device=dev)
+        dk = torch.empty((B, Tkv_out, H, D), dtype=torch.float32, device=dev)
+        dv = torch.empty((B, Tkv_out, H, D), dtype=torch.float32, device=dev)
+    else:
+        dq = torch.zeros((B, H, T_q, D), dtype=torch.float32, device=dev)
+        dk = torch.empty((B, H, T_kv, D), dtype=torch.float32, device=dev)
+        dv = torch.empty((B, H, T_kv, D), dtype=torch.float32, device=dev)
+    if BH == 0 or T_kv == 0 or T_q == 0:
+        if T_kv and BH:
+            dk.zero_()
+            dv.zero_()
+        return dq, dk, dv
+    sched = problem.schedule("dkdv")
+    lst, cnt, stride = sched["dkdv"]
+    _lib.call(
+        "scfa_attn_bwd",
+        _lib.ptr(q_sorted), _lib.ptr(k_sorted), _lib.ptr(v_sorted), _lib.ptr(do_sorted), BH, T_q, T_kv, D,
+        _lib.ptr(problem.q_idx), _lib.ptr(problem.k_idx), _lib.ptr(sched["k_runs"]), problem.Tq_pad, problem.Tkv_pad,
+        _lib.ptr(lse2), _lib.ptr(delta), _lib.ptr(lst), _lib.ptr(cnt), stride, _scale(scale, D), H,
+        Tq_out if boundary else T_q, Tkv_out if boundary else T_kv, 1 if boundary else 0,
+        _lib.ptr(dq), _lib.ptr(dk), _lib.ptr(dv), _lib.stream_ptr(),
+    )
+    return dq, dk, dv
+
+
 def make_row_tables(q_perm, k_perm, B, H, T_q_slots, T_kv_slots, T_Q, T_KV, Tq_pad, Tkv_pad, shared=False):
     """scfa_row_map for both sides (shared=True reuses the query table for keys)."""
     dev = q_perm.device

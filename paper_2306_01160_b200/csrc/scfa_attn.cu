@@ -48,7 +48,11 @@
 
 namespace scfa {
 
-enum Mode : int { MODE_FWD = 0, MODE_DQ = 1, MODE_DKDV = 2 };
+// MODE_BWD: the single-pass backward — key-stationary like MODE_DKDV, and each pair of
+// streamed 64-query tiles also issues dQ = scale * dS K into TMEM, drained by the epilogue
+// warpgroup with fp32 reductions into the caller's zero-filled dQ (not bitwise
+// deterministic: the add order varies; MODE_DQ + MODE_DKDV remain the deterministic path).
+enum Mode : int { MODE_FWD = 0, MODE_DQ = 1, MODE_DKDV = 2, MODE_BWD = 3 };
 
 #ifndef SCFA_TUNE_NS0_FWD
 #define SCFA_TUNE_NS0_FWD 2
@@ -82,7 +86,9 @@ struct Cfg {
   // buffer, so S(t+1) runs while P(t) is computed and both warpgroups work at once.
   // measured: dK/dV gains; dQ loses at D = 64 (two streams beat one MMA issuer) but gains at
   // D = 128, where TMEM holds only one dQ stream anyway
-  static constexpr bool ALT = (kMode == MODE_DKDV) || (kMode == MODE_DQ && kD == 128);
+  static constexpr bool FUSED = (kMode == MODE_BWD);
+  static constexpr bool KEYS = (kMode == MODE_DKDV || kMode == MODE_BWD);  // key-stationary
+  static constexpr bool ALT = KEYS || (kMode == MODE_DQ && kD == 128);
   static constexpr int NSTREAM = ALT ? 1 : ((kD == 64) ? 2 : 1);
   static constexpr int THREADS = 512;
   static constexpr int BM = 128;                             // stationary rows per work item
@@ -90,7 +96,7 @@ struct Cfg {
   static constexpr int DCH = kD / 64;                        // 128-byte column chunks
   static constexpr int NX = (kMode == MODE_FWD) ? 1 : 2;     // stationary tensors
   static constexpr int NXS = 2;                              // stationary slots (next item prefetch)
-  static constexpr bool AUX = (kMode == MODE_DKDV);          // per-column lse2 / delta with y0
+  static constexpr bool AUX = KEYS;                          // per-column lse2 / delta with y0
   static constexpr int X_BYTES = BM * kD * 2;
   static constexpr int XSLOT_BYTES = NX * X_BYTES;
   static constexpr int Y_BYTES = BN * kD * 2;
@@ -100,11 +106,11 @@ struct Cfg {
   static constexpr bool Y0_EARLY = (kMode == MODE_FWD);
   static constexpr bool Y1_EARLY = (kMode == MODE_DQ);
   // ring depths (SCFA_TUNE_* build-time overrides for tuning sweeps, scripts/tune.py)
-  static constexpr int NS0 = (kMode == MODE_FWD)   ? ((kD == 64) ? SCFA_TUNE_NS0_FWD : 2)
+  static constexpr int NS0 = FUSED ? 5 : (kMode == MODE_FWD)   ? ((kD == 64) ? SCFA_TUNE_NS0_FWD : 2)
                              : (ALT && kD == 64)   ? SCFA_TUNE_NS0_ALT
                              : (kMode == MODE_DQ && kD == 64) ? SCFA_TUNE_NS0_DQ
                                                    : 3;
-  static constexpr int NS1 = (kMode == MODE_FWD)   ? ((kD == 64) ? SCFA_TUNE_NS1_FWD : 2)
+  static constexpr int NS1 = FUSED ? 5 : (kMode == MODE_FWD)   ? ((kD == 64) ? SCFA_TUNE_NS1_FWD : 2)
                              : (ALT && kD == 64)   ? SCFA_TUNE_NS1_ALT
                              : (kMode == MODE_DQ && kD == 64) ? SCFA_TUNE_NS1_DQ
                                                    : 2;
@@ -120,29 +126,37 @@ struct Cfg {
   // 32 instead of 48 clk per N = 64 MMA, scripts/mma_issue.cu) — which leaves room for
   // two S / dP buffers, not three
   static constexpr bool KV_TMEM = (kMode == MODE_DKDV && kD == 64);
-  static constexpr int NBUF = KV_TMEM ? 2 : ((ALT && 3 * TM_BUF + ((kMode == MODE_DKDV) ? 2 * kD : kD) <= 512) ? 3 : 2);
+  static constexpr int NBUF = (KV_TMEM || FUSED) ? 2 : ((ALT && 3 * TM_BUF + (KEYS ? 2 * kD : kD) <= 512) ? 3 : 2);
   static constexpr int TM_S = 0;
   static constexpr int TM_DP = (kMode == MODE_FWD) ? 0 : BN;
   static constexpr int TM_ACC = ALT ? NBUF * TM_BUF : 128;
-  static constexpr int ACC_COLS = (kMode == MODE_DKDV) ? 2 * kD : kD;
-  static constexpr int P_COLS = (kMode == MODE_DKDV) ? BN : BN / 2;
+  static constexpr int ACC_COLS = KEYS ? 2 * kD : kD;
+  static constexpr int P_COLS = KEYS ? BN : BN / 2;
   static constexpr bool OVERLAP = !ALT && (TM_ACC + ACC_COLS + P_COLS <= TM_STREAM);
   static constexpr int TM_P = OVERLAP ? TM_ACC + ACC_COLS : TM_S;                 // P | dS | P^T
   static constexpr int TM_P2 = OVERLAP ? TM_ACC + ACC_COLS + BN / 2 : TM_DP;      // dS^T (DKDV)
   static_assert(TM_ACC + ACC_COLS <= TM_STREAM, "TMEM budget");
   static constexpr int TM_KV = TM_ACC + ACC_COLS;  // KV_TMEM buffer b: K [TM_KV + b*kD, +kD/2), V next
   static_assert(!KV_TMEM || TM_KV + 2 * kD <= TM_STREAM, "TMEM budget (K / V)");
+  // FUSED: two dQ accumulators (M = 128 rows = the 2 x 64 queries of a tile pair, N = kD)
+  static constexpr int TM_DQ = TM_ACC + ACC_COLS;
+  static_assert(!FUSED || TM_DQ + 2 * kD <= TM_STREAM, "TMEM budget (dQ)");
   // shared memory per stream (all TMA destinations 1024-aligned)
   static constexpr int OFF_X = 0;
   static constexpr int OFF_Y0 = OFF_X + NXS * XSLOT_BYTES;
   static constexpr int OFF_Y1 = OFF_Y0 + NS0 * Y_BYTES;
   static constexpr int OFF_AUX = OFF_Y1 + NS1 * Y_BYTES;
-  static constexpr int STREAM_BYTES = ((OFF_AUX + NS0 * AUX_BYTES + 1023) / 1024) * 1024;
+  // FUSED: dS of a tile pair as the dQ MMA's A operand (M = 128 queries, K = 128 keys,
+  // MN-major: two 64-query atoms of 128 key rows x 128 B), double-buffered by pair
+  static constexpr int DS_ATOM = BM * 128;
+  static constexpr int DS_PAIR = 2 * DS_ATOM;
+  static constexpr int OFF_DS = ((OFF_AUX + NS0 * AUX_BYTES + 1023) / 1024) * 1024;
+  static constexpr int STREAM_BYTES = OFF_DS + (FUSED ? 2 * DS_PAIR : 0);
   // per-stream control block after all streams' tiles: s_full, s_free, p_full, p_free,
   // acc_full, o_free, x_full/empty[NXS], y0_full/empty[NS0], y1_full/empty[NS1],
   // q_full/empty[NQ] (work ring); the ring
   static constexpr int NQ = 4;
-  static constexpr int N_BARS = 12 + 2 * NXS + 2 * NS0 + 2 * NS1 + 2 * NQ;
+  static constexpr int N_BARS = 12 + 2 * NXS + 2 * NS0 + 2 * NS1 + 2 * NQ + 6;
   static constexpr int OFF_BAR = 0;
   static constexpr int OFF_RING = OFF_BAR + 8 * N_BARS;  // int2 {item, tiles} x NQ
   static constexpr int CTRL_BYTES = ((OFF_RING + 8 * NQ + 15) / 16) * 16;
@@ -183,6 +197,9 @@ struct AttnArgs {
   int list_stride;
   int n_row_blocks;
   int n_items;
+  const int* col_idx;  // BWD: original position of each streamed (query) slot (BH, T_cols_pad)
+  float* out2;         // BWD: dQ, zero-filled by the caller, reduced into
+  int T_out_cols;      // BWD: boundary-layout length of the dQ rows
   __nv_bfloat16* out_o;  // FWD
   float* out0;           // FWD: M      DQ: dQ   DKDV: dK
   float* out1;           // FWD: L      DKDV: dV
@@ -227,6 +244,24 @@ SCFA_DEVICE bool out_row(const AttnArgs& a, int bh, int row, int pos, size_t& of
   const int b = bh / a.H, h = bh - b * a.H;
   off = (static_cast<size_t>(b) * a.T_out + pos) * a.H + h;
   return true;
+}
+
+// BWD: output row of streamed (query) slot `slot` with original position `pos` — the dQ
+// row, engine layout (bh, slot) or boundary layout (b, pos, h).
+SCFA_DEVICE bool out_col(const AttnArgs& a, int bh, int slot, int pos, size_t& off) {
+  if (slot >= a.T_cols) return false;
+  if (!a.out_boundary) {
+    off = static_cast<size_t>(bh) * a.T_cols + slot;
+    return true;
+  }
+  if (pos < 0 || pos >= a.T_out_cols) return false;  // pad slots
+  const int b = bh / a.H, h = bh - b * a.H;
+  off = (static_cast<size_t>(b) * a.T_out_cols + pos) * a.H + h;
+  return true;
+}
+
+SCFA_DEVICE void red_add_v4(float* p, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
 }
 
 // Which element pairs of a 32-column chunk take the polynomial exp2 (FMA pipe) instead of
@@ -308,6 +343,7 @@ SCFA_DEVICE void tmem_ld_cols(uint32_t taddr, uint32_t* r) {
 struct Bars {
   MBar s_full, s_free, p_full, p_free, acc_full, o_free, x_full, x_empty, y0_full, y0_empty, y1_full, y1_empty, q_full,
       q_empty;  // s_full / p_full / p_free: three consecutive barriers (TMEM buffers in ALT)
+  MBar ds_free, dq_full, dq_free;  // BWD, two each (by tile pair parity)
 };
 
 template <class C>
@@ -339,6 +375,12 @@ SCFA_DEVICE Bars bars_of(uint8_t* base) {
   b.q_full = p0 + i;
   i += C::NQ;
   b.q_empty = p0 + i;
+  i += C::NQ;
+  b.ds_free = p0 + i;
+  i += 2;
+  b.dq_full = p0 + i;
+  i += 2;
+  b.dq_free = p0 + i;
   return b;
 }
 
@@ -369,6 +411,7 @@ SCFA_DEVICE void epilogue_wg(const AttnArgs& args, uint8_t* smem_base, uint32_t 
   const int r = threadIdx.x & 127;
   const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
   int cnt[2] = {0, 0};
+  int pce = 0;  // BWD: tile pairs drained
   int live_streams = C::NSTREAM;
   uint8_t* eqb = smem_base + C::OFF_EQ + (warp & 3) * C::EQQ_BYTES;
   const MBar eq(smem_u32(eqb));
@@ -397,7 +440,7 @@ SCFA_DEVICE void epilogue_wg(const AttnArgs& args, uint8_t* smem_base, uint32_t 
           if (kMode == MODE_DQ && args.delta_out) args.delta_out[foff] = 0.f;
           if (out_row(args, bh, row, pos, orow)) {
 #pragma unroll
-            for (int o = 0; o < ((kMode == MODE_DKDV) ? 2 : 1); ++o) {
+            for (int o = 0; o < (C::KEYS ? 2 : 1); ++o) {
               float4* d4 = reinterpret_cast<float4*>(((o == 0) ? args.out0 : args.out1) + orow * kD);
 #pragma unroll
               for (int i = 0; i < kD / 4; ++i) d4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -431,6 +474,46 @@ SCFA_DEVICE void epilogue_wg(const AttnArgs& args, uint8_t* smem_base, uint32_t 
       const bool live = out_row(args, bh, row, pos, orow);
       const uint32_t t_acc = tmem0 + static_cast<uint32_t>(s * C::TM_STREAM) + lane_off + C::TM_ACC;
       uint8_t* stage = smem + C::OFF_X + (ia % C::NXS) * C::XSLOT_BYTES;
+      if (C::FUSED) {
+        // dQ of each tile pair of the item, as its MMAs finish: TMEM lane r holds query
+        // (r & 63) of tile 2m + (r >> 6).  The buffer is released as soon as it is read,
+        // then each row is reduced (fp32 red.v4) into the query's dQ row at its original
+        // position.  (Coalescing the reductions through shared memory, or issuing them from
+        // the row warpgroups, measured no faster: DESIGN.md §6.)
+        const uint32_t t_dq = tmem0 + lane_off + C::TM_DQ;
+        const uint16_t* lst = args.list + static_cast<size_t>(item.x) * args.list_stride;
+        for (int t0 = 0; t0 < item.y; t0 += 2, ++pce) {
+          const int pb = pce & 1;
+          mbar_wait_lazy(B.dq_full + pb, (pce >> 1) & 1);
+          tc_fence_after();
+          uint32_t v0[32], v1[32];
+          tmem_ld32(t_dq + pb * kD, v0);
+          tmem_ld32(t_dq + pb * kD + 32, v1);
+          tmem_wait_ld();
+          tc_fence_before();
+          mbar_arrive_relaxed(B.dq_free + pb);
+          const int t = t0 + (r >> 6);
+          if (t < item.y) {
+            const int slot = (lst[t] & 0x7fff) * C::BN + (r & 63);
+            size_t qoff = 0;
+            if (slot < args.T_cols) {
+              const int pos = args.col_idx[static_cast<size_t>(bh) * args.T_cols_pad + slot];
+              if (out_col(args, bh, slot, pos, qoff)) {
+                float* dst = args.out2 + qoff * kD;
+                const float sc = args.scale;
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                  red_add_v4(dst + 4 * i, __uint_as_float(v0[4 * i]) * sc, __uint_as_float(v0[4 * i + 1]) * sc,
+                             __uint_as_float(v0[4 * i + 2]) * sc, __uint_as_float(v0[4 * i + 3]) * sc);
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                  red_add_v4(dst + 32 + 4 * i, __uint_as_float(v1[4 * i]) * sc, __uint_as_float(v1[4 * i + 1]) * sc,
+                             __uint_as_float(v1[4 * i + 2]) * sc, __uint_as_float(v1[4 * i + 3]) * sc);
+              }
+            }
+          }
+        }
+      }
       mbar_wait_lazy(B.acc_full, ia & 1);
       tc_fence_after();
       if (kMode == MODE_FWD) {
@@ -452,7 +535,7 @@ SCFA_DEVICE void epilogue_wg(const AttnArgs& args, uint8_t* smem_base, uint32_t 
           for (int i = 0; i < 4; ++i) stage_put<RB>(stage, r, c / 8 + i, w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
         }
         tc_fence_before();
-        mbar_arrive(B.o_free);
+        mbar_arrive_relaxed(B.o_free);
         // the reference raises NumericError when o turns non-finite (softmax.py:63-64)
         if (__any_sync(0xffffffffu, live && !finite_ok) && args.err_flag && lane == 0)
           atomicCAS(args.err_flag, 0, SCFA_ERR_NUMERIC);
@@ -471,7 +554,7 @@ SCFA_DEVICE void epilogue_wg(const AttnArgs& args, uint8_t* smem_base, uint32_t 
           for (int i = 0; i < 8; ++i) stage_put<RB>(stage, r, c / 4 + i, v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
         }
         tc_fence_before();
-        mbar_arrive(B.o_free);
+        mbar_arrive_relaxed(B.o_free);
         stage_copy_out<RB>(stage, warp & 3, lane, reinterpret_cast<uint8_t*>(args.out0), static_cast<long long>(orow) * RB,
                            live);
       } else {
@@ -494,7 +577,7 @@ SCFA_DEVICE void epilogue_wg(const AttnArgs& args, uint8_t* smem_base, uint32_t 
           tmem_ld32(t_acc + 32, *reinterpret_cast<uint32_t(*)[32]>(dv + 32));
           tmem_wait_ld();
           tc_fence_before();
-          mbar_arrive(B.o_free);
+          mbar_arrive_relaxed(B.o_free);
           stage_copy_out<RB>(stage, warp & 3, lane, reinterpret_cast<uint8_t*>(args.out0),
                              static_cast<long long>(orow) * RB, live);
 #pragma unroll
@@ -513,7 +596,7 @@ SCFA_DEVICE void epilogue_wg(const AttnArgs& args, uint8_t* smem_base, uint32_t 
             for (int i = 0; i < 8; ++i) stage_put<RB>(stage, r, c / 4 + i, v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
           }
           tc_fence_before();
-          mbar_arrive(B.o_free);
+          mbar_arrive_relaxed(B.o_free);
           stage_copy_out<RB>(stage, warp & 3, lane, reinterpret_cast<uint8_t*>(args.out1),
                              static_cast<long long>(orow) * RB, live);
         }
@@ -560,6 +643,11 @@ __global__ void __launch_bounds__(512, 1)
       for (int i = 0; i < C::NS1; ++i) {
         mbar_init(b.y1_full + i, 1);
         mbar_init(b.y1_empty + i, 1);
+      }
+      for (int i = 0; i < 2; ++i) {
+        mbar_init(b.ds_free + i, 1);   // BWD: the pair's dQ MMAs have read its dS
+        mbar_init(b.dq_full + i, 1);   // BWD: the pair's dQ is in TMEM
+        mbar_init(b.dq_free + i, 128); // BWD: the epilogue has read it
       }
       for (int i = 0; i < C::NQ; ++i) {
         mbar_init(b.q_full + i, 1);
@@ -718,7 +806,9 @@ __global__ void __launch_bounds__(512, 1)
       constexpr uint32_t idesc_acc = make_idesc_bf16(128, kD, false, true);
       // the accumulate MMAs of tile `p` (P V | dS K | P^T dO + dS^T Q)
       int tg = 0, ia = 0;
-      auto flush = [&](int ptg, bool first, bool last, int pia) {
+      int pc = 0;  // BWD: tile pairs whose dQ has been issued
+      constexpr uint32_t idesc_dq = make_idesc_bf16(128, kD, true, true);  // A = dS, B = K: both MN-major
+      auto flush = [&](int ptg, bool first, bool last, int pia, int pt) {
         const int s0 = ptg % C::NS0, s1 = ptg % C::NS1;
         if (kMode == MODE_FWD) mbar_wait_lazy(bar_y1_full + s1, (ptg / C::NS1) & 1);  // V not needed before
         if (lane == 0) { SCFA_STAMP_AT(ptg, 12); }
@@ -726,10 +816,15 @@ __global__ void __launch_bounds__(512, 1)
         mbar_wait(bar_p_full + jb, C::ALT ? ((ptg / C::NBUF) & 1) : (ptg & 1));
         if (lane == 0) { SCFA_STAMP_AT(ptg, 13); }
         if (first && pia > 0) mbar_wait_lazy(B.o_free, (pia - 1) & 1);  // the epilogue has read the previous item
+        // BWD: a pair of tiles (local 2m, 2m+1; or a last odd tile alone) is complete: its dQ
+        // goes into TMEM buffer pc % 2 once the epilogue has drained that buffer's last pair
+        const bool dq_now = C::FUSED && (((pt & 1) == 1) || last);
+        if (dq_now && pc >= 2) mbar_wait_lazy(B.dq_free + (pc & 1), ((pc >> 1) - 1) & 1);
+        if (lane == 0) { SCFA_STAMP_AT(ptg, 4); }
         tc_fence_after();
         // the epilogue reuses the stationary slot once acc_full fires: the write-out must
         // have read it by then
-        if (kMode != MODE_DKDV && last && args.x_writeout && lane == 0) bulk_wait_read0();
+        if (!C::KEYS && last && args.x_writeout && lane == 0) bulk_wait_read0();
         __syncwarp();
         const uint32_t y0_addr = smem_u32(smem + C::OFF_Y0 + s0 * C::Y_BYTES);
         const uint32_t y1_addr = smem_u32(smem + C::OFF_Y1 + s1 * C::Y_BYTES);
@@ -752,23 +847,38 @@ __global__ void __launch_bounds__(512, 1)
                     idesc_acc, on);
           }
         }
+        if (C::FUSED && dq_now) {
+          // dQ[pair] = dS K over the item's 128 keys: A = the pair's dS (M = 128 queries,
+          // MN-major, written by the row threads), B = the stationary K tile read MN-major
+          // (N = head dim contiguous); 16 keys per MMA
+          const uint32_t ds_addr = smem_u32(smem + C::OFF_DS + (pc & 1) * C::DS_PAIR);
+          const uint32_t k_addr = smem_u32(smem + C::OFF_X + (pia % C::NXS) * C::XSLOT_BYTES);
+          const uint32_t dq_acc = tmem + C::TM_DQ + (pc & 1) * kD;
+#pragma unroll
+          for (int k = 0; k < C::BM / 16; ++k)
+            umma_ss(dq_acc, make_sdesc_sw128(ds_addr + k * 2048, C::DS_ATOM, 1024),
+                    make_sdesc_sw128(k_addr + k * 2048, C::BM * 128, 1024), idesc_dq, k > 0);
+          umma_commit(B.ds_free + (pc & 1));
+          umma_commit(B.dq_full + (pc & 1));
+        }
         if (!C::Y0_EARLY) umma_commit(bar_y0_empty + s0);
         if (!C::Y1_EARLY) umma_commit(bar_y1_empty + s1);
         umma_commit(bar_p_free + jb);
         if (last) umma_commit(bar_acc_full);
         }
         __syncwarp();
+        if (dq_now) ++pc;
       };
       // The item's last tile accumulates behind the next item's first S, as inner tiles do,
       // when the next item is already staged; otherwise (the producer is behind, or no
       // item is left) it accumulates at once, since the epilogue waits for it.
       constexpr bool kDeferLast = true;
-      int p_tg = -1, p_ia = 0;
+      int p_tg = -1, p_ia = 0, p_t = 0;
       bool p_first = false, p_last = false;
       for (int k = 0;; ++k) {
         const int qs = k % C::NQ;
         if (p_tg >= 0 && (!kDeferLast || !mbar_test(bar_q_full + qs, (k / C::NQ) & 1))) {
-          flush(p_tg, p_first, p_last, p_ia);
+          flush(p_tg, p_first, p_last, p_ia, p_t);
           p_tg = -1;
         }
         mbar_wait_lazy(bar_q_full + qs, (k / C::NQ) & 1);
@@ -782,11 +892,11 @@ __global__ void __launch_bounds__(512, 1)
         const uint32_t x1_addr = x0_addr + C::X_BYTES;
         if (p_tg >= 0 && !(mbar_test(bar_x_full + xs, (ia / C::NXS) & 1) &&
                            mbar_test(bar_y0_full + tg % C::NS0, (tg / C::NS0) & 1))) {
-          flush(p_tg, p_first, p_last, p_ia);
+          flush(p_tg, p_first, p_last, p_ia, p_t);
           p_tg = -1;
         }
         mbar_wait_lazy(bar_x_full + xs, (ia / C::NXS) & 1);
-        if (kMode != MODE_DKDV && args.x_writeout && lane == 0) {
+        if (!C::KEYS && args.x_writeout && lane == 0) {
           // the gathered stationary rows (FWD: Q, DQ: dO), in kernel order, for the dK/dV
           // pass (the slot is read by TMA only, the proxy of its load; the wait is before
           // acc_full, after which the epilogue reuses the slot)
@@ -820,7 +930,7 @@ __global__ void __launch_bounds__(512, 1)
           } else if (C::OVERLAP) {
             if (tg > 0) mbar_wait_lazy(bar_s_free, (tg - 1) & 1);
           } else if (p_tg >= 0) {
-            flush(p_tg, p_first, p_last, p_ia);  // aliased P: the accumulate MMAs must read it first
+            flush(p_tg, p_first, p_last, p_ia, p_t);  // aliased P: the accumulate MMAs must read it first
             p_tg = -1;
           }
           if (lane == 0) { SCFA_MSTAMP(7); }
@@ -859,17 +969,18 @@ __global__ void __launch_bounds__(512, 1)
           }
           __syncwarp();
           if (lane == 0) { SCFA_MSTAMP(3); }
-          if (p_tg >= 0) flush(p_tg, p_first, p_last, p_ia);  // overlap: tile t-1 accumulates behind S(t)
+          if (p_tg >= 0) flush(p_tg, p_first, p_last, p_ia, p_t);  // overlap: tile t-1 accumulates behind S(t)
           p_tg = tg;
           p_ia = ia;
+          p_t = t;
           p_first = (t == 0);
           p_last = (t == n - 1);
           if (lane == 0) { SCFA_MSTAMP(5); }
         }
         ++ia;
       }
-      if (p_tg >= 0) flush(p_tg, p_first, p_last, p_ia);
-      if (kMode != MODE_DKDV && args.x_writeout && lane == 0) bulk_wait0();  // write-outs complete
+      if (p_tg >= 0) flush(p_tg, p_first, p_last, p_ia, p_t);
+      if (!C::KEYS && args.x_writeout && lane == 0) bulk_wait0();  // write-outs complete
       __syncwarp();
     }
    }
@@ -902,6 +1013,7 @@ __global__ void __launch_bounds__(512, 1)
       mbar_arrive(eq + slot);
     };
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    int pcr = 0;  // BWD: tile pairs of the items before this one
     const uint32_t t_s = tmem + lane_off + C::TM_S;
     const uint32_t t_dp = tmem + lane_off + C::TM_DP;
     const uint32_t t_p = tmem + lane_off + C::TM_P;
@@ -1114,6 +1226,8 @@ __global__ void __launch_bounds__(512, 1)
       } else {
         // ---------------- backward passes: P and dS recomputed from (lse2, delta)
         float my_nlse = 0.f, my_ndelta = 0.f;
+        const int pc0 = pcr;  // BWD: pair index of this item's tiles 0 / 1
+        pcr += (n + 1) >> 1;
         if (kMode == MODE_DQ) {
           my_nlse = -args.lse2[roff];
           if (args.delta_out) {
@@ -1181,12 +1295,18 @@ __global__ void __launch_bounds__(512, 1)
           tc_fence_after();
           const float* clse = nullptr;
           const float* cdelta = nullptr;
-          if (kMode == MODE_DKDV) {
+          if (C::KEYS) {
             const int s0 = tg % C::NS0;
             mbar_wait(bar_y0_full + s0, (tg / C::NS0) & 1);  // acquire the per-column lse/delta
             clse = reinterpret_cast<const float*>(smem + C::OFF_AUX + s0 * C::AUX_BYTES);
             cdelta = clse + C::BN;
           }
+          // BWD: this tile's dS goes to half (t & 1) of pair buffer pc % 2, free once the dQ
+          // MMAs of the pair two before have read it
+          const int pc = pc0 + (t >> 1);
+          uint8_t* ds_row = smem + C::OFF_DS + (pc & 1) * C::DS_PAIR + (t & 1) * C::DS_ATOM + r * 128;
+          if (C::FUSED && pc >= 2) mbar_wait(B.ds_free + (pc & 1), ((pc >> 1) - 1) & 1);
+          SCFA_STAMP(10);
           uint32_t vis[NW];
           if (full) {
 #pragma unroll
@@ -1248,7 +1368,20 @@ __global__ void __launch_bounds__(512, 1)
               tmem_st16(t_pb + cc / 2, pk_p);
               tmem_st16(t_p2b + cc / 2, pk_ds);
             }
+            if (C::FUSED) {
+              // dS row of this key: 32 queries = four 16-byte chunks, 128-byte swizzle (as TMA
+              // writes an SW128 tile), the MN-major image the dQ MMA reads
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const int c = cc / 8 + i;
+                const uint32_t addr = smem_u32(ds_row + ((c ^ (r & 7)) << 4));
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(pk_ds[4 * i]),
+                             "r"(pk_ds[4 * i + 1]), "r"(pk_ds[4 * i + 2]), "r"(pk_ds[4 * i + 3])
+                             : "memory");
+              }
+            }
           }
+          if (C::FUSED) fence_proxy_async_smem();  // dS visible to the tensor core before p_full
           tmem_wait_st();
           tc_fence_before();
           mbar_arrive(bar_p_full + jb);
@@ -1259,7 +1392,7 @@ __global__ void __launch_bounds__(512, 1)
           ++ia;
         } else if (!C::ALT && live) {
 #pragma unroll
-          for (int o = 0; o < ((kMode == MODE_DKDV) ? 2 : 1); ++o) {
+          for (int o = 0; o < (C::KEYS ? 2 : 1); ++o) {
             float4* d4 = reinterpret_cast<float4*>(((o == 0) ? args.out0 : args.out1) + orow * kD);
 #pragma unroll
             for (int i = 0; i < kD / 4; ++i) d4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1308,7 +1441,7 @@ static int make_map(CUtensorMap* map, const void* base, int BH, int T, int D, in
 
 static long long* g_dbg_buf = nullptr;
 static int g_dbg_tiles = 0;
-static int g_per_sm[3][2] = {};  // resident CTAs per SM chosen per (mode, D); 0 = not launched yet
+static int g_per_sm[4][2] = {};  // resident CTAs per SM chosen per (mode, D); 0 = not launched yet
 
 static int sm_count() {
   static int n = 0;
@@ -1370,6 +1503,9 @@ static int launch_mode(const AttnLaunch& L, cudaStream_t stream) {
   a.out0 = L.out0;
   a.out1 = L.out1;
   a.out_lse2 = L.out_lse2;
+  a.col_idx = L.col_idx;
+  a.out2 = L.out2;
+  a.T_out_cols = L.T_out_cols;
   a.scale_log2 = L.scale * 1.4426950408889634f;
   a.scale = L.scale;
   a.err_flag = L.err_flag;
@@ -1403,6 +1539,9 @@ int launch_attention(const AttnLaunch& L, cudaStream_t stream) {
 #if SCFA_ONLY(2, 64)
   if (L.D == 64 && L.mode == MODE_DKDV) return launch_mode<MODE_DKDV, 64>(L, stream);
 #endif
+#if SCFA_ONLY(3, 64)
+  if (L.D == 64 && L.mode == MODE_BWD) return launch_mode<MODE_BWD, 64>(L, stream);
+#endif
 #if SCFA_ONLY(0, 128)
   if (L.D == 128 && L.mode == MODE_FWD) return launch_mode<MODE_FWD, 128>(L, stream);
 #endif
@@ -1428,6 +1567,6 @@ extern "C" int scfa_debug_timing(void* buf, int64_t tiles_per_cta) {
 }
 
 extern "C" int scfa_debug_ctas_per_sm(int mode, int64_t D) {
-  if (mode < 0 || mode > 2 || (D != 64 && D != 128)) return -1;
+  if (mode < 0 || mode > 3 || (D != 64 && D != 128)) return -1;
   return scfa::g_per_sm[mode][D == 64 ? 0 : 1];
 }

@@ -254,3 +254,55 @@ extern "C" int scfa_attn_bwd_dkdv(const void* q, const void* k, const void* v, c
   if (rc && !g_err[0]) set_error("attention backward (dK/dV) launch failed: %s", cudaGetErrorString(cudaGetLastError()));
   return rc;
 }
+
+extern "C" int scfa_attn_bwd(const void* q, const void* k, const void* v, const void* d_out, int64_t BH, int64_t T_q,
+                             int64_t T_kv, int64_t D, const int32_t* q_idx, const int32_t* k_idx,
+                             const int32_t* k_runs, int64_t Tq_pad, int64_t Tkv_pad, const float* lse2,
+                             const float* delta, const uint16_t* list, const int32_t* list_count,
+                             int64_t list_stride, float scale, int64_t H, int64_t Tq_out, int64_t Tkv_out,
+                             int out_boundary, float* dq, float* dk, float* dv, void* stream) {
+  int rc = check_attn_args(BH, T_q, T_kv, D, Tq_pad, Tkv_pad, q, k, v);
+  if (rc) return rc;
+  if (D != 64) {
+    set_error("attn_bwd (single pass): head dim %lld unsupported (64; use the two-pass dQ + dK/dV)",
+              static_cast<long long>(D));
+    return SCFA_ERR_SHAPE;
+  }
+  if (!dq || !q_idx) {
+    set_error("attn_bwd: dq and q_idx are required");
+    return SCFA_ERR_PARAM;
+  }
+  if (BH == 0 || T_kv == 0 || T_q == 0) return SCFA_OK;  // dQ stays as given (zero), dK / dV: no rows
+  AttnLaunch L{};
+  L.mode = 3;  // rows = keys; dQ reduced per tile pair
+  L.D = static_cast<int>(D);
+  L.BH = static_cast<int>(BH);
+  L.H = static_cast<int>(H);
+  L.T_out = static_cast<int>(Tkv_out);
+  L.T_out_cols = static_cast<int>(Tq_out);
+  L.out_boundary = out_boundary;
+  L.scale = scale;
+  L.lse2 = lse2;
+  L.delta = delta;
+  L.list = list;
+  L.list_count = list_count;
+  L.list_stride = static_cast<int>(list_stride);
+  L.out0 = dk;
+  L.out1 = dv;
+  L.out2 = dq;
+  L.col_idx = q_idx;
+  L.T_rows = static_cast<int>(T_kv);
+  L.T_cols = static_cast<int>(T_q);
+  L.T_rows_pad = static_cast<int>(Tkv_pad);
+  L.T_cols_pad = static_cast<int>(Tq_pad);
+  L.x0 = k;
+  L.x1 = v;
+  L.y0 = q;
+  L.y1 = d_out;
+  L.row_idx = k_idx;
+  L.row_runs = k_runs;
+  L.n_row_blocks = (L.T_rows + 127) / 128;
+  rc = launch_attention(L, static_cast<cudaStream_t>(stream));
+  if (rc && !g_err[0]) set_error("attention backward (single pass) launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+  return rc;
+}

@@ -64,6 +64,13 @@ SCFA_DEVICE void mbar_arrive(MBar bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar.a) : "memory");
 }
 
+// Arrive without release semantics: for consumers whose data is already in registers
+// (tcgen05.ld + wait::ld, ld.shared), so the arrive need not wait for this thread's
+// outstanding global stores / reductions to be performed.
+SCFA_DEVICE void mbar_arrive_relaxed(MBar bar) {
+  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(bar.a) : "memory");
+}
+
 SCFA_DEVICE void mbar_arrive_expect_tx(MBar bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar.a),
                "r"(bytes)

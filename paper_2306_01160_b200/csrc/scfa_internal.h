@@ -17,7 +17,7 @@ constexpr int32_t kQHashOob = -3;         // bucket sentinel of a query slot pas
 constexpr int32_t kKHashOob = -2;         // bucket sentinel of a key slot past the end
 
 struct AttnLaunch {
-  int mode;  // 0 fwd, 1 dq, 2 dkdv
+  int mode;  // 0 fwd, 1 dq, 2 dkdv, 3 fused bwd (dq + dkdv)
   int D;
   int BH;
   int H;             // heads (for the boundary-layout epilogue)
@@ -47,6 +47,9 @@ struct AttnLaunch {
   float* out0;
   float* out1;
   float* out_lse2;
+  const int* col_idx;  // BWD: original position per streamed (query) slot (BH, T_cols_pad)
+  float* out2;         // BWD: dQ (zero-filled; reduced into)
+  int T_out_cols;      // BWD: boundary length of the dQ rows
   float scale;
   int32_t* err_flag;  // FWD: SCFA_ERR_NUMERIC when an output row or its l is non-finite (softmax.py:63-64)
 };

@@ -210,7 +210,7 @@ def _permute3(xs, ranks, T_perm):
 
 _PREP_MAX_T = 16384
 _Q_WRITEOUT = True  # forward gathers Q and writes the bucket-order copy (see _fwd_bwd)
-_DO_WRITEOUT = True  # dQ gathers Q / dO, fuses delta, writes the bucket-order dO copy
+_DO_WRITEOUT = True  # dQ gathers Q / dO, fuses delta, writes the bucket-order dO copy (two-pass backward)
 
 
 def _event_ptr(ev):
@@ -415,10 +415,12 @@ def hash_sparse_attention(q, k, v, q_hash, k_hash, scale=None, blocks=BlockSpec(
 class _HashState:
     """What the backward stage needs from the forward stage."""
 
-    __slots__ = ("prob", "sb", "q", "xq", "xk", "xv", "outputs", "rows", "q_only", "scale", "T_Q", "T_KV", "err")
+    __slots__ = ("prob", "sb", "q", "xq", "xk", "xv", "outputs", "rows", "q_only", "scale", "T_Q", "T_KV", "err",
+                 "single_pass")
 
 
-def _hash_forward_stage(q, k, v, q_hash, k_hash, scale=None, exclude_self=True, row_tables=False):
+def _hash_forward_stage(q, k, v, q_hash, k_hash, scale=None, exclude_self=True, row_tables=False,
+                        single_pass=False):
     """Preparation + forward of the boundary-layout hash path; returns a _HashState.
 
     Default (shared ids): Q / K / V are put in bucket order without copy passes for Q:
@@ -442,6 +444,7 @@ def _hash_forward_stage(q, k, v, q_hash, k_hash, scale=None, exclude_self=True, 
     st.prob, st.sb, st.q, st.scale = prob, sb, q, scale
     st.T_Q, st.T_KV = q.shape[1], k.shape[1]
     st.rows, st.q_only, st.err = (prob.rows if row_tables else None), None, err
+    st.single_pass = False
     if row_tables:
         st.xq, st.xk, st.xv = q, k, v
         prob.schedule("fwd", "dq", "dkdv")  # runs + all three tile lists in one pass
@@ -463,7 +466,9 @@ def _hash_forward_stage(q, k, v, q_hash, k_hash, scale=None, exclude_self=True, 
             xq, xk, xv = _permute3([q, k, v], [sb.q_rank, sb.k_rank, sb.k_rank], st.T_Q)
         else:
             xq, xk, xv = _gather3([q, k, v], [sb.q_perm, sb.k_perm, sb.k_perm], "bthd")
-    prob.schedule("fwd", "dq", "dkdv")  # overlaps the copies
+    # overlaps the copies; the single-pass backward needs no dQ list
+    st.single_pass = bool(single_pass and q_writeout and q.shape[3] == 64)
+    prob.schedule(*(("fwd", "dkdv") if st.single_pass else ("fwd", "dq", "dkdv")))
     main.wait_stream(side)
     for t in (xq, xk, xv):
         if t is not None:
@@ -488,6 +493,19 @@ def _hash_backward_stage(st, d_out):
     prob, sb = st.prob, st.sb
     if tuple(d_out.shape) != tuple(st.q.shape):  # dO rows are addressed like Q's (hash_sparse.py:182-213)
         raise ShapeError(f"dO shape {tuple(d_out.shape)} != Q shape {tuple(st.q.shape)}")
+    if st.single_pass:
+        # single pass: delta = rowsum(dO * O) with dO moved into bucket order (read in memory
+        # order, written to each position's slot), then dQ, dK, dV in one key-stationary sweep
+        from ._kernel import backward_single_pass
+
+        B, T, H, D = st.q.shape
+        Tq_pad = prob.Tq_pad
+        xdo = torch.empty_like(st.xq)
+        delta = torch.empty((B * H, Tq_pad), dtype=torch.float32, device=d_out.device)
+        _lib.call("scfa_bwd_prep_rank", _lib.ptr(st.outputs.O), _lib.ptr(d_out), B, T, H, D, Tq_pad,
+                  _lib.ptr(sb.q_rank), _lib.ptr(xdo), _lib.ptr(delta), _lib.stream_ptr())
+        return backward_single_pass(prob, st.xq, st.xk, st.xv, xdo, st.outputs._lse2, delta, st.scale, st.T_Q,
+                                    st.T_KV)
     if st.q_only is not None and _DO_WRITEOUT:
         # dQ gathers Q / dO through the row table, fuses delta and writes dO back in
         # bucket order for dK/dV: no separate delta / dO pass
@@ -501,12 +519,16 @@ def _hash_backward_stage(st, d_out):
                               boundary=(st.T_Q, st.T_KV, False), rows=st.rows, q_rank=sb.q_rank if shared else None)
 
 
-def _fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, exclude_self=True, row_tables=False, check=False):
+def _fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, exclude_self=True, row_tables=False, check=False,
+             single_pass=False):
     """The fused boundary-layout fwd + bwd; returns (FlashOutputs, dq, dk, dv, problem).
 
     check=False (graph capture, the bench's device-resident step) leaves the status word
-    unread; check=True reads it once after the backward is queued."""
-    st = _hash_forward_stage(q, k, v, q_hash, k_hash, scale, exclude_self, row_tables)
+    unread; check=True reads it once after the backward is queued.  single_pass=True (D = 64,
+    shared ids) runs the one-sweep backward (scfa_attn_bwd: dQ reduced in fp32, order
+    varies); the default two-pass backward (dQ pass + dK/dV pass) is bitwise reproducible
+    and measured as fast or faster."""
+    st = _hash_forward_stage(q, k, v, q_hash, k_hash, scale, exclude_self, row_tables, single_pass)
     dq, dk, dv = _hash_backward_stage(st, d_out)
     if check:
         check_status(st.err)
@@ -516,7 +538,7 @@ def _fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, exclude_self=True, row_
 
 @padded_call("fwd_bwd")
 def hash_sparse_attention_fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, exclude_self=True, row_tables=False,
-                                  out=None, check=True):
+                                  out=None, check=True, single_pass=False):
     """Forward + backward through the whole hash path, boundary layout in and out.
 
     Returns (O bf16, dQ, dK, dV fp32), each (B, T, H, D).  The reference
@@ -537,11 +559,16 @@ def hash_sparse_attention_fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale=None, ex
     (hash_sparse.py:112-113) and a non-finite output NumericError (softmax.py:63-64).
     Both are flagged on the device and read once, after every launch of the call is
     queued, so the check adds no bubble to the GPU timeline.
+
+    single_pass=True: at D = 64 the backward is one key-stationary pass whose dQ is reduced
+    in fp32 (reduction order varies run to run, ~1 ulp); the default two-pass backward is
+    bitwise reproducible.
     """
     if not (isinstance(q, torch.Tensor) and not q.is_cuda):
-        outputs, dq, dk, dv, _ = _fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale, exclude_self, row_tables, check)
+        outputs, dq, dk, dv, _ = _fwd_bwd(q, k, v, q_hash, k_hash, d_out, scale, exclude_self, row_tables, check,
+                                          single_pass)
         return outputs.O, dq, dk, dv
-    return _fwd_bwd_host(q, k, v, q_hash, k_hash, d_out, scale, exclude_self, out, check)
+    return _fwd_bwd_host(q, k, v, q_hash, k_hash, d_out, scale, exclude_self, out, check, single_pass)
 
 
 _COPY_STREAMS = {}
@@ -555,7 +582,7 @@ def _copy_streams(dev):
     return _COPY_STREAMS[dev]
 
 
-def _fwd_bwd_host(q, k, v, q_hash, k_hash, d_out, scale, exclude_self, out, check=True):
+def _fwd_bwd_host(q, k, v, q_hash, k_hash, d_out, scale, exclude_self, out, check=True, single_pass=False):
     dev = torch.device("cuda", torch.cuda.current_device())
     B, T, H, D = q.shape
     same = k_hash is q_hash
@@ -579,7 +606,8 @@ def _fwd_bwd_host(q, k, v, q_hash, k_hash, d_out, scale, exclude_self, out, chec
         comp.wait_event(ready)
         for t in xs + [kh]:
             t.record_stream(comp)
-        outputs, dq, dk, dv, _ = _fwd_bwd(xs[0], xs[1], xs[2], xs[4], kh, xs[3], scale, exclude_self)
+        outputs, dq, dk, dv, _ = _fwd_bwd(xs[0], xs[1], xs[2], xs[4], kh, xs[3], scale, exclude_self,
+                                          single_pass=single_pass)
         errs.append(outputs._err)
         done = torch.cuda.Event()
         done.record(comp)

@@ -1,0 +1,11 @@
+#!/bin/bash
+# A/B of alternative builds: bench step / stage times for each library given (paths
+# relative to the repo root; "tree" = the in-tree build), alternating twice.
+for i in 1 2; do
+  for lib in "$@"; do
+    if [ "$lib" = tree ]; then L=""; else L="$GRAFT_REPO_ROOT/$lib"; fi
+    SCFA_LIB=$L timeout 300 python bench.py --steps 20 --warmup 5 --no-cfg3 --no-cudnn --no-cpu-baseline 2>/dev/null | python -c "
+import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); s=d['stages_ms']
+print('$lib'.ljust(28), round(d['ms_per_step'],4), ' '.join(f'{k.replace(\"scfa_\",\"\")}={v}' for k,v in s.items()))"
+  done
+done

@@ -17,7 +17,7 @@ import subprocess
 from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-MODE_NAME = {"0": "scfa_attn_fwd", "1": "scfa_attn_bwd_dq", "2": "scfa_attn_bwd_dkdv"}
+MODE_NAME = {"0": "scfa_attn_fwd", "1": "scfa_attn_bwd_dq", "2": "scfa_attn_bwd_dkdv", "3": "scfa_attn_bwd"}
 METRICS = [
     ("gpu__time_duration.sum", "us"),
     ("dram__bytes_read.sum", "MB read"),

@@ -228,3 +228,35 @@ def test_padding_safety_fuzz_bitwise(B, H, T, D):
     assert torch.equal(fg[0][kept_q], grads[0][kept_q])
     assert torch.equal(fg[1][kept_k], grads[1][kept_k])
     assert torch.equal(fg[2][kept_k], grads[2][kept_k])
+
+
+# ------------------------------------------------------------------ single-pass backward
+
+@pytest.mark.parametrize("name", [n for n in gc.case_names("hash")])
+def test_single_pass_backward_golden(name):
+    """scfa_attn_bwd (dQ, dK, dV in one key-stationary sweep, dQ reduced in fp32) against the
+    reference goldens; cases it does not cover (distinct ids, D = 128) fall back to the
+    two-pass backward and must match just the same."""
+    meta, g = gc.load(name)
+    q, k, v, dO = (_t(x, torch.bfloat16) for x in gc.inputs(meta))
+    qh, kh = (_t(x) for x in gc.sparsity(meta))
+    if meta["shared"]:
+        kh = qh
+    o, dq, dk, dv = scfa.hash_sparse_attention_fwd_bwd(q, k, v, qh, kh, dO, exclude_self=meta["exclude_self"],
+                                                       single_pass=True)
+    _close("O", _np(o), g["O"])
+    for label, got in (("dq", dq), ("dk", dk), ("dv", dv)):
+        _close(label, _np(got), g[label])
+
+
+@pytest.mark.parametrize("B,T,H,nb", [(1, 300, 2, 4), (4, 8192, 12, 16), (2, 16384, 3, 64)])
+def test_single_pass_matches_two_pass(B, T, H, nb):
+    """dK / dV bit for bit (same arithmetic and order); dQ to fp32 reduction-order noise."""
+    g = torch.Generator(device="cuda").manual_seed(T + nb)
+    q, k, v, dO = (torch.randn((B, T, H, 64), device="cuda", generator=g).to(torch.bfloat16) for _ in range(4))
+    ids = torch.randint(0, nb, (B, T, H), device="cuda", generator=g)
+    a = scfa.hash_sparse_attention_fwd_bwd(q, k, v, ids, ids, dO, single_pass=True)
+    b = scfa.hash_sparse_attention_fwd_bwd(q, k, v, ids, ids, dO)
+    assert torch.equal(a[0], b[0]) and torch.equal(a[2], b[2]) and torch.equal(a[3], b[3])
+    err = float((a[1] - b[1]).abs().max())
+    assert err <= 1e-4 * max(1.0, float(b[1].abs().max())), err
