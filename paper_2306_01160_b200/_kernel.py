@@ -251,6 +251,8 @@ def check_status(err, what="attention"):
     if code:
         msgs = {_lib.ERR_SHAPE: "bucket ids must be non-negative (and < 2**31)",
                 _lib.ERR_NUMERIC: "non-finite values in attention output (update_stats, softmax.py:63-64)"}
+        if what != "attention" and code == _lib.ERR_SHAPE:
+            msgs[code] = what
         _lib.raise_for_status(code, msgs.get(code, what))
 
 

@@ -40,11 +40,13 @@ class _HashSparseAttention(torch.autograd.Function):
 
 class _QkSparseAttention(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, q, k, v, q_keep, k_keep, scale):
+    def forward(ctx, q, k, v, q_keep, k_keep, scale, check):
         # the same stages as qk_sparse_attention_fwd_bwd
         from .qk_sparse import _qk_forward_stage
 
         st = _qk_forward_stage(q, k, v, q_keep, k_keep, scale)
+        if check:  # keep entries in {0, 1} (qk_sparse.py:54-55), a non-finite output (softmax.py:63-64)
+            check_status(st.err, "keep entries must be 0 or 1")
         ctx.state = (st, q.dtype, k.dtype, v.dtype)
         return st.outputs.O.to(q.dtype)
 
@@ -55,7 +57,7 @@ class _QkSparseAttention(torch.autograd.Function):
         st, qt, kt, vt = ctx.state
         dq, dk, dv = _qk_backward_stage(st, d_out.contiguous())
         ctx.state = None
-        return dq.to(qt), dk.to(kt), dv.to(vt), None, None, None
+        return dq.to(qt), dk.to(kt), dv.to(vt), None, None, None, None
 
 
 @padded_call("attn")
@@ -70,9 +72,11 @@ def hash_sparse_attention_autograd(q, k, v, q_hash, k_hash, scale=None, exclude_
 
 
 @padded_call("attn")
-def qk_sparse_attention_autograd(q, k, v, q_keep, k_keep, scale=None):
-    """qk_sparse_attention (qk_sparse.py:228-239) with gradients w.r.t. q, k, v."""
-    return _QkSparseAttention.apply(q, k, v, q_keep, k_keep, scale)
+def qk_sparse_attention_autograd(q, k, v, q_keep, k_keep, scale=None, check=True):
+    """qk_sparse_attention (qk_sparse.py:228-239) with gradients w.r.t. q, k, v.
+
+    check=False skips the status read-back (one host sync per call)."""
+    return _QkSparseAttention.apply(q, k, v, q_keep, k_keep, scale, check)
 
 
 _DENSE_PROBLEMS = {}

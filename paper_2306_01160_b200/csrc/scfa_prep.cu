@@ -678,6 +678,49 @@ __global__ void __launch_bounds__(256) permute_rows3_kernel(const __grid_constan
   }
 }
 
+// The same permutation for the common case — every tensor shares one rank vector, row
+// counts fit 32-bit indexing, rows are 16-byte multiples that split evenly over a warp
+// (VL lanes per row, 32 / VL rows per warp instruction): the (b, t, h) decode and the rank
+// load are done once per row for all NT tensors, each warp reads 32 x 16 contiguous bytes
+// of every source and writes whole rows.  U rows per lane in flight.
+template <int NT, int U>
+__global__ void __launch_bounds__(256) permute_rows_fast_kernel(const __grid_constant__ GatherJobs J, int vl_shift,
+                                                                 int T, int H, int n_rows, int row_bytes) {
+  const int vl = 1 << vl_shift;
+  const int lane_row = (threadIdx.x & 31) >> vl_shift;  // row within the warp's group
+  const int c = threadIdx.x & (vl - 1);                   // 16-byte chunk of the row
+  const int rows_per_warp = 32 >> vl_shift;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int32_t* __restrict__ rank = J.perm[0];
+  const int n_slots = static_cast<int>(J.n_slots[0]);
+  for (int base = warp * rows_per_warp * U; base < n_rows; base += warps * rows_per_warp * U) {
+    uint4 v[U][NT];
+    long long doff[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int r = base + u * rows_per_warp + lane_row;  // memory-order row (b, t, h), h fastest
+      doff[u] = -1;
+      if (r < n_rows) {
+        const int h = r % H, bt = r / H;
+        const int t = bt % T, b = bt / T;
+        const int bh = b * H + h;
+        const int slot = __ldg(rank + static_cast<size_t>(bh) * T + t);
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+          v[u][j] = __ldg(reinterpret_cast<const uint4*>(J.src[j] + static_cast<size_t>(r) * row_bytes) + c);
+        if (slot < n_slots) doff[u] = (static_cast<long long>(bh) * n_slots + slot) * row_bytes + c * 16;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (doff[u] >= 0) {
+#pragma unroll
+        for (int j = 0; j < NT; ++j) *reinterpret_cast<uint4*>(J.dst[j] + doff[u]) = v[u][j];
+      }
+  }
+}
+
 __global__ void gather_rows_kernel(const uint8_t* __restrict__ src, int eb, int64_t H, int64_t D, int64_t sb,
                                    int64_t st, int64_t sh, const int32_t* __restrict__ perm, int64_t T_perm,
                                    int64_t n_slots, uint8_t* __restrict__ dst, int64_t n_rows) {
@@ -1060,6 +1103,36 @@ extern "C" int scfa_permute_rows3(int n, const void* const* srcs, void* const* d
   }
   const int64_t work = B * T * H * (D * elem_bytes / 16);
   if (work == 0) return SCFA_OK;
+  // fast path: shared rank vector and slot count, contiguous (B, T, H, D) sources, a row of
+  // 1..32 sixteen-byte chunks (power of two), 32-bit row indexing
+  const int64_t row_bytes = D * elem_bytes;
+  const int64_t vecs = row_bytes / 16;
+  bool fast = (vecs & (vecs - 1)) == 0 && vecs <= 32 && B * T * H < (1LL << 31) && B * H * T < (1LL << 31);
+  for (int i = 0; i < n && fast; ++i)
+    fast = ranks[i] == ranks[0] && n_slots[i] == n_slots[0] && strides[3 * i + 2] == D &&
+           strides[3 * i + 1] == H * D && strides[3 * i] == T * H * D &&
+           (reinterpret_cast<uintptr_t>(srcs[i]) & 15) == 0 && (reinterpret_cast<uintptr_t>(dsts[i]) & 15) == 0;
+  if (fast) {
+    int shift = 0;
+    while ((1LL << shift) < vecs) ++shift;
+#ifndef SCFA_TUNE_PERM_U
+#define SCFA_TUNE_PERM_U 4
+#endif
+#ifndef SCFA_TUNE_PERM_G
+#define SCFA_TUNE_PERM_G 8
+#endif
+    constexpr int U = SCFA_TUNE_PERM_U;
+    const int64_t rows = B * T * H;
+    const int64_t rows_per_block = (256 / 32) * (32 >> shift) * U;
+    int64_t g = (rows + rows_per_block - 1) / rows_per_block;
+    if (g > 148 * SCFA_TUNE_PERM_G) g = 148 * SCFA_TUNE_PERM_G;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int Ti = static_cast<int>(T), Hi = static_cast<int>(H), R = static_cast<int>(rows), RB = static_cast<int>(row_bytes);
+    if (n == 1) permute_rows_fast_kernel<1, U><<<static_cast<unsigned>(g), 256, 0, s>>>(J, shift, Ti, Hi, R, RB);
+    else if (n == 2) permute_rows_fast_kernel<2, U><<<static_cast<unsigned>(g), 256, 0, s>>>(J, shift, Ti, Hi, R, RB);
+    else permute_rows_fast_kernel<3, U><<<static_cast<unsigned>(g), 256, 0, s>>>(J, shift, Ti, Hi, R, RB);
+    return check_launch("permute_rows (fast)");
+  }
   int64_t g = (work + 256 * 4 - 1) / (256 * 4);
   if (g > 148 * 16) g = 148 * 16;
   dim3 grid(static_cast<unsigned>(g), static_cast<unsigned>(n));

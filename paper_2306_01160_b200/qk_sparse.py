@@ -190,6 +190,38 @@ def qk_preprocess(q, k, v, q_keep, k_keep, materialize=True):
     )
 
 
+def _prepare_static(q, k, v, q_keep, k_keep, err):
+    """qk_preprocess for the fused paths with every size static: the compacted buffers hold
+    T_Q / T_KV slots (kept rows first, in position order, then pad slots — QUERY_PAD /
+    KEY_PAD in the index vectors, the dropped rows' data in the operands) instead of the
+    reference's max kept count (qk_sparse.py:58), so nothing is read back to the host and
+    the whole fwd + bwd can be captured in a CUDA graph.  Pad slots have empty visibility
+    runs: no tile lists them, their outputs are zero.  Keep entries outside {0, 1} are
+    flagged SCFA_ERR_SHAPE in the device status word `err` (qk_sparse.py:54-55)."""
+    B, T_Q, H, D = q.shape
+    T_KV = k.shape[1]
+    if T_KV >= KEY_PAD:
+        raise ShapeError(f"T_KV must be < {KEY_PAD}")
+    dev = q.device
+    qk_ = _keep_tensor(q_keep, (B, T_Q, H), dev)
+    kk_ = _keep_tensor(k_keep, (B, T_KV, H), dev)
+    BH = B * H
+    cnt = torch.empty(2 * BH, dtype=torch.int32, device=dev)
+    q_perm, q_rank = _compact_perm(qk_, B, T_Q, H, cnt[:BH], err)
+    k_perm, k_rank = _compact_perm(kk_, B, T_KV, H, cnt[BH:], err)
+    q_aux = _aux(q_perm, cnt[:BH], B, H, T_Q, QUERY_PAD, _OOB_Q)
+    k_aux = _aux(k_perm, cnt[BH:], B, H, T_KV, KEY_PAD, _OOB_K)
+    problem = Problem(B, H, T_Q, T_KV, D, q_aux, k_aux)
+    k_c, v_c = _gather(k, k_perm, T_KV), _gather(v, k_perm, T_KV)
+    problem.rows = make_row_tables(q_perm, k_perm, B, H, T_Q, T_KV, T_Q, T_KV, problem.Tq_pad, problem.Tkv_pad)
+    return QkPrepared(
+        q_c=q, k_c=k_c, v_c=v_c,
+        q_idx=q_aux[:, :T_Q].view(B, H, T_Q), k_idx=k_aux[:, :T_KV].view(B, H, T_KV),
+        scatter_index=q_perm.view(B, H, T_Q).transpose(1, 2),
+        T_Q=T_Q, problem=problem, q_rank=q_rank, k_rank=k_rank,
+    )
+
+
 def _problem_from(q_c, k_c, q_idx, k_idx, validate=True):
     check_forward_operands(q_c, k_c, k_c)
     B, H, T_Q, D = q_c.shape
@@ -282,23 +314,28 @@ class _QkState:
 def _qk_forward_stage(q, k, v, q_keep, k_keep, scale=None, row_tables=False):
     """Preparation + forward of the boundary-layout QK path; returns a _QkState.
 
-    Default: only K / V are compacted up front; the forward reads Q through the row table
-    and writes the compacted Q back (as the hash path).  row_tables=True: every load goes
-    through the row tables.  Dropped rows of O are zeroed here (not zero-filled up front).
+    Default: static sizes (_prepare_static, no host synchronisation, graph-capturable);
+    only K / V are compacted up front; the forward reads Q through the row table and writes
+    the compacted Q back (as the hash path).  row_tables=True: the reference's sizing (one
+    read-back of the kept counts) and every load through the row tables.  Dropped rows of O
+    are zeroed here (not zero-filled up front).
     """
     st = _QkState()
     st.T_Q, st.T_KV, st.scale, st.q_keep, st.k_keep = q.shape[1], k.shape[1], scale, q_keep, k_keep
     st.q_only, st.xq, st.rows = None, None, None
+    q, k, v = as_operand(q), as_operand(k), as_operand(v)
+    if q.dim() != 4 or k.dim() != 4 or k.shape != v.shape or q.shape[0] != k.shape[0] or q.shape[2:] != k.shape[2:]:
+        raise ShapeError(f"operand shapes disagree: {tuple(q.shape)}, {tuple(k.shape)}, {tuple(v.shape)}")
+    st.err = torch.zeros(1, dtype=torch.int32, device=q.device)
     if row_tables:
         st.prep, mode = qk_preprocess(q, k, v, q_keep, k_keep, materialize=False), "rows"
+    elif st.T_Q == 0:
+        st.prep, mode = qk_preprocess(q, k, v, q_keep, k_keep), "sorted"
     else:
-        st.prep, mode = qk_preprocess(q, k, v, q_keep, k_keep, materialize="kv"), "gathered"
-        if st.prep.problem.rows is None or st.prep.problem.T_q == 0:  # degenerate: every query dropped
-            st.prep, mode = qk_preprocess(q, k, v, q_keep, k_keep), "sorted"
+        st.prep, mode = _prepare_static(q, k, v, q_keep, k_keep, st.err), "gathered"
     st.prob = prob = st.prep.problem
     prob.schedule("fwd", "dq", "dkdv")
-    st.q = as_operand(q)
-    st.err = torch.zeros(1, dtype=torch.int32, device=st.q.device)
+    st.q = q
     if mode == "gathered":
         st.q_only = RowTables(prob.rows.q_rows, None, prob.rows.R_q, prob.rows.R_kv)
         st.xq = torch.empty((prob.B, prob.H, prob.T_q, prob.D), dtype=torch.bfloat16, device=st.q.device)
@@ -347,7 +384,7 @@ def qk_sparse_attention_fwd_bwd(q, k, v, q_keep, k_keep, d_out, scale=None, row_
     st = _qk_forward_stage(q, k, v, q_keep, k_keep, scale, row_tables)
     dq, dk, dv = _qk_backward_stage(st, d_out)
     if check:
-        check_status(st.err)
+        check_status(st.err, "keep entries must be 0 or 1")
     return st.outputs.O, dq, dk, dv
 
 
