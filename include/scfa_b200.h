@@ -298,14 +298,18 @@ int scfa_attn_bwd_dq(const void* q, const void* k, const void* v, const void* d_
 /* Backward pass 2 (dK/dV, key-block owner over the transposed schedule,
  * _kernel.py:181-192).  k_runs, list_dkdv, count_dkdv from scfa_build_schedule.
  * dk, dv (B*H, T_kv, D) f32, or (B, T_out, H, D) scattered by k_idx when out_boundary,
- * or the rows k_rows of [R_kv, D] f32 tables in gather mode.                         */
+ * or the rows k_rows of [R_kv, D] f32 tables in gather mode.
+ * ABI 5: out_rows (optional, tiled operands only) routes key slot s of slice bh to row
+ * out_rows[bh, s] of [B*T*H, D] dk / dv tables for every s < T_kv, pad slots included:
+ * with the static QK compaction every dropped key has a pad slot whose dK / dV row is
+ * zero, so the call writes every row and no zero-fill of dropped rows is needed.      */
 int scfa_attn_bwd_dkdv(const void* q, const void* k, const void* v, const void* d_out, int64_t BH,
                        int64_t T_q, int64_t T_kv, int64_t D, const int32_t* k_idx,
                        const int32_t* k_runs, int64_t Tq_pad, int64_t Tkv_pad, const float* lse2,
                        const float* delta, const uint16_t* list, const int32_t* list_count,
                        int64_t list_stride, float scale, int64_t H, int64_t T_out, int out_boundary,
                        float* dk, float* dv, const int32_t* q_rows, const int32_t* k_rows,
-                       int64_t R_q, int64_t R_kv, void* stream);
+                       int64_t R_q, int64_t R_kv, const int32_t* out_rows, void* stream);
 
 /* Single-pass backward (ABI 5): dQ, dK, dV in one key-stationary sweep over the dK/dV
  * schedule (_kernel.py:139-193 with both of its passes fused).  Arguments as

@@ -390,7 +390,7 @@ def attention_backward(problem, q, k, v, outputs, d_out, scale=None, boundary=No
             _lib.ptr(q), _lib.ptr(k), _lib.ptr(v), _lib.ptr(d_sorted), BH, T_q, T_kv, D,
             _lib.ptr(problem.k_idx), _lib.ptr(sched["k_runs"]), problem.Tq_pad, problem.Tkv_pad,
             _lib.ptr(lse2), _lib.ptr(delta), _lib.ptr(lst), _lib.ptr(cnt), stride,
-            _scale(scale, D), H, Tkv_out, out_b, _lib.ptr(dk), _lib.ptr(dv), *rargs, _lib.stream_ptr(),
+            _scale(scale, D), H, Tkv_out, out_b, _lib.ptr(dk), _lib.ptr(dv), *rargs, None, _lib.stream_ptr(),
         )
     return dq, dk, dv
 
@@ -422,9 +422,10 @@ def dq_backward_gathered(problem, q, k_sorted, v_sorted, outputs, d_out, rows, s
     return dq, delta
 
 
-def dkdv_backward_sorted(problem, q_sorted, k_sorted, v_sorted, do_sorted, lse2, delta, scale, T_out):
+def dkdv_backward_sorted(problem, q_sorted, k_sorted, v_sorted, do_sorted, lse2, delta, scale, T_out, out_rows=None):
     """dK / dV from bucket-order (B, H, T, D) copies, written to their original positions of
-    (B, T_out, H, D) fp32 tensors."""
+    (B, T_out, H, D) fp32 tensors.  out_rows (BH, Tkv_pad) int32: route every key slot, pads
+    included, through this row table (each row of dK / dV is then written)."""
     B, H, D = problem.B, problem.H, problem.D
     T_q, T_kv = problem.T_q, problem.T_kv
     dev = k_sorted.device
@@ -440,7 +441,7 @@ def dkdv_backward_sorted(problem, q_sorted, k_sorted, v_sorted, do_sorted, lse2,
         _lib.ptr(q_sorted), _lib.ptr(k_sorted), _lib.ptr(v_sorted), _lib.ptr(do_sorted), BH, T_q, T_kv, D,
         _lib.ptr(problem.k_idx), _lib.ptr(sched["k_runs"]), problem.Tq_pad, problem.Tkv_pad,
         _lib.ptr(lse2), _lib.ptr(delta), _lib.ptr(lst), _lib.ptr(cnt), stride,
-        _scale(scale, D), H, T_out, 1, _lib.ptr(dk), _lib.ptr(dv), *_NO_ROWS, _lib.stream_ptr(),
+        _scale(scale, D), H, T_out, 1, _lib.ptr(dk), _lib.ptr(dv), *_NO_ROWS, _lib.ptr(out_rows), _lib.stream_ptr(),
     )
     return dk, dv
 

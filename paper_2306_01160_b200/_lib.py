@@ -71,7 +71,7 @@ _SIGS = {
     "scfa_debug_timing": [_P, _L],
     "scfa_debug_ctas_per_sm": [_I, _L],
     "scfa_attn_bwd_dkdv": [_P, _P, _P, _P, _L, _L, _L, _L, _P, _P, _L, _L, _P, _P, _P, _P, _L, _F, _L, _L,
-                           _I, _P, _P, _P, _P, _L, _L, _P],
+                           _I, _P, _P, _P, _P, _L, _L, _P, _P],
 }
 
 _lib = None

@@ -187,6 +187,8 @@ struct AttnArgs {
   const float* lse2;           // (BH, Tq_pad), log2 domain; +inf where no key is visible
   const float* delta;          // (BH, Tq_pad)
   const int* x_rows;  // gather mode: global row per stationary slot (BH, T_rows_pad); null = tiled loads
+  const int* out_rows;  // optional output routing: global row of each stationary slot (BH, T_rows_pad), pad
+                        // slots included (every row of the [R, D] output is written; tiled loads)
   const int* y_rows;  // gather mode: global row per streamed slot (BH, T_cols_pad)
   int x_writeout;              // gather mode: write a gathered stationary tile out through tm_xo (kernel
                                // order): FWD its Q, DQ its dO (the tensors dK/dV streams)
@@ -232,6 +234,10 @@ SCFA_DEVICE int item_of(const AttnArgs& a, int w) {
 // (bh, row) or boundary layout (b, pos, h) — the fused inverse scatter.
 SCFA_DEVICE bool out_row(const AttnArgs& a, int bh, int row, int pos, size_t& off) {
   if (row >= a.T_rows) return false;
+  if (a.out_rows) {  // routing table: pad slots map to the positions they stand for (zero rows)
+    off = static_cast<size_t>(a.out_rows[static_cast<size_t>(bh) * a.T_rows_pad + row]);
+    return true;
+  }
   if (a.x_rows) {  // row tables: `pos` is the global row the stationary operand came from
     off = static_cast<size_t>(pos);
     return true;
@@ -1488,6 +1494,7 @@ static int launch_mode(const AttnLaunch& L, cudaStream_t stream) {
   a.row_idx = L.row_idx;
   a.row_runs = reinterpret_cast<const int2*>(L.row_runs);
   a.x_rows = L.x_rows;
+  a.out_rows = L.out_rows;
   a.y_rows = L.y_rows;
   a.x_writeout = writeout ? 1 : 0;
   a.o_src = static_cast<const __nv_bfloat16*>(L.o_src);

@@ -215,12 +215,17 @@ extern "C" int scfa_attn_bwd_dkdv(const void* q, const void* k, const void* v, c
                                   const uint16_t* list, const int32_t* list_count, int64_t list_stride, float scale,
                                   int64_t H, int64_t T_out, int out_boundary, float* dk, float* dv,
                                   const int32_t* q_rows, const int32_t* k_rows, int64_t R_q, int64_t R_kv,
-                                  void* stream) {
+                                  const int32_t* out_rows, void* stream) {
   int rc = check_attn_args(BH, T_q, T_kv, D, Tq_pad, Tkv_pad, q, k, v);
   if (rc) return rc;
   if (BH == 0 || T_kv == 0) return SCFA_OK;
+  if (out_rows && k_rows) {
+    set_error("attn_bwd_dkdv: out_rows is for tiled operands (row tables route by k_rows)");
+    return SCFA_ERR_PARAM;
+  }
   AttnLaunch L{};
   L.mode = 2;  // rows = keys
+  L.out_rows = out_rows;
   L.D = static_cast<int>(D);
   L.BH = static_cast<int>(BH);
   L.H = static_cast<int>(H);

@@ -34,6 +34,7 @@ struct AttnLaunch {
   const float* delta;
   const int* x_rows;   // gather mode: global row of each stationary slot (BH, T_rows_pad); null = tiled
   const int* y_rows;   // gather mode: global row of each streamed slot (BH, T_cols_pad)
+  const int* out_rows; // optional output routing table of the stationary slots (BH, T_rows_pad)
   long long x_nrows;   // rows of the x / out row tables (gather mode)
   long long y_nrows;   // rows of the y row tables
   void* x_out;         // FWD gather mode: stationary Q rows written back in kernel order (BH, T_rows, D)

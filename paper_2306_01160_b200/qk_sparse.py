@@ -212,7 +212,14 @@ def _prepare_static(q, k, v, q_keep, k_keep, err):
     q_aux = _aux(q_perm, cnt[:BH], B, H, T_Q, QUERY_PAD, _OOB_Q)
     k_aux = _aux(k_perm, cnt[BH:], B, H, T_KV, KEY_PAD, _OOB_K)
     problem = Problem(B, H, T_Q, T_KV, D, q_aux, k_aux)
-    k_c, v_c = _gather(k, k_perm, T_KV), _gather(v, k_perm, T_KV)
+    if k.stride(3) == 1 and k.is_contiguous() and v.is_contiguous():
+        # every position has a slot: move K / V rows in memory order to their slots (one rank
+        # read per row for both tensors, scfa_permute_rows3)
+        from .hash_sparse import _permute3
+
+        k_c, v_c = _permute3([k, v], [k_rank, k_rank], T_KV)
+    else:
+        k_c, v_c = _gather(k, k_perm, T_KV), _gather(v, k_perm, T_KV)
     problem.rows = make_row_tables(q_perm, k_perm, B, H, T_Q, T_KV, T_Q, T_KV, problem.Tq_pad, problem.Tkv_pad)
     return QkPrepared(
         q_c=q, k_c=k_c, v_c=v_c,
@@ -308,7 +315,7 @@ class _QkState:
     """What the QK backward stage needs from the forward stage."""
 
     __slots__ = ("prob", "prep", "q", "xq", "outputs", "rows", "q_only", "scale", "T_Q", "T_KV", "q_keep", "k_keep",
-                 "err")
+                 "err", "static")
 
 
 def _qk_forward_stage(q, k, v, q_keep, k_keep, scale=None, row_tables=False):
@@ -327,12 +334,14 @@ def _qk_forward_stage(q, k, v, q_keep, k_keep, scale=None, row_tables=False):
     if q.dim() != 4 or k.dim() != 4 or k.shape != v.shape or q.shape[0] != k.shape[0] or q.shape[2:] != k.shape[2:]:
         raise ShapeError(f"operand shapes disagree: {tuple(q.shape)}, {tuple(k.shape)}, {tuple(v.shape)}")
     st.err = torch.zeros(1, dtype=torch.int32, device=q.device)
+    st.static = False
     if row_tables:
         st.prep, mode = qk_preprocess(q, k, v, q_keep, k_keep, materialize=False), "rows"
     elif st.T_Q == 0:
         st.prep, mode = qk_preprocess(q, k, v, q_keep, k_keep), "sorted"
     else:
         st.prep, mode = _prepare_static(q, k, v, q_keep, k_keep, st.err), "gathered"
+        st.static = True
     st.prob = prob = st.prep.problem
     prob.schedule("fwd", "dq", "dkdv")
     st.q = q
@@ -345,7 +354,10 @@ def _qk_forward_stage(q, k, v, q_keep, k_keep, scale=None, row_tables=False):
         st.rows = prob.rows if mode == "rows" else None
         st.outputs = attention_forward(prob, st.prep.q_c, st.prep.k_c, st.prep.v_c, scale,
                                        boundary=(st.T_Q, False), rows=st.rows, err=st.err)
-    _zero_dropped_rows(q_keep, st.outputs.O)
+    if not st.static:
+        # static sizing: every dropped position has a pad slot whose (zero) output row the
+        # epilogue writes through the row table, so nothing is left to clear
+        _zero_dropped_rows(q_keep, st.outputs.O)
     return st
 
 
@@ -362,12 +374,13 @@ def _qk_backward_stage(st, d_out):
         dq, delta = dq_backward_gathered(prob, st.q, prep.k_c, prep.v_c, st.outputs, d_b, st.q_only, st.scale,
                                          st.T_Q, xdo)
         dk, dv = dkdv_backward_sorted(prob, st.xq, prep.k_c, prep.v_c, xdo, st.outputs._lse2, delta, st.scale,
-                                      st.T_KV)
+                                      st.T_KV, out_rows=prob.rows.k_rows if st.static else None)
     else:
         dq, dk, dv = attention_backward(prob, prep.q_c, prep.k_c, prep.v_c, st.outputs, d_b, st.scale,
                                         boundary=(st.T_Q, st.T_KV, False), rows=st.rows)
-    _zero_dropped_rows(st.q_keep, dq)
-    _zero_dropped(st.k_keep, dk, dv)
+    if not st.static:  # (static: pad slots wrote the dropped rows' zeros)
+        _zero_dropped_rows(st.q_keep, dq)
+        _zero_dropped(st.k_keep, dk, dv)
     return dq, dk, dv
 
 

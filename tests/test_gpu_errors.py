@@ -118,3 +118,23 @@ def test_host_results_are_complete_on_return():
     for a, b in zip(got, want):
         assert not a.is_cuda
         assert torch.equal(a, b.cpu())
+
+
+def test_contract_narrowing_at_the_boundary():
+    """The engine's documented limits raise the reference's ShapeError: head dim > 128
+    (the tcgen05 tiles take 64 / 128; the reference takes any D) and bucket ids >= 2**31
+    (int32 keys; the reference sorts int64, hash_sparse.py:93-94)."""
+    q, k, v, dO = _qkv(D=64)
+    wide = torch.zeros((1, 200, 2, 160), device="cuda", dtype=torch.bfloat16)
+    ids = _ids()
+    with pytest.raises(scfa.ShapeError):
+        scfa.hash_sparse_attention(wide, wide, wide, ids, ids)
+    with pytest.raises(scfa.ShapeError):
+        scfa.qk_sparse_attention(wide, wide, wide, torch.ones((1, 200, 2)), torch.ones((1, 200, 2)))
+    big = ids.clone()
+    big[0, 5, 0] = 2 ** 31
+    qe, ke, ve = (x.transpose(1, 2).contiguous() for x in (q, k, v))
+    with pytest.raises(scfa.ShapeError):
+        scfa.sort_by_bucket(qe, ke, ve, big.transpose(1, 2), big.transpose(1, 2))
+    with pytest.raises(scfa.ShapeError):
+        scfa.hash_sparse_attention(q, k, v, big, big)
