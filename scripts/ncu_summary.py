@@ -69,6 +69,7 @@ def main():
     ap.add_argument("--launches", default=os.path.join(ROOT, "gpurun_out", "launches.csv"))
     ap.add_argument("--bench", default=os.path.join(ROOT, "gpurun_out", "bench.json"))
     ap.add_argument("--note", default="")
+    ap.add_argument("--no-traffic", action="store_true", help="do not update profiles/ncu_traffic.json")
     a = ap.parse_args()
     md = [f"# Profile {a.tag}", ""]
     if a.note:
@@ -95,6 +96,11 @@ def main():
                 v = r[col[m]] if m in col else ""
                 try:
                     f = float(v.replace(",", ""))
+                    unit = units[col[m]] if m in col else ""
+                    if m == "gpu__time_duration.sum":  # to microseconds whatever ncu chose
+                        f *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(unit, 1.0)
+                    elif m.startswith("dram__bytes"):  # to MB
+                        f *= {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(unit, 1.0)
                     vals.append(f"{f:.1f}")
                 except ValueError:
                     vals.append(v)
@@ -113,7 +119,7 @@ def main():
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     with open(os.path.join(ROOT, "profiles", f"{a.tag}.md"), "w") as f:
         f.write("\n".join(md) + "\n")
-    if traffic:
+    if traffic and not a.no_traffic:
         path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         old = json.load(open(path)) if os.path.exists(path) else {}
         old.update(traffic)
