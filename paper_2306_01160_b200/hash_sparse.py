@@ -582,7 +582,25 @@ def _copy_streams(dev):
     return _COPY_STREAMS[dev]
 
 
+_TRACE = None  # diagnostics: a list receives (name, stream event) marks of the host-streaming timeline
+
+
+def _mark(name, stream):
+    if _TRACE is not None:
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        _TRACE.append((name, e))
+
+
 def _fwd_bwd_host(q, k, v, q_hash, k_hash, d_out, scale, exclude_self, out, check=True, single_pass=False):
+    """Host tensors in, host results out: batch elements streamed over three CUDA streams —
+    upload, attention, download of consecutive elements overlap (every (b, h) slice is
+    independent, hash_sparse.py:223-238, so the results equal one whole-batch call).
+
+    The call is bound by the download of the fp32 gradients; what the link cannot hide is
+    the lead before the first download.  So each element's Q / K / V / ids go up before its
+    dO, the forward runs as soon as they are there, and O goes down while dO is still on
+    its way and the backward runs (the gradients follow)."""
     dev = torch.device("cuda", torch.cuda.current_device())
     B, T, H, D = q.shape
     same = k_hash is q_hash
@@ -599,24 +617,42 @@ def _fwd_bwd_host(q, k, v, q_hash, k_hash, d_out, scale, exclude_self, out, chec
     for b in range(B):
         sl = slice(b, b + 1)
         with torch.cuda.stream(h2d):
-            xs = [t[sl].to(dev, non_blocking=True) for t in (q, k, v, d_out, q_hash)]
-            kh = xs[4] if same else k_hash[sl].to(dev, non_blocking=True)
-            ready = torch.cuda.Event()
-            ready.record(h2d)
-        comp.wait_event(ready)
-        for t in xs + [kh]:
+            _mark(f"h2d{b}", h2d)
+            xs = [t[sl].to(dev, non_blocking=True) for t in (q, k, v, q_hash)]
+            kh = xs[3] if same else k_hash[sl].to(dev, non_blocking=True)
+            ready_f = torch.cuda.Event()
+            ready_f.record(h2d)
+            do_b = d_out[sl].to(dev, non_blocking=True)
+            ready_b = torch.cuda.Event()
+            ready_b.record(h2d)
+            _mark(f"h2d{b}-end", h2d)
+        comp.wait_event(ready_f)
+        for t in xs + [kh, do_b]:
             t.record_stream(comp)
-        outputs, dq, dk, dv, _ = _fwd_bwd(xs[0], xs[1], xs[2], xs[4], kh, xs[3], scale, exclude_self,
-                                          single_pass=single_pass)
-        errs.append(outputs._err)
+        _mark(f"fwd{b}", comp)
+        st = _hash_forward_stage(xs[0], xs[1], xs[2], xs[3], kh, scale, exclude_self, single_pass=single_pass)
+        fwd_done = torch.cuda.Event()
+        fwd_done.record(comp)
+        with torch.cuda.stream(d2h):
+            d2h.wait_event(fwd_done)
+            _mark(f"d2h{b}", d2h)
+            out[0][sl].copy_(st.outputs.O, non_blocking=True)
+            st.outputs.O.record_stream(d2h)
+        comp.wait_event(ready_b)
+        _mark(f"bwd{b}", comp)
+        dq, dk, dv = _hash_backward_stage(st, do_b)
+        st.outputs._err = st.err
+        errs.append(st.err)
+        _mark(f"bwd{b}-end", comp)
         done = torch.cuda.Event()
         done.record(comp)
         with torch.cuda.stream(d2h):
             d2h.wait_event(done)
-            for dst, src in zip(out, (outputs.O, dq, dk, dv)):
+            for dst, src in zip(out[1:], (dq, dk, dv)):
                 dst[sl].copy_(src, non_blocking=True)
                 src.record_stream(d2h)
-        keep.append((xs, kh, outputs, dq, dk, dv))
+            _mark(f"d2h{b}-end", d2h)
+        keep.append((xs, kh, do_b, st, dq, dk, dv))
     comp.wait_stream(d2h)
     # the reference API is synchronous: the host results are complete on return
     comp.synchronize()

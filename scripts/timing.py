@@ -73,6 +73,10 @@ torch.cuda.synchronize()
 _lib.EVENT_HOOK = None
 print("ctas/sm", [lib.scfa_debug_ctas_per_sm(m, 64) for m in range(3)])
 
+os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+np.savez_compressed(os.path.join(ROOT, "gpurun_out", f"timing_{MODE}.npz"),
+                    **{n: b.cpu().numpy() for n, b in bufs.items()},
+                    ctas_per_sm=np.array([lib.scfa_debug_ctas_per_sm(m, 64) for m in range(3)]))
 med = lambda x: float(np.median(x)) if len(x) else float("nan")
 for name, buf in bufs.items():
     d = buf.view(grid, TILES, SLOTS).cpu().numpy().astype(np.float64)
