@@ -508,6 +508,10 @@ __global__ void __cluster_dims__(kSortCluster, 1, 1) __launch_bounds__(kSortThre
     C.dbase[d] = incl - gsum;
   }
   __syncthreads();
+  // this CTA is done reading the others' shared memory: a relaxed arrive now, the matching
+  // wait at exit (a full cluster.sync there would also wait for every scattered global
+  // write below to be acknowledged)
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   if (threadIdx.x < 256) {
     int wofs = 0;
     for (int w = 0; w < warp; ++w) wofs += C.wsum[w];
@@ -540,7 +544,7 @@ __global__ void __cluster_dims__(kSortCluster, 1, 1) __launch_bounds__(kSortThre
     if (threadIdx.x < 256) bounds[threadIdx.x] = C.dbase[threadIdx.x];
     if (threadIdx.x == 0) bounds[256] = T;
   }
-  cluster.sync();  // the other CTAs' reads of this CTA's shared memory are done
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // the others' reads of this CTA's smem are done
 }
 
 // Kernel 2 (one thread per slot, all slices): sorted vectors, rank and visibility runs.
