@@ -87,6 +87,11 @@ struct Cfg {
   // measured: dK/dV gains; dQ loses at D = 64 (two streams beat one MMA issuer) but gains at
   // D = 128, where TMEM holds only one dQ stream anyway
   static constexpr bool FUSED = (kMode == MODE_BWD);
+  // FWD at D = 128 (one item stream: TMEM holds one S + O set): the two row warpgroups split
+  // each 128-column S tile by columns, each with its own running max / sum and its own O
+  // accumulator (O0 += P[:, :64] V[:64], O1 += P[:, 64:] V[64:]); the epilogue combines
+  // O = (2^(m0-m) O0 + 2^(m1-m) O1) / (2^(m0-m) l0 + 2^(m1-m) l1).
+  static constexpr bool SPLIT = (kMode == MODE_FWD && kD == 128);
   static constexpr bool KEYS = (kMode == MODE_DKDV || kMode == MODE_BWD);  // key-stationary
   static constexpr bool ALT = KEYS || (kMode == MODE_DQ && kD == 128);
   static constexpr int NSTREAM = ALT ? 1 : ((kD == 64) ? 2 : 1);
@@ -130,7 +135,7 @@ struct Cfg {
   static constexpr int TM_S = 0;
   static constexpr int TM_DP = (kMode == MODE_FWD) ? 0 : BN;
   static constexpr int TM_ACC = ALT ? NBUF * TM_BUF : 128;
-  static constexpr int ACC_COLS = KEYS ? 2 * kD : kD;
+  static constexpr int ACC_COLS = (KEYS || SPLIT) ? 2 * kD : kD;
   static constexpr int P_COLS = KEYS ? BN : BN / 2;
   static constexpr bool OVERLAP = !ALT && (TM_ACC + ACC_COLS + P_COLS <= TM_STREAM);
   static constexpr int TM_P = OVERLAP ? TM_ACC + ACC_COLS : TM_S;                 // P | dS | P^T
@@ -166,10 +171,13 @@ struct Cfg {
   // ticket, entries {int4 info, float inv_l[32]}
   static constexpr int QE = SCFA_TUNE_QE;
   static constexpr int OFF_EQ = OFF_CTRL + NSTREAM * CTRL_BYTES;
-  static constexpr int EQ_ENTRY = 16 + 4 * 32;
+  static constexpr int EQ_ENTRY = 16 + 4 * 32 + (SPLIT ? 4 * 32 : 0);  // info, inv_l[32] (SPLIT: + a1[32])
+  // SPLIT: the second warpgroup's (m_run, l_run, m_true) per row for the item's combine, by item parity
+  static constexpr int XCH_BYTES = SPLIT ? 2 * 3 * BM * 4 : 0;
   static constexpr int EQQ_BYTES = 16 * QE + 16 + QE * EQ_ENTRY;  // one quadrant
   static constexpr int EQ_BYTES = 4 * EQQ_BYTES;
-  static constexpr int SMEM_BYTES = OFF_EQ + EQ_BYTES + 16;
+  static constexpr int OFF_XCH = OFF_EQ + EQ_BYTES;
+  static constexpr int SMEM_BYTES = OFF_XCH + XCH_BYTES + 16;
   static_assert(X_BYTES % 1024 == 0 && Y_BYTES % 1024 == 0, "TMA tiles must stay 1024-aligned");
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
   // epilogue staging reuses the item's stationary slot
@@ -425,7 +433,7 @@ SCFA_DEVICE void epilogue_wg(const AttnArgs& args, uint8_t* smem_base, uint32_t 
     {
       int s;
       int2 item;
-      float inv_l = 0.f;
+      float inv_l = 0.f, a1 = 0.f;  // SPLIT: O = inv_l * O0 + a1 * O1
       if (C::ALT) {  // one stream: follow its work ring (items finish in ring order)
         s = 0;
         const Bars B0 = bars_of<C>(smem_base + C::OFF_CTRL);
@@ -460,6 +468,7 @@ SCFA_DEVICE void epilogue_wg(const AttnArgs& args, uint8_t* smem_base, uint32_t 
         const uint8_t* ent = eqb + 16 * C::QE + 16 + slot * C::EQ_ENTRY;
         const int4 info = *reinterpret_cast<const int4*>(ent);
         inv_l = reinterpret_cast<const float*>(ent + 16)[lane];
+        if (C::SPLIT) a1 = reinterpret_cast<const float*>(ent + 16 + 128)[lane];
         mbar_arrive(eq + C::QE + slot);
         if (info.y < 0) {  // a stream's end
           --live_streams;
@@ -529,11 +538,21 @@ SCFA_DEVICE void epilogue_wg(const AttnArgs& args, uint8_t* smem_base, uint32_t 
         for (int c = 0; c < kD; c += 32) {
           uint32_t v[32];
           tmem_ld32(t_acc + c, v);
-          tmem_wait_ld();
+          if (C::SPLIT) {
+            uint32_t u[32];
+            tmem_ld32(t_acc + kD + c, u);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              v[i] = __float_as_uint(fmaf(__uint_as_float(v[i]), inv_l, __uint_as_float(u[i]) * a1));
+          } else {
+            tmem_wait_ld();
+          }
           uint32_t w[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            const float o0 = __uint_as_float(v[2 * i]) * inv_l, o1 = __uint_as_float(v[2 * i + 1]) * inv_l;
+            const float o0 = C::SPLIT ? __uint_as_float(v[2 * i]) : __uint_as_float(v[2 * i]) * inv_l;
+            const float o1 = C::SPLIT ? __uint_as_float(v[2 * i + 1]) : __uint_as_float(v[2 * i + 1]) * inv_l;
             finite_ok &= (fabsf(o0) <= FLT_MAX) & (fabsf(o1) <= FLT_MAX);
             w[i] = pack_bf16(o0, o1);
           }
@@ -624,7 +643,7 @@ __global__ void __launch_bounds__(512, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int wg = warp >> 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_base + C::OFF_EQ + C::EQ_BYTES);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_base + C::OFF_XCH + C::XCH_BYTES);
 
   if (threadIdx.x == 0) {
     if (smem_u32(smem_base) & 1023) __trap();  // TMA SWIZZLE_128B destinations need 1024-byte alignment
@@ -632,10 +651,10 @@ __global__ void __launch_bounds__(512, 1)
       const Bars b = bars_of<C>(smem_base + C::OFF_CTRL + st * C::CTRL_BYTES);
       for (int j = 0; j < 3; ++j) {
         mbar_init(b.s_full + j, 1);
-        mbar_init(b.p_full + j, 128);
+        mbar_init(b.p_full + j, C::SPLIT ? 256 : 128);
         mbar_init(b.p_free + j, 1);
       }
-      mbar_init(b.s_free, 128);
+      mbar_init(b.s_free, C::SPLIT ? 256 : 128);
       mbar_init(b.acc_full, 1);
       mbar_init(b.o_free, 128);  // epilogue threads: accumulators read, the next item may overwrite
       for (int i = 0; i < C::NXS; ++i) {
@@ -658,7 +677,7 @@ __global__ void __launch_bounds__(512, 1)
       for (int i = 0; i < C::NQ; ++i) {
         mbar_init(b.q_full + i, 1);
         // the MMA thread + the row threads (+ the second row warpgroup and the epilogue in ALT)
-        mbar_init(b.q_empty + i, C::ALT ? 1 + 128 + 128 + 128 : 1 + 128);
+        mbar_init(b.q_empty + i, C::ALT ? 1 + 128 + 128 + 128 : (C::SPLIT ? 1 + 256 : 1 + 128));
       }
     }
     for (int q = 0; q < 4; ++q) {
@@ -681,9 +700,9 @@ __global__ void __launch_bounds__(512, 1)
   // Register rebalancing happens first thing inside each warpgroup's branch (nothing
   // live across it, no merge after it): the row warpgroups take the file the epilogue /
   // producer / MMA warps do not need.
-  constexpr int kRowRegs = (C::NSTREAM == 2 || C::ALT) ? 176 : 240;
-  const int s = C::ALT ? 0 : ((wg < 2) ? wg : ((warp >= 12) ? ((warp - 12) >> 1) : 0));
-  const bool active = C::ALT ? (wg < 2 || ((warp - 12) >> 1) == 0) : (s < C::NSTREAM);
+  constexpr int kRowRegs = (C::NSTREAM == 2 || C::ALT || C::SPLIT) ? 176 : 240;
+  const int s = (C::ALT || C::SPLIT) ? 0 : ((wg < 2) ? wg : ((warp >= 12) ? ((warp - 12) >> 1) : 0));
+  const bool active = (C::ALT || C::SPLIT) ? (wg < 2 || ((warp - 12) >> 1) == 0) : (s < C::NSTREAM);
   if (wg == 3) {
    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
    if (((warp - 12) & 1) == 0 && active) {
@@ -840,9 +859,11 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
         for (int k = 0; k < C::BN / 16; ++k) {
           const uint32_t on = (!first || k > 0);
-          if (kMode == MODE_FWD) {  // O += P V
-            umma_ts(acc, pb + C::TM_P + k * 8, make_sdesc_sw128(y1_addr + k * 2048, C::BN * 128, 1024), idesc_acc,
-                    on);
+          if (kMode == MODE_FWD) {  // O += P V  (SPLIT: keys [0, 64) into O0, [64, 128) into O1)
+            const uint32_t acc_k = (C::SPLIT && k >= C::BN / 32) ? acc + kD : acc;
+            const uint32_t on_k = C::SPLIT ? static_cast<uint32_t>(!first || (k % (C::BN / 32)) > 0) : on;
+            umma_ts(acc_k, pb + C::TM_P + k * 8, make_sdesc_sw128(y1_addr + k * 2048, C::BN * 128, 1024), idesc_acc,
+                    on_k);
           } else if (kMode == MODE_DQ) {  // dQ += dS K
             umma_ts(acc, pb + C::TM_P + k * 8, make_sdesc_sw128(y0_addr + k * 2048, C::BN * 128, 1024), idesc_acc,
                     on);
@@ -1004,7 +1025,7 @@ __global__ void __launch_bounds__(512, 1)
     // hand an item (or the stream's end, lb = -1) to the epilogue queue: a ticket per
     // item keeps one queue for both streams in completion order
     int tg = 0, ia = 0;
-    auto handoff = [&](int lb_, int n_, float inv_l_) {
+    auto handoff = [&](int lb_, int n_, float inv_l_, float a1_ = 0.f) {
       // per row warp: quadrant (warp & 3) of the item goes to epilogue warp (warp & 3)
       uint8_t* eqb = smem_base + C::OFF_EQ + (warp & 3) * C::EQQ_BYTES;
       int tk = 0;
@@ -1015,6 +1036,7 @@ __global__ void __launch_bounds__(512, 1)
       if (tk >= C::QE) mbar_wait(eq + C::QE + slot, ((tk / C::QE) - 1) & 1);
       uint8_t* ent = eqb + 16 * C::QE + 16 + slot * C::EQ_ENTRY;
       reinterpret_cast<float*>(ent + 16)[lane] = inv_l_;
+      if (C::SPLIT) reinterpret_cast<float*>(ent + 16 + 128)[lane] = a1_;
       if (lane == 0) *reinterpret_cast<int4*>(ent) = make_int4(s, lb_, n_, 0);
       mbar_arrive(eq + slot);
     };
@@ -1074,6 +1096,9 @@ __global__ void __launch_bounds__(512, 1)
         // Chunks no row of the warp can see are skipped (P = 0, no exponentials).
         constexpr float kLag = 64.f;
         constexpr int NCH = C::BN / 32;
+        constexpr int NCH_W = C::SPLIT ? NCH / 2 : NCH;  // chunks of each tile this warpgroup owns
+        const int ch0 = C::SPLIT ? wg * NCH_W : 0;
+        const uint32_t t_accw = t_acc + (C::SPLIT ? static_cast<uint32_t>(wg * kD) : 0u);  // its O
         const bool neg = sl < 0.f;  // a negative scale turns the row max into a row min
         const float mask_val = neg ? INFINITY : NEG_INF;
         float m_run = NEG_INF;   // log2-domain exponent base (lags the max by < kLag)
@@ -1092,14 +1117,15 @@ __global__ void __launch_bounds__(512, 1)
           float la[4] = {0.f, 0.f, 0.f, 0.f};
           bool p_ready = (tg == 0);  // P columns free: the previous tile's PV has read them
 #pragma unroll
-          for (int ch = 0; ch < NCH; ++ch) {
+          for (int chl = 0; chl < NCH_W; ++chl) {
+            const int ch = ch0 + chl;
             const uint32_t wv = full ? 0xffffffffu : (bits_below(rhi - 32 * ch) & ~bits_below(rlo - 32 * ch));
             uint32_t pk[16];
             if (__any_sync(0xffffffffu, wv != 0u)) {
               float x[32];
               tmem_ld32(t_s + 32 * ch, *reinterpret_cast<uint32_t(*)[32]>(x));
               tmem_wait_ld();
-              if (ch == NCH - 1) {
+              if (chl == NCH_W - 1) {
                 tc_fence_before();
                 mbar_arrive(bar_s_free);  // S fully read: the next tile's S may overwrite it
               }
@@ -1140,7 +1166,7 @@ __global__ void __launch_bounds__(512, 1)
                   }
                   tmem_wait_st();
 #pragma unroll 1
-                  for (int j = 0; j < ch; ++j) {
+                  for (int j = ch0; j < ch; ++j) {
                     uint32_t q16[16];
                     tmem_ld16(t_p + 16 * j, q16);
                     tmem_wait_ld();
@@ -1154,7 +1180,7 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll 1
                   for (int c = 0; c < kD; c += 32) {
                     uint32_t v[32];
-                    tmem_ld32(t_acc + c, v);
+                    tmem_ld32(t_accw + c, v);
                     tmem_wait_ld();
 #pragma unroll
                     for (int i = 0; i < 32; i += 2) {
@@ -1163,7 +1189,7 @@ __global__ void __launch_bounds__(512, 1)
                       v[i] = __float_as_uint(o0);
                       v[i + 1] = __float_as_uint(o1);
                     }
-                    tmem_st32(t_acc + c, v);
+                    tmem_st32(t_accw + c, v);
                   }
                   tmem_wait_st();
                 }
@@ -1187,7 +1213,7 @@ __global__ void __launch_bounds__(512, 1)
                 pk[c >> 1] = pack_bf16(a0, a1);
               }
             } else {
-              if (ch == NCH - 1) {
+              if (chl == NCH_W - 1) {
                 tc_fence_before();
                 mbar_arrive(bar_s_free);
               }
@@ -1208,9 +1234,40 @@ __global__ void __launch_bounds__(512, 1)
           SCFA_STAMP(2);
         }
         // ---------------- hand O / l to the epilogue warpgroup; write M, L, lse2 here
-        const float inv_l = (l_run > 0.f) ? rcp_approx(l_run) : 0.f;
+        float inv_l, a1 = 0.f;
+        if (C::SPLIT) {
+          // the two warpgroups' statistics of each row meet here; the second one is done
+          if (wg == 1) {
+            if (n > 0) {
+              float* xch = reinterpret_cast<float*>(smem_base + C::OFF_XCH) + (ia & 1) * 3 * C::BM;
+              xch[r] = m_run;
+              xch[C::BM + r] = l_run;
+              xch[2 * C::BM + r] = m_true;
+              named_bar_sync(1, 256);
+              ++ia;
+            }
+            continue;
+          }
+          float e0 = 0.f, e1 = 0.f;
+          if (n > 0) {
+            named_bar_sync(1, 256);
+            const float* xch = reinterpret_cast<const float*>(smem_base + C::OFF_XCH) + (ia & 1) * 3 * C::BM;
+            const float m1 = xch[r], l1 = xch[C::BM + r], t1 = xch[2 * C::BM + r];
+            const float mr = fmaxf(m_run, m1);
+            e0 = (m_run == NEG_INF) ? 0.f : ex2(m_run - mr);
+            e1 = (m1 == NEG_INF) ? 0.f : ex2(m1 - mr);
+            l_run = l_run * e0 + l1 * e1;
+            m_run = mr;
+            m_true = fmaxf(m_true, t1);
+          }
+          const float inv = (l_run > 0.f) ? rcp_approx(l_run) : 0.f;
+          inv_l = e0 * inv;  // O0's factor; O1's is a1
+          a1 = e1 * inv;
+        } else {
+          inv_l = (l_run > 0.f) ? rcp_approx(l_run) : 0.f;
+        }
         if (n > 0) {
-          handoff(lb, n, inv_l);
+          handoff(lb, n, inv_l, a1);
           ++ia;
         } else if (live) {
           uint4* dst = reinterpret_cast<uint4*>(args.out_o + orow * kD);
@@ -1406,7 +1463,7 @@ __global__ void __launch_bounds__(512, 1)
         }
       }
     }
-    if (!C::ALT) handoff(-1, 0, 0.f);  // end of the stream
+    if (!C::ALT && (!C::SPLIT || wg == 0)) handoff(-1, 0, 0.f);  // end of the stream
   }
 
   tc_fence_before();
