@@ -9,8 +9,8 @@ qk (configs[2]): drop rate 0..90% of queries and keys per head at T = 16384, B =
 
 Per point: our fwd+bwd (the fused path bench.py times, inputs resident on the GPU,
 CUDA events; hash and our dense comparator replay a CUDA graph as bench.py does — the
-eager hash time is listed too —, QK runs eagerly: its preparation reads the kept counts
-back to the host, qk_sparse.py:58), effective TFLOP/s on the visible (query, key) pairs (14 * D flops
+eager hash time is listed too —, and so does QK: its fused path sizes the compacted buffers
+statically, with no host read-back), effective TFLOP/s on the visible (query, key) pairs (14 * D flops
 per pair: fwd 4, dQ 6 incl. the recompute, dK/dV 4 ... as bench.py), our dense causal
 comparator at the same shape, and torch's SDPA (cuDNN) dense causal fwd+bwd as a
 library reference point.  Synthetic data: torch.randn Q/K/V/dO, uniform bucket ids /
@@ -76,7 +76,7 @@ def dense_times(B, T, H, D, steps, warmup):
     qe, ke, ve, de = (x.transpose(1, 2).contiguous() for x in (q, k, v, dO))
 
     def ours():
-        o = scfa.flash_forward(qe, ke, ve)
+        o = scfa.flash_forward(qe, ke, ve, check=False)
         scfa.flash_backward(qe, ke, ve, o, de)
 
     qs, ks, vs = (x.clone().requires_grad_() for x in (qe, ke, ve))
@@ -117,7 +117,8 @@ def qk_point(B, T, H, D, drop, steps, warmup):
     qkd, kkd = torch.from_numpy(qk).to(dev), torch.from_numpy(kk).to(dev)
     kc = torch.cumsum(kkd > 0, dim=1)
     p_live = int(torch.where(qkd > 0, kc, torch.zeros_like(kc)).sum())
-    ms = timed(lambda: scfa.qk_sparse_attention_fwd_bwd(q, k, v, qkd, kkd, dO), steps, warmup)
+    # static compacted sizes (no host read-back): CUDA-graph replay, as bench.py's cfg3
+    ms = timed_graph(lambda: scfa.qk_sparse_attention_fwd_bwd(q, k, v, qkd, kkd, dO, check=False), steps, warmup)
     del q, k, v, dO
     torch.cuda.empty_cache()
     d_ours, d_sdpa = dense_times(B, T, H, D, steps, warmup)
