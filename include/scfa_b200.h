@@ -67,6 +67,27 @@ int scfa_qk_compact(const void* keep, int keep_dtype, int64_t B, int64_t T, int6
                     int64_t st, int64_t sh, int32_t* perm, int32_t* rank, int32_t* counts,
                     int32_t* err_flag, void* stream);
 
+/* Fused QK preparation for the static-size fused fwd + bwd (ABI 6), one launch for what
+ * qk_preprocess does per head (pkg/src/scfa/qk_sparse.py:186-211) with the compacted buffer
+ * holding every position (kept first, in position order, then the dropped ones) instead of
+ * the max kept count (qk_sparse.py:58), so no size is read back to the host:
+ *   perm_q / rank_q (B*H, T_Q), perm_k / rank_k (B*H, T_KV) int32: argsort(~kept, stable)
+ *     (qk_sparse.py:59) and its inverse;
+ *   q_idx (B*H, Tq_pad), k_idx (B*H, Tkv_pad) int32: pad_index (qk_sparse.py:74-83) —
+ *     QUERY_PAD / KEY_PAD for dropped slots, past the end -1 / INT32_MAX;
+ *   q_runs / k_runs (B*H, T*_pad) int32 pairs: the causal visibility runs of
+ *     scfa_build_schedule (a kept query at t sees key slots [0, #kept keys <= t));
+ *   q_rows / k_rows (B*H, T*_pad) int32: slot -> row (b*T + t)*H + h of the caller's
+ *     (B, T, H, D) tensors (scfa_row_map);
+ *   counts (2*B*H) int32: kept queries per head, then kept keys.
+ * keep_q / keep_k: (B, T, H) with element strides; entries outside {0, 1} set SCFA_ERR_SHAPE in
+ * *err_flag (qk_sparse.py:54-55).  T_Q, T_KV <= 16384.                                   */
+int scfa_qk_prepare(const void* keep_q, int keep_q_dtype, int64_t sbq, int64_t stq, int64_t shq,
+                    const void* keep_k, int keep_k_dtype, int64_t sbk, int64_t stk, int64_t shk, int64_t B,
+                    int64_t T_Q, int64_t T_KV, int64_t H, int32_t* perm_q, int32_t* rank_q, int32_t* perm_k,
+                    int32_t* rank_k, int32_t* q_idx, int32_t* k_idx, int32_t* q_runs, int32_t* k_runs,
+                    int32_t* q_rows, int32_t* k_rows, int32_t* counts, int32_t* err_flag, void* stream);
+
 /* ---------------------------------------------------------------- hash prep
  * Replaces _bucket_order / sort_by_bucket's stable argsort
  * (pkg/src/scfa/hash_sparse.py:89-133).  Stable LSD radix sort per (b,h) by

@@ -23,7 +23,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # SCFA_LIB overrides the path (A/B timing of two builds); the default is the in-tree build
 LIB_PATH = os.environ.get("SCFA_LIB") or os.path.join(_HERE, "lib", "libscfa_b200.so")
 
-ABI_VERSION = 5  # include/scfa_b200.h / scfa_abi_version()
+ABI_VERSION = 6  # include/scfa_b200.h / scfa_abi_version()
 OK = 0
 ERR_SHAPE, ERR_FORMAT, ERR_PARAM, ERR_NUMERIC, ERR_CONTRACT, ERR_CUDA = 1, 2, 3, 4, 5, 6
 DT_F32, DT_F64, DT_U8, DT_I32, DT_I64, DT_BF16 = 0, 1, 2, 3, 4, 5
@@ -42,6 +42,8 @@ _P, _I, _L, _F = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_float
 # name -> argtypes (all return int status, except the two introspection calls)
 _SIGS = {
     "scfa_qk_compact": [_P, _I, _L, _L, _L, _L, _L, _L, _P, _P, _P, _P, _P],
+    "scfa_qk_prepare": [_P, _I, _L, _L, _L, _P, _I, _L, _L, _L, _L, _L, _L, _L, _P, _P, _P, _P, _P, _P, _P, _P,
+                        _P, _P, _P, _P, _P],
     "scfa_hash_sort": [_P, _I, _L, _L, _L, _L, _L, _L, _P, _I, _L, _L, _P, _P, _P, _P, _P],
     "scfa_gather_rows": [_P, _I, _L, _L, _L, _L, _L, _L, _P, _L, _L, _P, _P],
     "scfa_gather_rows3": [_I, _P, _P, _P, _P, _I, _L, _L, _L, _P, _P, _P],

@@ -92,7 +92,7 @@ static int check_attn_args(int64_t BH, int64_t T_q, int64_t T_kv, int64_t D, int
 
 using namespace scfa;
 
-extern "C" int scfa_abi_version(void) { return 5; }
+extern "C" int scfa_abi_version(void) { return 6; }
 
 extern "C" const char* scfa_last_error(void) { return g_err; }
 

@@ -115,6 +115,169 @@ __global__ void qk_compact_kernel(const void* keep, int dt, int64_t T, int64_t H
   }
 }
 
+// ------------------------------------------------------------------ fused QK preparation
+//
+// The fused QK fwd + bwd's whole index preparation for one (b, h) slice per CTA, static sizes
+// (every position has a slot: kept positions first in position order, then the dropped
+// ones, qk_sparse.py:41-71 with the buffer = T instead of the max kept count):
+//   perm / rank                       compact()'s argsort(~kept, stable) and its inverse
+//   q_idx / k_idx (padded)            pad_index (qk_sparse.py:74-83): QUERY_PAD / KEY_PAD
+//   row tables                        slot -> row of the caller's (B, T, H, D) tensors
+//   visibility runs                   causal (k_idx <= q_idx, _kernel.py:82-89): a kept query
+//                                     at position t sees key slots [0, #kept keys <= t); a
+//                                     kept key at t is seen by query slots [#kept q < t, #kept q)
+// Keep vectors are read once (every thread a contiguous segment of positions, all loads in
+// flight), one block scan per side gives the kept-before counts, and both sides' prefix
+// counts sit in shared memory so the runs need no search.  Replaces two compaction passes,
+// two aux builds, two row maps and the runs kernel (seven launches) by one.
+constexpr int kQkPrepThreads = 1024;
+constexpr int kQkPrepMaxT = 16384;
+
+SCFA_DEVICE int block_excl_scan(int v, int* sm, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int n = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += n;
+  }
+  if (lane == 31) sm[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int w = (lane < static_cast<int>(blockDim.x >> 5)) ? sm[lane] : 0;
+    int wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += n;
+    }
+    sm[lane] = wi - w;
+    if (lane == 31) sm[32] = wi;
+  }
+  __syncthreads();
+  const int r = sm[warp] + incl - v;
+  *total = sm[32];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kQkPrepThreads) qk_prepare_kernel(
+    const void* keep_q, int dtq, int64_t sbq, int64_t stq, int64_t shq, const void* keep_k, int dtk, int64_t sbk,
+    int64_t stk, int64_t shk, int T_Q, int T_KV, int Tq_pad, int Tkv_pad, int H, int32_t* perm_q, int32_t* rank_q,
+    int32_t* perm_k, int32_t* rank_k, int32_t* q_idx, int32_t* k_idx, int2* q_runs, int2* k_runs, int32_t* q_rows,
+    int32_t* k_rows, int32_t* counts, int BH, int32_t* err) {
+  // Position t = c * 1024 + threadIdx.x (chunk c): a warp covers 32 consecutive positions, so
+  // the keep loads, rank stores and (kept or dropped runs of) slot stores are coalesced.
+  extern __shared__ __align__(16) int qsm[];
+  int* pq = qsm;                                  // [T_Q + 1]: kept queries before position t
+  int* pk = pq + T_Q + 1;                         // [T_KV + 1]: kept keys before position t
+  int* wc = pk + T_KV + 1;                        // [2][kChunks * 32]: per (chunk, warp) kept counts
+  int* red = wc + 2 * (kQkPrepMaxT / 32);         // 33 ints scan scratch
+  constexpr int kChunks = kQkPrepMaxT / kQkPrepThreads;
+  const int bh = blockIdx.x;
+  const int b = bh / H, h = bh - b * H;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t lt = lanemask_lt();
+  uint32_t bq = 0, bk = 0;  // keep bit of this thread's position in each chunk
+  bool bad = false;
+  constexpr int kBatch = 8;
+#pragma unroll
+  for (int c0 = 0; c0 < kChunks; c0 += kBatch) {
+    double vq[kBatch], vk[kBatch];
+#pragma unroll
+    for (int j2 = 0; j2 < kBatch; ++j2) {  // a batch of loads in flight per side
+      const int t = (c0 + j2) * kQkPrepThreads + threadIdx.x;
+      vq[j2] = (t < T_Q) ? load_num(keep_q, dtq, b * sbq + h * shq + static_cast<int64_t>(t) * stq) : 0.0;
+      vk[j2] = (t < T_KV) ? load_num(keep_k, dtk, b * sbk + h * shk + static_cast<int64_t>(t) * stk) : 0.0;
+    }
+#pragma unroll
+    for (int j2 = 0; j2 < kBatch; ++j2) {
+      bad |= !(vq[j2] == 0.0 || vq[j2] == 1.0) || !(vk[j2] == 0.0 || vk[j2] == 1.0);
+      bq |= (vq[j2] == 1.0 ? 1u : 0u) << (c0 + j2);
+      bk |= (vk[j2] == 1.0 ? 1u : 0u) << (c0 + j2);
+    }
+  }
+  if (bad) flag_error(err, SCFA_ERR_SHAPE);  // keep entries must be 0 or 1 (qk_sparse.py:54-55)
+  // per (chunk, warp) counts in position order, one block scan over them per side
+#pragma unroll
+  for (int c = 0; c < kChunks; ++c) {
+    const uint32_t balq = __ballot_sync(0xffffffffu, (bq >> c) & 1u);
+    const uint32_t balk = __ballot_sync(0xffffffffu, (bk >> c) & 1u);
+    if (lane == 0) {
+      wc[c * 32 + warp] = __popc(balq);
+      wc[kChunks * 32 + c * 32 + warp] = __popc(balk);
+    }
+  }
+  __syncthreads();
+  int nq = 0, nk = 0;
+  {  // 512 entries per side: threads [0, 512) scan q, then k
+    const int e = threadIdx.x & (kChunks * 32 - 1);
+    const int vq0 = (threadIdx.x < kChunks * 32) ? wc[e] : 0;
+    const int oq = block_excl_scan(vq0, red, &nq);
+    const int vk0 = (threadIdx.x < kChunks * 32) ? wc[kChunks * 32 + e] : 0;
+    const int ok = block_excl_scan(vk0, red, &nk);
+    if (threadIdx.x < kChunks * 32) {
+      wc[e] = oq;
+      wc[kChunks * 32 + e] = ok;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < kChunks; ++c) {
+    const int t = c * kQkPrepThreads + threadIdx.x;
+    const uint32_t balq = __ballot_sync(0xffffffffu, (bq >> c) & 1u);
+    const uint32_t balk = __ballot_sync(0xffffffffu, (bk >> c) & 1u);
+    if (t < T_Q) pq[t] = wc[c * 32 + warp] + __popc(balq & lt);
+    if (t < T_KV) pk[t] = wc[kChunks * 32 + c * 32 + warp] + __popc(balk & lt);
+  }
+  if (threadIdx.x == 0) {
+    pq[T_Q] = nq;
+    pk[T_KV] = nk;
+    counts[bh] = nq;
+    counts[BH + bh] = nk;
+  }
+  __syncthreads();
+  const size_t oqs = static_cast<size_t>(bh) * Tq_pad, oks = static_cast<size_t>(bh) * Tkv_pad;
+#pragma unroll
+  for (int c = 0; c < kChunks; ++c) {
+    const int t = c * kQkPrepThreads + threadIdx.x;
+    if (t < T_Q) {  // queries: slot, padded idx, row, run
+      const bool kept = (bq >> c) & 1u;
+      const int before = pq[t];
+      const int slot = kept ? before : nq + (t - before);
+      perm_q[static_cast<size_t>(bh) * T_Q + slot] = t;
+      rank_q[static_cast<size_t>(bh) * T_Q + t] = slot;
+      q_idx[oqs + slot] = kept ? t : kQueryPad;
+      q_rows[oqs + slot] = (b * T_Q + t) * H + h;
+      const int hi = (T_KV == 0) ? 0 : (t + 1 <= T_KV ? pk[t + 1] : nk);  // keys at positions <= t
+      q_runs[oqs + slot] = kept ? make_int2(0, hi) : make_int2(0, 0);
+    }
+    if (t < T_KV) {  // keys: seen by the kept queries at positions >= t; dropped: (nq, nq)
+      const bool kept = (bk >> c) & 1u;
+      const int before = pk[t];
+      const int slot = kept ? before : nk + (t - before);
+      perm_k[static_cast<size_t>(bh) * T_KV + slot] = t;
+      rank_k[static_cast<size_t>(bh) * T_KV + t] = slot;
+      k_idx[oks + slot] = kept ? t : kKeyPad;
+      k_rows[oks + slot] = (b * T_KV + t) * H + h;
+      const int lo = (T_Q == 0) ? 0 : (t <= T_Q ? pq[t] : nq);
+      k_runs[oks + slot] = (T_Q == 0) ? make_int2(0, 0) : (kept ? make_int2(lo, nq) : make_int2(nq, nq));
+    }
+  }
+  // pad slots past the lengths: out-of-range idx, empty runs, a valid row (slot 0's)
+  __syncthreads();
+  for (int s2 = T_Q + threadIdx.x; s2 < Tq_pad; s2 += blockDim.x) {
+    q_idx[oqs + s2] = kQueryPad;
+    q_runs[oqs + s2] = make_int2(0, 0);
+    q_rows[oqs + s2] = (T_Q > 0) ? (b * T_Q + perm_q[static_cast<size_t>(bh) * T_Q]) * H + h : 0;
+  }
+  for (int s2 = T_KV + threadIdx.x; s2 < Tkv_pad; s2 += blockDim.x) {
+    k_idx[oks + s2] = kColOob;
+    k_runs[oks + s2] = make_int2(0, 0);
+    k_rows[oks + s2] = (T_KV > 0) ? (b * T_KV + perm_k[static_cast<size_t>(bh) * T_KV]) * H + h : 0;
+  }
+}
+
 // ------------------------------------------------------------------ hash radix sort
 
 constexpr int kSortThreads = 1024;
@@ -993,6 +1156,40 @@ extern "C" int scfa_qk_compact(const void* keep, int keep_dtype, int64_t B, int6
   qk_compact_kernel<<<static_cast<unsigned>(B * H), 1024, 0, static_cast<cudaStream_t>(stream)>>>(
       keep, keep_dtype, T, H, sb, st, sh, perm, rank, counts, err_flag);
   return check_launch("qk_compact");
+}
+
+extern "C" int scfa_qk_prepare(const void* keep_q, int keep_q_dtype, int64_t sbq, int64_t stq, int64_t shq,
+                               const void* keep_k, int keep_k_dtype, int64_t sbk, int64_t stk, int64_t shk, int64_t B,
+                               int64_t T_Q, int64_t T_KV, int64_t H, int32_t* perm_q, int32_t* rank_q, int32_t* perm_k,
+                               int32_t* rank_k, int32_t* q_idx, int32_t* k_idx, int32_t* q_runs, int32_t* k_runs,
+                               int32_t* q_rows, int32_t* k_rows, int32_t* counts, int32_t* err_flag, void* stream) {
+  if (B < 0 || T_Q < 0 || T_KV < 0 || H < 0) { set_error("negative extent"); return SCFA_ERR_SHAPE; }
+  if (T_Q > kQkPrepMaxT || T_KV > kQkPrepMaxT) {
+    set_error("qk_prepare: T > %d (use scfa_qk_compact)", kQkPrepMaxT);
+    return SCFA_ERR_SHAPE;
+  }
+  if (B * H > 65535) { set_error("qk_prepare: too many (b, h) slices"); return SCFA_ERR_SHAPE; }
+  if (B * H == 0 || (T_Q == 0 && T_KV == 0)) return SCFA_OK;
+  if (B * T_Q * H >= (1LL << 31) || B * T_KV * H >= (1LL << 31)) {
+    set_error("qk_prepare: row tables need B*T*H < 2^31");
+    return SCFA_ERR_SHAPE;
+  }
+  const size_t smem = (static_cast<size_t>(T_Q) + T_KV + 2 + 2 * (kQkPrepMaxT / 32) + 33) * sizeof(int);
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(qk_prepare_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>((2 * kQkPrepMaxT + 2 + 2 * (kQkPrepMaxT / 32) + 33) * sizeof(int))) !=
+        cudaSuccess)
+      return check_launch("qk_prepare attribute");
+    attr = true;
+  }
+  const int Tq_pad = static_cast<int>((T_Q + 127) / 128) * 128, Tkv_pad = static_cast<int>((T_KV + 127) / 128) * 128;
+  qk_prepare_kernel<<<static_cast<unsigned>(B * H), kQkPrepThreads, smem, static_cast<cudaStream_t>(stream)>>>(
+      keep_q, keep_q_dtype, sbq, stq, shq, keep_k, keep_k_dtype, sbk, stk, shk, static_cast<int>(T_Q),
+      static_cast<int>(T_KV), Tq_pad, Tkv_pad, static_cast<int>(H), perm_q, rank_q, perm_k, rank_k, q_idx, k_idx,
+      reinterpret_cast<int2*>(q_runs), reinterpret_cast<int2*>(k_runs), q_rows, k_rows, counts,
+      static_cast<int>(B * H), err_flag);
+  return check_launch("qk_prepare");
 }
 
 extern "C" int scfa_hash_sort(const void* hash, int hash_dtype, int64_t B, int64_t T, int64_t H, int64_t sb,

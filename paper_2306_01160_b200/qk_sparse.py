@@ -56,6 +56,7 @@ class QkPrepared(NamedTuple):
     problem: object = None  # engine Problem (padded vectors, schedules)
     q_rank: torch.Tensor = None  # (B*H, T_Q) position -> slot
     k_rank: torch.Tensor = None  # (B*H, T_KV)
+    copy_event: object = None  # fused path: K / V compacted on a side stream; join before the forward
 
 
 def _keep_tensor(keep, shape, device):
@@ -190,6 +191,9 @@ def qk_preprocess(q, k, v, q_keep, k_keep, materialize=True):
     )
 
 
+_QK_PREP_MAX_T = 16384  # scfa_qk_prepare (one CTA per slice, both sides' prefix counts in shared memory)
+
+
 def _prepare_static(q, k, v, q_keep, k_keep, err):
     """qk_preprocess for the fused paths with every size static: the compacted buffers hold
     T_Q / T_KV slots (kept rows first, in position order, then pad slots — QUERY_PAD /
@@ -197,7 +201,12 @@ def _prepare_static(q, k, v, q_keep, k_keep, err):
     reference's max kept count (qk_sparse.py:58), so nothing is read back to the host and
     the whole fwd + bwd can be captured in a CUDA graph.  Pad slots have empty visibility
     runs: no tile lists them, their outputs are zero.  Keep entries outside {0, 1} are
-    flagged SCFA_ERR_SHAPE in the device status word `err` (qk_sparse.py:54-55)."""
+    flagged SCFA_ERR_SHAPE in the device status word `err` (qk_sparse.py:54-55).
+
+    One launch (scfa_qk_prepare) builds perm / rank, the padded index vectors, the row
+    tables and the visibility runs of both sides; the K / V compaction (one rank read per
+    row, scfa_permute_rows3) then runs on a side stream under the tile-list build — the
+    caller joins it (`prep.copy_event`) before the forward."""
     B, T_Q, H, D = q.shape
     T_KV = k.shape[1]
     if T_KV >= KEY_PAD:
@@ -206,6 +215,53 @@ def _prepare_static(q, k, v, q_keep, k_keep, err):
     qk_ = _keep_tensor(q_keep, (B, T_Q, H), dev)
     kk_ = _keep_tensor(k_keep, (B, T_KV, H), dev)
     BH = B * H
+    contiguous_kv = k.stride(3) == 1 and k.is_contiguous() and v.is_contiguous()
+    if T_Q > _QK_PREP_MAX_T or T_KV > _QK_PREP_MAX_T or BH > 65535 or not contiguous_kv:
+        return _prepare_static_passes(q, k, v, qk_, kk_, err)
+    Tq_pad, Tkv_pad = pad128(T_Q), pad128(T_KV)
+    i32 = dict(dtype=torch.int32, device=dev)
+    perm_q, rank_q = torch.empty((BH, T_Q), **i32), torch.empty((BH, T_Q), **i32)
+    perm_k, rank_k = torch.empty((BH, T_KV), **i32), torch.empty((BH, T_KV), **i32)
+    q_aux, k_aux = torch.empty((BH, Tq_pad), **i32), torch.empty((BH, Tkv_pad), **i32)
+    q_runs, k_runs = torch.empty((BH, Tq_pad, 2), **i32), torch.empty((BH, Tkv_pad, 2), **i32)
+    q_rows, k_rows = torch.empty((BH, Tq_pad), **i32), torch.empty((BH, Tkv_pad), **i32)
+    cnt = torch.empty(2 * BH, **i32)
+    _lib.call("scfa_qk_prepare", _lib.ptr(qk_), _lib.dtype_code(qk_), *qk_.stride(), _lib.ptr(kk_),
+              _lib.dtype_code(kk_), *kk_.stride(), B, T_Q, T_KV, H, _lib.ptr(perm_q), _lib.ptr(rank_q),
+              _lib.ptr(perm_k), _lib.ptr(rank_k), _lib.ptr(q_aux), _lib.ptr(k_aux), _lib.ptr(q_runs),
+              _lib.ptr(k_runs), _lib.ptr(q_rows), _lib.ptr(k_rows), _lib.ptr(cnt), _lib.ptr(err), _lib.stream_ptr())
+    problem = Problem(B, H, T_Q, T_KV, D, q_aux, k_aux)
+    problem.set_runs(q_runs, k_runs)
+    problem.rows = RowTables(q_rows, k_rows, B * T_Q * H, B * T_KV * H)
+    # every key position has a slot: K / V rows move in memory order to their slots, on a
+    # side stream under the tile-list build
+    from .hash_sparse import _copy_streams, _permute3
+
+    main = torch.cuda.current_stream(dev)
+    side = _copy_streams(dev)[2]
+    side.wait_stream(main)
+    with torch.cuda.stream(side):
+        k_c, v_c = _permute3([k, v], [rank_k, rank_k], T_KV)
+        ev = torch.cuda.Event()
+        ev.record(side)
+    for t in (k_c, v_c):
+        t.record_stream(main)
+    prep = QkPrepared(
+        q_c=q, k_c=k_c, v_c=v_c,
+        q_idx=q_aux[:, :T_Q].view(B, H, T_Q), k_idx=k_aux[:, :T_KV].view(B, H, T_KV),
+        scatter_index=perm_q.view(B, H, T_Q).transpose(1, 2),
+        T_Q=T_Q, problem=problem, q_rank=rank_q, k_rank=rank_k, copy_event=ev,
+    )
+    return prep
+
+
+def _prepare_static_passes(q, k, v, qk_, kk_, err):
+    """_prepare_static as separate passes (compaction per side, aux vectors, row maps; the
+    runs come from scfa_build_schedule): T above scfa_qk_prepare's limit or strided K / V."""
+    B, T_Q, H, D = q.shape
+    T_KV = k.shape[1]
+    dev = q.device
+    BH = B * H
     cnt = torch.empty(2 * BH, dtype=torch.int32, device=dev)
     q_perm, q_rank = _compact_perm(qk_, B, T_Q, H, cnt[:BH], err)
     k_perm, k_rank = _compact_perm(kk_, B, T_KV, H, cnt[BH:], err)
@@ -213,20 +269,19 @@ def _prepare_static(q, k, v, q_keep, k_keep, err):
     k_aux = _aux(k_perm, cnt[BH:], B, H, T_KV, KEY_PAD, _OOB_K)
     problem = Problem(B, H, T_Q, T_KV, D, q_aux, k_aux)
     if k.stride(3) == 1 and k.is_contiguous() and v.is_contiguous():
-        # every position has a slot: move K / V rows in memory order to their slots (one rank
-        # read per row for both tensors, scfa_permute_rows3)
         from .hash_sparse import _permute3
 
         k_c, v_c = _permute3([k, v], [k_rank, k_rank], T_KV)
     else:
         k_c, v_c = _gather(k, k_perm, T_KV), _gather(v, k_perm, T_KV)
     problem.rows = make_row_tables(q_perm, k_perm, B, H, T_Q, T_KV, T_Q, T_KV, problem.Tq_pad, problem.Tkv_pad)
-    return QkPrepared(
+    prep = QkPrepared(
         q_c=q, k_c=k_c, v_c=v_c,
         q_idx=q_aux[:, :T_Q].view(B, H, T_Q), k_idx=k_aux[:, :T_KV].view(B, H, T_KV),
         scatter_index=q_perm.view(B, H, T_Q).transpose(1, 2),
         T_Q=T_Q, problem=problem, q_rank=q_rank, k_rank=k_rank,
     )
+    return prep
 
 
 def _problem_from(q_c, k_c, q_idx, k_idx, validate=True):
@@ -344,6 +399,8 @@ def _qk_forward_stage(q, k, v, q_keep, k_keep, scale=None, row_tables=False):
         st.static = True
     st.prob = prob = st.prep.problem
     prob.schedule("fwd", "dq", "dkdv")
+    if getattr(st.prep, "copy_event", None) is not None:
+        torch.cuda.current_stream(q.device).wait_event(st.prep.copy_event)  # K / V compacted
     st.q = q
     if mode == "gathered":
         st.q_only = RowTables(prob.rows.q_rows, None, prob.rows.R_q, prob.rows.R_kv)
