@@ -567,7 +567,7 @@ struct ClusterSortSmem {
   unsigned long long mx;
 };
 
-__global__ void __cluster_dims__(kSortCluster, 1, 1) __launch_bounds__(kSortThreads)
+__global__ void __cluster_dims__(kSortCluster, 1, 1) __launch_bounds__(kSortThreads, 2)
     hash_prepare_sort_cluster_kernel(const void* hash, int hdt, int T, int T_pad, int64_t H, int64_t sb, int64_t st,
                                      int64_t sh, int32_t* perm, int32_t* rank, int32_t* scratch,
                                      int32_t* sorted_hash, int32_t* err) {
