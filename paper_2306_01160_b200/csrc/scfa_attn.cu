@@ -72,6 +72,9 @@ enum Mode : int { MODE_FWD = 0, MODE_DQ = 1, MODE_DKDV = 2, MODE_BWD = 3 };
 #ifndef SCFA_TUNE_NS1_ALT
 #define SCFA_TUNE_NS1_ALT 5
 #endif
+#ifndef SCFA_TUNE_KV_TMEM
+#define SCFA_TUNE_KV_TMEM 1
+#endif
 #ifndef SCFA_TUNE_QE
 #define SCFA_TUNE_QE 3
 #endif
@@ -130,7 +133,7 @@ struct Cfg {
   // buffers: item i uses buffer i % 2), so the S^T / dP^T MMAs read A from TMEM (TS mode:
   // 32 instead of 48 clk per N = 64 MMA, scripts/mma_issue.cu) — which leaves room for
   // two S / dP buffers, not three
-  static constexpr bool KV_TMEM = (kMode == MODE_DKDV && kD == 64);
+  static constexpr bool KV_TMEM = SCFA_TUNE_KV_TMEM && (kMode == MODE_DKDV && kD == 64);
   static constexpr int NBUF = (KV_TMEM || FUSED) ? 2 : ((ALT && 3 * TM_BUF + (KEYS ? 2 * kD : kD) <= 512) ? 3 : 2);
   static constexpr int TM_S = 0;
   static constexpr int TM_DP = (kMode == MODE_FWD) ? 0 : BN;
