@@ -1384,6 +1384,20 @@ __global__ void __launch_bounds__(512, 1)
           // columns already read (chunk k's P / dS land in columns [16k, 16k+16) of S / dP)
 #pragma unroll
           for (int cc = 0; cc < C::BN; cc += 32) {
+            uint32_t pk_p[16], pk_ds[16];
+            // a chunk no row of this warp can see: P = dS = 0 without loading S / dP or any
+            // exponential (bitwise the masked result)
+            if (!full && !__any_sync(0xffffffffu, vis[cc >> 5] != 0u)) {
+              if (!C::ALT && C::OVERLAP && cc + 32 == C::BN) {
+                tc_fence_before();
+                mbar_arrive(bar_s_free);
+              }
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                pk_p[i] = 0u;
+                pk_ds[i] = 0u;
+              }
+            } else {
             float sv[32], dv[32];
             tmem_ld32(t_sb + cc, *reinterpret_cast<uint32_t(*)[32]>(sv));
             tmem_ld32(t_dpb + cc, *reinterpret_cast<uint32_t(*)[32]>(dv));
@@ -1392,7 +1406,6 @@ __global__ void __launch_bounds__(512, 1)
               tc_fence_before();
               mbar_arrive(bar_s_free);
             }
-            uint32_t pk_p[16], pk_ds[16];
 #pragma unroll
             for (int c = cc; c < cc + 32; c += 4) {
               float nl[4], nd[4];
@@ -1423,6 +1436,7 @@ __global__ void __launch_bounds__(512, 1)
                 pk_p[(c - cc + e) >> 1] = pack_bf16(p0, p1);
                 pk_ds[(c - cc + e) >> 1] = pack_bf16(d0, d1);
               }
+            }
             }
             if (!C::ALT && cc == 0) {  // the previous tile's accumulate MMAs read these columns
               if (tg > 0) mbar_wait(bar_p_free, (tg - 1) & 1);
