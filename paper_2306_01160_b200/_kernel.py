@@ -123,8 +123,9 @@ class Problem:
                     n_rb = max(-(-T_rows // 128), 1)
                     stride = max(-(-T_cols // cb), 1)
                     lst = torch.empty((self.BH, n_rb, stride), dtype=torch.int16, device=dev)
-                    # counts (BH, n_rb) + the attention kernels' work counter pair
-                    cnt = torch.zeros(self.BH * n_rb + 2, dtype=torch.int32, device=dev)[: self.BH * n_rb].view(
+                    # counts (BH, n_rb) + the attention kernels' work counter pair; the list kernel
+                    # writes every count and zeroes the pair (no fill launch)
+                    cnt = torch.empty(self.BH * n_rb + 2, dtype=torch.int32, device=dev)[: self.BH * n_rb].view(
                         self.BH, n_rb)  # same base address; the pair lives past the view
                     self._lists[name] = (lst, cnt, stride)
                     args += [_lib.ptr(lst), _lib.ptr(cnt), stride]

@@ -18,6 +18,8 @@
 //    iff every row's run covers it, so the kernel skips the mask there.
 // 3. The reference's own schedule at any BlockSpec, used to report
 //    FlashOutputs.tiles_computed with the reference's meaning.
+#include <cstdlib>
+
 #include "scfa_common.cuh"
 #include "scfa_internal.h"
 
@@ -112,7 +114,124 @@ struct ListJob {
 struct ListJobs {
   ListJob job[3];
   unsigned long long* tiles;  // [3] accumulated, may be null
+  int BH;
 };
+
+// One warp per (list, slice, row block): the same lists as tile_list_kernel without shared
+// memory or block barriers.  Every sorted problem here has run starts that never decrease
+// along the rows (keys / queries sorted by position, or by (bucket, position) with each
+// bucket's runs inside its own slot range), so the union of the rows' column-block ranges
+// is an interval merge: a prefix max of the range ends says which blocks each row adds.
+// When the union is one interval (QK, dense, shared-id hash: always) the lanes write it
+// together; otherwise each row writes the blocks it adds; a decreasing start (never seen)
+// falls back to one ballot per column block.  Lists and counts are bit-identical to
+// tile_list_kernel's.
+__global__ void __launch_bounds__(128) tile_list_warp_kernel(const __grid_constant__ ListJobs jobs, int n_rb_max) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = static_cast<int64_t>(blockIdx.x) * 4 + (threadIdx.x >> 5);
+  const int64_t per_z = static_cast<int64_t>(jobs.BH) * n_rb_max;
+  const int z = static_cast<int>(w / per_z);
+  if (z >= 3) return;
+  const int64_t rem = w - z * per_z;
+  const int bh = static_cast<int>(rem / n_rb_max), rb = static_cast<int>(rem - static_cast<int64_t>(bh) * n_rb_max);
+  const ListJob& J = jobs.job[z];
+  if (J.list == nullptr || rb >= J.n_rb) return;
+  if (rb == 0 && bh == 0 && lane < 2) J.count[static_cast<int64_t>(jobs.BH) * J.n_rb + lane] = 0;
+  const int B = J.col_block, n_cb = J.n_cb;
+  // rows 4 * lane .. 4 * lane + 3 of the block, in order
+  int lo[4], hi[4];
+  bool ne[4];
+  int my_full_lo = 0, my_full_hi = n_cb;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = rb * kRowBlock + 4 * lane + i;
+    const int2 r = (row < J.T_rows_pad) ? J.runs[static_cast<int64_t>(bh) * J.T_rows_pad + row] : make_int2(0, 0);
+    ne[i] = r.y > r.x;
+    lo[i] = ne[i] ? r.x / B : 0;
+    hi[i] = ne[i] ? (r.y - 1) / B + 1 : 0;
+    my_full_lo = max(my_full_lo, ne[i] ? (r.x + B - 1) / B : 0);
+    my_full_hi = min(my_full_hi, ne[i] ? r.y / B : 0);
+  }
+  const int flo = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(my_full_lo)));
+  const int fhi = static_cast<int>(__reduce_min_sync(0xffffffffu, static_cast<unsigned>(my_full_hi)));
+  // per lane: max end and max start of its rows; a start below an earlier row's start is a
+  // decreasing start
+  int lmax_hi = 0, lmax_lo = -1, lmin_lo = 0x7fffffff;
+  bool mono = true;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (ne[i]) {
+      mono &= lo[i] >= lmax_lo;
+      lmax_lo = max(lmax_lo, lo[i]);
+      lmax_hi = max(lmax_hi, hi[i]);
+      lmin_lo = min(lmin_lo, lo[i]);
+    }
+  // exclusive prefix max (over lanes) of ends and starts
+  int px_hi = lmax_hi, px_lo = lmax_lo;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int a = __shfl_up_sync(0xffffffffu, px_hi, o), b = __shfl_up_sync(0xffffffffu, px_lo, o);
+    if (lane >= o) {
+      px_hi = max(px_hi, a);
+      px_lo = max(px_lo, b);
+    }
+  }
+  int prev_hi = __shfl_up_sync(0xffffffffu, px_hi, 1), prev_lo = __shfl_up_sync(0xffffffffu, px_lo, 1);
+  if (lane == 0) {
+    prev_hi = 0;
+    prev_lo = -1;
+  }
+  mono &= (lmin_lo == 0x7fffffff) || lmin_lo >= prev_lo;  // this lane's first start vs every earlier row
+  const bool all_mono = __all_sync(0xffffffffu, mono);
+  uint16_t* out = J.list + (static_cast<int64_t>(bh) * J.n_rb + rb) * J.stride;
+  auto entry = [&](int cb) { return static_cast<uint16_t>(cb | ((cb >= flo && cb < fhi) ? 0x8000 : 0)); };
+  int total;
+  if (all_mono) {
+    int add = 0, run_hi = prev_hi;  // blocks this lane's rows add to the union
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (ne[i]) {
+        add += max(0, hi[i] - max(lo[i], run_hi));
+        run_hi = max(run_hi, hi[i]);
+      }
+    int pos = add;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, pos, o);
+      if (lane >= o) pos += a;
+    }
+    total = __shfl_sync(0xffffffffu, pos, 31);
+    pos -= add;
+    const int u_lo = static_cast<int>(__reduce_min_sync(0xffffffffu, static_cast<unsigned>(lmin_lo)));
+    const int u_hi = __shfl_sync(0xffffffffu, px_hi, 31);
+    if (total > 0 && total == u_hi - u_lo) {  // one interval: written by all lanes
+      for (int j = lane; j < total; j += 32) out[j] = entry(u_lo + j);
+    } else {
+      run_hi = prev_hi;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (ne[i]) {
+          for (int cb = max(lo[i], run_hi); cb < hi[i]; ++cb) out[pos++] = entry(cb);
+          run_hi = max(run_hi, hi[i]);
+        }
+    }
+  } else {  // general: one ballot per column block
+    total = 0;
+    for (int cb = 0; cb < n_cb; ++cb) {
+      bool hit = false;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) hit |= ne[i] && lo[i] <= cb && cb < hi[i];
+      if (__any_sync(0xffffffffu, hit)) {
+        if (lane == 0) out[total] = entry(cb);
+        ++total;
+      }
+    }
+  }
+  if (lane == 0) {
+    J.count[static_cast<int64_t>(bh) * J.n_rb + rb] = total;
+    if (jobs.tiles) atomicAdd(jobs.tiles + z, static_cast<unsigned long long>(total));
+  }
+}
 
 // One CTA (128 threads = 128 rows) per (row block, slice, list).  Each row adds its
 // run's column-block range to a difference array; a block scan turns it into the
@@ -346,9 +465,16 @@ extern "C" int scfa_build_schedule(const int32_t* q_idx, const int32_t* q_hash, 
                                      q_out, k_out);
   }
   const int n_rb = n_rb_q > n_rb_k ? n_rb_q : n_rb_k;
+  jobs.BH = static_cast<int>(BH);
   if ((list_fwd || list_dq || list_dkdv) && n_rb > 0) {
-    dim3 grid(static_cast<unsigned>(n_rb), static_cast<unsigned>(BH), 3);
-    tile_list_kernel<<<grid, 128, 0, s>>>(jobs);
+    static const bool cta_lists = getenv("SCFA_CTA_LISTS") != nullptr;  // diagnostics: the per-CTA kernel
+    if (cta_lists) {
+      dim3 grid(static_cast<unsigned>(n_rb), static_cast<unsigned>(BH), 3);
+      tile_list_kernel<<<grid, 128, 0, s>>>(jobs);
+    } else {
+      const int64_t warps = 3 * BH * n_rb;
+      tile_list_warp_kernel<<<static_cast<unsigned>((warps + 3) / 4), 128, 0, s>>>(jobs, n_rb);
+    }
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
