@@ -135,6 +135,22 @@ def test_fused_prepare_matches_general_path(T, nb, excl, seed):
     want = np.argsort(h.cpu().numpy().transpose(0, 2, 1).reshape(B * H, T), axis=1, kind="stable")
     assert np.array_equal(sb.q_perm.cpu().numpy(), want)
     assert np.array_equal(sb.q_rank.cpu().numpy(), np.argsort(want, axis=1))
+    # the sorted vectors and row table the sort writes (itself, on the cluster path)
+    T_pad = fused.Tq_pad
+    perm = sb.q_perm.cpu().numpy()
+    hs_np = h.cpu().numpy().transpose(0, 2, 1).reshape(B * H, T)
+    qi, ki = fused.q_idx.cpu().numpy(), fused.k_idx.cpu().numpy()
+    qh, kh = fused.q_hash.cpu().numpy(), fused.k_hash.cpu().numpy()
+    assert np.array_equal(qi[:, :T], perm) and np.array_equal(ki[:, :T], perm)
+    sorted_ids = np.take_along_axis(hs_np, perm, axis=1)
+    assert np.array_equal(qh[:, :T], sorted_ids) and np.array_equal(kh[:, :T], sorted_ids)
+    assert (qi[:, T:] == -1).all() and (ki[:, T:] == 0x7FFFFFFF).all()
+    assert (qh[:, T:] == -3).all() and (kh[:, T:] == -2).all()
+    rows = fused.rows.q_rows.cpu().numpy()
+    bh = np.arange(B * H)[:, None]
+    want_rows = ((bh // H) * T + perm) * H + bh % H
+    assert np.array_equal(rows[:, :T], want_rows)
+    assert (rows[:, T:] == want_rows[:, :1]).all()
     flags = fused.flags
     general = Problem(B, H, T, T, D, fused.q_idx.clone(), fused.k_idx.clone(), fused.q_hash.clone(),
                       fused.k_hash.clone(), flags=flags)
