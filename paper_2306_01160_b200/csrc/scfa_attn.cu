@@ -72,6 +72,9 @@ enum Mode : int { MODE_FWD = 0, MODE_DQ = 1, MODE_DKDV = 2, MODE_BWD = 3 };
 #ifndef SCFA_TUNE_NS1_ALT
 #define SCFA_TUNE_NS1_ALT 5
 #endif
+#ifndef SCFA_TUNE_ROW_REGS_DQ
+#define SCFA_TUNE_ROW_REGS_DQ 184
+#endif
 #ifndef SCFA_TUNE_KV_TMEM
 #define SCFA_TUNE_KV_TMEM 1
 #endif
@@ -703,7 +706,12 @@ __global__ void __launch_bounds__(512, 1)
   // Register rebalancing happens first thing inside each warpgroup's branch (nothing
   // live across it, no merge after it): the row warpgroups take the file the epilogue /
   // producer / MMA warps do not need.
-  constexpr int kRowRegs = (C::NSTREAM == 2 || C::ALT || C::SPLIT) ? 176 : 240;
+  // row / epilogue register split (the two row warpgroups take what the epilogue gives up);
+  // SCFA_TUNE_ROW_REGS_DQ: the dQ pass's row code spills at 176 and not at 184, the
+  // epilogue still fits 88 there (ptxas -v)
+  constexpr int kRowSplit = (kMode == MODE_DQ && kD == 64) ? SCFA_TUNE_ROW_REGS_DQ : 176;
+  constexpr int kRowRegs = (C::NSTREAM == 2 || C::ALT || C::SPLIT) ? kRowSplit : 240;
+  constexpr int kEpiRegs = (C::NSTREAM == 2 || C::ALT || C::SPLIT) ? 104 - 2 * (kRowSplit - 176) : 104;
   const int s = (C::ALT || C::SPLIT) ? 0 : ((wg < 2) ? wg : ((warp >= 12) ? ((warp - 12) >> 1) : 0));
   const bool active = (C::ALT || C::SPLIT) ? (wg < 2 || ((warp - 12) >> 1) == 0) : (s < C::NSTREAM);
   if (wg == 3) {
@@ -1016,7 +1024,7 @@ __global__ void __launch_bounds__(512, 1)
    }
   } else if (wg == 2) {
     // ------------------------------------------------------------ epilogue warpgroup
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 104;" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kEpiRegs) : "memory");
     epilogue_wg<kMode, kD>(args, smem_base, *tmem_slot, warp, lane, 0);
   } else if (!active) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 24;" ::: "memory");  // idle row warpgroup (one stream)
