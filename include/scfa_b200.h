@@ -218,8 +218,11 @@ int scfa_validate_sorted(const int32_t* idx, const int32_t* hash, int64_t BH, in
  *   dq  : query rows in 128-row blocks x 64-key tiles    (scfa_attn_bwd_dq)
  *   dkdv: key rows in 128-row blocks x 64-query tiles    (scfa_attn_bwd_dkdv)
  * list_* (B*H, n_row_blocks, stride_*) with stride >= n_col_blocks; count_*
- * (B*H * n_row_blocks + 2) int32: the counts, then a work-counter pair the attention
- * kernels use to hand out items dynamically (zeroed here, left zero by every launch).  A NULL list skips that list.  tiles[3] (may be
+ * (3 * B*H * n_row_blocks + 4) int32 (ABI 6): the n = B*H*n_row_blocks counts, a
+ * work-counter pair the attention kernels use to hand out items dynamically (zeroed here,
+ * left zero by every launch), then at offset n + 2 + (n & 1) the order they hand them out in:
+ * n {item, count} pairs, most tiles first (stable), so a persistent grid's last items are its
+ * shortest.  A NULL list skips that list.  tiles[3] (may be
  * NULL) accumulates the listed-tile totals.  flags: SCFA_FLAG_*.            */
 int scfa_build_schedule(const int32_t* q_idx, const int32_t* q_hash, const int32_t* k_idx,
                         const int32_t* k_hash, int64_t BH, int64_t T_q, int64_t T_kv, int64_t Tq_pad,

@@ -123,10 +123,12 @@ class Problem:
                     n_rb = max(-(-T_rows // 128), 1)
                     stride = max(-(-T_cols // cb), 1)
                     lst = torch.empty((self.BH, n_rb, stride), dtype=torch.int16, device=dev)
-                    # counts (BH, n_rb) + the attention kernels' work counter pair; the list kernel
-                    # writes every count and zeroes the pair (no fill launch)
-                    cnt = torch.empty(self.BH * n_rb + 2, dtype=torch.int32, device=dev)[: self.BH * n_rb].view(
-                        self.BH, n_rb)  # same base address; the pair lives past the view
+                    # counts (BH, n_rb), the attention kernels' work counter pair, then the item
+                    # order (longest first, {item, count} pairs, 8-byte aligned); the list
+                    # kernels write all of it (no fill launch)
+                    n_it = self.BH * n_rb
+                    cnt = torch.empty(3 * n_it + 4, dtype=torch.int32, device=dev)[:n_it].view(
+                        self.BH, n_rb)  # same base address; pair and order live past the view
                     self._lists[name] = (lst, cnt, stride)
                     args += [_lib.ptr(lst), _lib.ptr(cnt), stride]
                 else:
@@ -138,7 +140,7 @@ class Problem:
                 self.BH, self.T_q, self.T_kv, self.Tq_pad, self.Tkv_pad, self.flags,
                 _lib.ptr(self._lists.get("q_runs")), _lib.ptr(self._lists.get("k_runs")), ready,
                 *args, _lib.ptr(self._tiles_total), _lib.stream_ptr(),
-                kernels=(0 if ready == 3 else 1) + 1,
+                kernels=(0 if ready == 3 else 1) + 2,
             )
         return self._lists
 

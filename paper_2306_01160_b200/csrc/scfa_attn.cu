@@ -734,8 +734,10 @@ __global__ void __launch_bounds__(512, 1)
       if (lane == 0) {
         const int w = atomicAdd(work_ctr, 1);
         if (w < args.n_items) {
-          e.x = item_of(args, w);
-          e.y = args.list_count[e.x];
+          // the schedule's order: the longest items first (item_order_kernel)
+          const int* ord = args.list_count + item_order_offset(args.n_items) + 2 * w;
+          e.x = ord[0];
+          e.y = ord[1];
         }
         const int qs = k % C::NQ;
         if (k >= C::NQ) mbar_wait_lazy(bar_q_empty + qs, ((k / C::NQ) - 1) & 1);

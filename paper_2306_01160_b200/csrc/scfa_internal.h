@@ -56,6 +56,17 @@ struct AttnLaunch {
 };
 
 int launch_attention(const AttnLaunch& L, cudaStream_t stream);
+
+// Item order of a tile list: after the n = B*H*n_row_blocks counts and the work-counter pair
+// of a count buffer (8-byte aligned), n {item, tile count} pairs, most tiles first (LPT: the
+// longest items are handed out first, so the grid's last items are its shortest).
+__host__ __device__ inline int64_t item_order_offset(int64_t n_items) { return n_items + 2 + (n_items & 1); }
+struct OrderJob {
+  int32_t* count;  // the list's count buffer (counts, pair, order)
+  int n_rb;        // row blocks per slice
+  int lpt;         // 0: keep the default order (last row block first, cycling over slices)
+};
+int launch_item_order(const OrderJob* jobs, int n_jobs, int BH, cudaStream_t stream);
 int encode_tensor_map(CUtensorMap* map, int dtype_bytes, int rank, const void* base, const cuuint64_t* dims,
                       const cuuint64_t* strides_bytes, const cuuint32_t* box);
 int encode_tensor_map_bf16_3d(CUtensorMap* map, const void* base, const cuuint64_t* dims,

@@ -486,6 +486,63 @@ SCFA_DEVICE void radix_pass(PrepSmem& S, const int32_t* key, int T, int shift, c
   __syncthreads();
 }
 
+// Item order of the tile lists (one CTA per list): the attention kernels' default order
+// (last row block first, cycling over slices) stably re-sorted by tile count, longest first —
+// an LPT schedule: with items handed out dynamically, the last ones left are the shortest, so
+// the streams of a persistent grid finish close together.  One 8-bit counting pass (counts
+// above 255 share the top class).  Lists of more than kPrepMaxT items keep the default order.
+struct OrderJobs {
+  OrderJob job[3];
+  int BH;
+};
+
+__global__ void __launch_bounds__(kSortThreads) item_order_kernel(const __grid_constant__ OrderJobs J) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  PrepSmem& S = *reinterpret_cast<PrepSmem*>(dsm);
+  int32_t* key = reinterpret_cast<int32_t*>(dsm + sizeof(PrepSmem));
+  const OrderJob& o = J.job[blockIdx.x];
+  if (o.count == nullptr) return;
+  const int n = J.BH * o.n_rb;
+  int32_t* order = o.count + item_order_offset(n);
+  auto item_of = [&](int w) {  // scfa_attn.cu item_of: last row block first, cycling over slices
+    const int rb = o.n_rb - 1 - w / J.BH, bh = w - (w / J.BH) * J.BH;
+    return bh * o.n_rb + rb;
+  };
+  if (n > kPrepMaxT || !o.lpt) {
+    for (int w = threadIdx.x; w < n; w += blockDim.x) {
+      const int it = item_of(w);
+      order[2 * w] = it;
+      order[2 * w + 1] = o.count[it];
+    }
+    return;
+  }
+  int32_t* sorted = key + kPrepMaxT;
+  for (int w = threadIdx.x; w < n; w += blockDim.x) key[w] = 255 - min(o.count[item_of(w)], 255);
+  __syncthreads();
+  radix_pass(S, key, n, 0, nullptr, sorted, nullptr, nullptr);  // stable: equal counts keep their order
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const int it = item_of(sorted[j]);
+    order[2 * j] = it;
+    order[2 * j + 1] = o.count[it];
+  }
+}
+
+int launch_item_order(const OrderJob* jobs, int n_jobs, int BH, cudaStream_t stream) {
+  OrderJobs J{};
+  for (int i = 0; i < n_jobs && i < 3; ++i) J.job[i] = jobs[i];
+  J.BH = BH;
+  const size_t smem = sizeof(PrepSmem) + 2 * kPrepMaxT * sizeof(int32_t);
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(item_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
+        cudaSuccess)
+      return SCFA_ERR_CUDA;
+    attr = true;
+  }
+  item_order_kernel<<<3, kSortThreads, smem, stream>>>(J);
+  return cudaGetLastError() == cudaSuccess ? SCFA_OK : SCFA_ERR_CUDA;
+}
+
 // Kernel 1 (one CTA per slice): keys cached in shared memory, stable LSD radix
 // passes -> perm; the final pass also writes the sorted ids.  With one pass (ids <
 // 256, every bench / LM bucket count) the pass's digit offsets ARE the bucket runs:

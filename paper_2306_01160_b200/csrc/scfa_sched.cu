@@ -20,6 +20,10 @@
 //    FlashOutputs.tiles_computed with the reference's meaning.
 #include <cstdlib>
 
+#ifndef SCFA_LPT_LISTS
+#define SCFA_LPT_LISTS 5  // bit z: list z (fwd, dq, dkdv) handed out longest first (dQ: measured slower)
+#endif
+
 #include "scfa_common.cuh"
 #include "scfa_internal.h"
 
@@ -474,6 +478,15 @@ extern "C" int scfa_build_schedule(const int32_t* q_idx, const int32_t* q_hash, 
     } else {
       const int64_t warps = 3 * BH * n_rb;
       tile_list_warp_kernel<<<static_cast<unsigned>((warps + 3) / 4), 128, 0, s>>>(jobs, n_rb);
+    }
+    // the longest items first (count buffers hold the order after the work-counter pair)
+    static const int lpt_mask = getenv("SCFA_LPT") ? atoi(getenv("SCFA_LPT")) : SCFA_LPT_LISTS;  // A/B knob
+    OrderJob oj[3] = {};
+    for (int z = 0; z < 3; ++z)
+      if (jobs.job[z].list) oj[z] = OrderJob{jobs.job[z].count, jobs.job[z].n_rb, (lpt_mask >> z) & 1};
+    if (launch_item_order(oj, 3, static_cast<int>(BH), s) != SCFA_OK) {
+      set_error("schedule: item order launch failed");
+      return SCFA_ERR_CUDA;
     }
   }
   cudaError_t e = cudaGetLastError();
