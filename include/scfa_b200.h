@@ -310,14 +310,17 @@ int scfa_zero_dropped(const void* keep, int keep_dtype, int64_t B, int64_t T, in
  * per query slot from the O rows (addressed like d_out) and written to delta_out
  * (B*H, Tq_pad) for scfa_attn_bwd_dkdv; `delta` is then ignored.
  * ABI 4: do_out (optional, needs q_rows) receives the gathered dO rows in kernel order,
- * (B*H, T_q, D) bf16, for scfa_attn_bwd_dkdv's streamed operand.                     */
+ * (B*H, T_q, D) bf16, for scfa_attn_bwd_dkdv's streamed operand.
+ * ABI 6: q_sorted (optional, with q_rows): Q already in kernel order, (B*H, T_q, D) bf16 (the
+ * forward's q_out) — loaded as tiled boxes; only dO goes through the row table.          */
 int scfa_attn_bwd_dq(const void* q, const void* k, const void* v, const void* d_out, int64_t BH,
                      int64_t T_q, int64_t T_kv, int64_t D, const int32_t* q_idx,
                      const int32_t* q_runs, int64_t Tq_pad, int64_t Tkv_pad, const float* lse2,
                      const float* delta, const uint16_t* list, const int32_t* list_count,
                      int64_t list_stride, float scale, int64_t H, int64_t T_out, int out_boundary,
                      float* dq, const int32_t* q_rows, const int32_t* k_rows, int64_t R_q,
-                     int64_t R_kv, const void* o, float* delta_out, void* do_out, void* stream);
+                     int64_t R_kv, const void* o, float* delta_out, void* do_out,
+                     const void* q_sorted, void* stream);
 
 /* Backward pass 2 (dK/dV, key-block owner over the transposed schedule,
  * _kernel.py:181-192).  k_runs, list_dkdv, count_dkdv from scfa_build_schedule.

@@ -384,7 +384,7 @@ def attention_backward(problem, q, k, v, outputs, d_out, scale=None, boundary=No
             _lib.ptr(problem.q_idx), _lib.ptr(sched["q_runs"]), problem.Tq_pad, problem.Tkv_pad,
             _lib.ptr(lse2), _lib.ptr(delta), _lib.ptr(lst), _lib.ptr(cnt), stride,
             _scale(scale, D), H, Tq_out, out_b, _lib.ptr(dq), *rargs,
-            _lib.ptr(O) if fuse else None, _lib.ptr(delta) if fuse else None, None, _lib.stream_ptr(),
+            _lib.ptr(O) if fuse else None, _lib.ptr(delta) if fuse else None, None, None, _lib.stream_ptr(),
         )
     if T_kv > 0:
         lst, cnt, stride = sched["dkdv"]
@@ -398,7 +398,8 @@ def attention_backward(problem, q, k, v, outputs, d_out, scale=None, boundary=No
     return dq, dk, dv
 
 
-def dq_backward_gathered(problem, q, k_sorted, v_sorted, outputs, d_out, rows, scale, T_out, do_out):
+def dq_backward_gathered(problem, q, k_sorted, v_sorted, outputs, d_out, rows, scale, T_out, do_out,
+                         q_sorted=None):
     """dQ with the stationary Q / dO read through rows.q_rows from the caller's (B, T, H, D)
     tensors (gather4, once per item) and streamed K / V from bucket-order copies; delta =
     rowsum(dO * O) fused in (O read where the forward wrote it) and the gathered dO written
@@ -420,7 +421,8 @@ def dq_backward_gathered(problem, q, k_sorted, v_sorted, outputs, d_out, rows, s
         _lib.ptr(problem.q_idx), _lib.ptr(sched["q_runs"]), problem.Tq_pad, problem.Tkv_pad,
         _lib.ptr(outputs._lse2), _lib.ptr(delta), _lib.ptr(lst), _lib.ptr(cnt), stride,
         _scale(scale, D), H, T_out, 1, _lib.ptr(dq), *rows.args(),
-        _lib.ptr(as_operand(outputs.O, dev)), _lib.ptr(delta), _lib.ptr(do_out), _lib.stream_ptr(),
+        _lib.ptr(as_operand(outputs.O, dev)), _lib.ptr(delta), _lib.ptr(do_out), _lib.ptr(q_sorted),
+        _lib.stream_ptr(),
     )
     return dq, delta
 

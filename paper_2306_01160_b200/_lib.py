@@ -67,7 +67,7 @@ _SIGS = {
     "scfa_bwd_prep_rank": [_P, _P, _L, _L, _L, _L, _L, _P, _P, _P, _P],
     "scfa_bwd_prep": [_P, _P, _P, _P, _P, _L, _L, _L, _L, _P, _L, _L, _P, _P, _P, _P],
     "scfa_attn_bwd_dq": [_P, _P, _P, _P, _L, _L, _L, _L, _P, _P, _L, _L, _P, _P, _P, _P, _L, _F, _L, _L, _I,
-                         _P, _P, _P, _L, _L, _P, _P, _P, _P],
+                         _P, _P, _P, _L, _L, _P, _P, _P, _P, _P],
     "scfa_attn_bwd": [_P, _P, _P, _P, _L, _L, _L, _L, _P, _P, _P, _L, _L, _P, _P, _P, _P, _L, _F, _L, _L, _L, _I,
                       _P, _P, _P, _P],
     "scfa_debug_timing": [_P, _L],

@@ -204,6 +204,7 @@ struct AttnArgs {
   const int* out_rows;  // optional output routing: global row of each stationary slot (BH, T_rows_pad), pad
                         // slots included (every row of the [R, D] output is written; tiled loads)
   const int* y_rows;  // gather mode: global row per streamed slot (BH, T_cols_pad)
+  int x0_tiled;                // gather mode: the first stationary tensor comes tiled (kernel order)
   int x_writeout;              // gather mode: write a gathered stationary tile out through tm_xo (kernel
                                // order): FWD its Q, DQ its dO (the tensors dK/dV streams)
   const __nv_bfloat16* o_src;  // DQ: O rows (addressed like dO) for the fused delta
@@ -766,9 +767,13 @@ __global__ void __launch_bounds__(512, 1)
       if (gx) {  // 128 stationary rows: 4 per lane
         const int4 r4 = __ldg(reinterpret_cast<const int4*>(args.x_rows + static_cast<size_t>(bh) * args.T_rows_pad +
                                                           rb * C::BM) + lane);
+        if (args.x0_tiled && lane == 0) {  // Q already in kernel order: one tiled box per chunk
+          for (int c = 0; c < C::DCH; ++c) tma_load_3d(xb + c * C::BM * 128, &tm_x0, bar_x_full + xs, c * 64, rb * C::BM, bh);
+        }
 #pragma unroll
         for (int c = 0; c < C::DCH; ++c) {
-          tma_gather4(xb + c * C::BM * 128 + lane * 512, &tm_x0, bar_x_full + xs, c * 64, r4.x, r4.y, r4.z, r4.w);
+          if (!args.x0_tiled)
+            tma_gather4(xb + c * C::BM * 128 + lane * 512, &tm_x0, bar_x_full + xs, c * 64, r4.x, r4.y, r4.z, r4.w);
           if (C::NX == 2)
             tma_gather4(xb + C::X_BYTES + c * C::BM * 128 + lane * 512, &tm_x1, bar_x_full + xs, c * 64, r4.x, r4.y,
                         r4.z, r4.w);
@@ -1550,7 +1555,11 @@ static int launch_mode(const AttnLaunch& L, cudaStream_t stream) {
   CUtensorMap mx0, mx1, my0, my1, mxo;
   int rc = 0;
   if (L.x_rows) {
-    rc |= make_row_map(&mx0, L.x0, L.x_nrows, kD, 2);
+    if (L.x0_tiled) {
+      rc |= make_map(&mx0, L.x0_tiled, L.BH, L.T_rows, kD, C::BM);
+    } else {
+      rc |= make_row_map(&mx0, L.x0, L.x_nrows, kD, 2);
+    }
     rc |= make_row_map(&mx1, L.x1 ? L.x1 : L.x0, L.x_nrows, kD, 2);
   } else {
     rc |= make_map(&mx0, L.x0, L.BH, L.T_rows, kD, C::BM);
@@ -1581,6 +1590,7 @@ static int launch_mode(const AttnLaunch& L, cudaStream_t stream) {
   a.out_rows = L.out_rows;
   a.y_rows = L.y_rows;
   a.x_writeout = writeout ? 1 : 0;
+  a.x0_tiled = (L.x_rows && L.x0_tiled && kMode == MODE_DQ) ? 1 : 0;
   a.o_src = static_cast<const __nv_bfloat16*>(L.o_src);
   a.delta_out = L.delta_out;
   a.lse2 = L.lse2;

@@ -155,7 +155,7 @@ extern "C" int scfa_attn_bwd_dq(const void* q, const void* k, const void* v, con
                                 const uint16_t* list, const int32_t* list_count, int64_t list_stride, float scale,
                                 int64_t H, int64_t T_out, int out_boundary, float* dq, const int32_t* q_rows,
                                 const int32_t* k_rows, int64_t R_q, int64_t R_kv, const void* o, float* delta_out,
-                                void* do_out, void* stream) {
+                                void* do_out, const void* q_sorted, void* stream) {
   int rc = check_attn_args(BH, T_q, T_kv, D, Tq_pad, Tkv_pad, q, k, v);
   if (rc) return rc;
   if (BH == 0 || T_q == 0) return SCFA_OK;
@@ -201,6 +201,7 @@ extern "C" int scfa_attn_bwd_dq(const void* q, const void* k, const void* v, con
     return SCFA_ERR_PARAM;
   }
   L.x_out = do_out;
+  L.x0_tiled = q_rows ? q_sorted : nullptr;
   L.o_src = o;
   L.delta_out = o ? delta_out : nullptr;
   L.n_row_blocks = (L.T_rows + 127) / 128;

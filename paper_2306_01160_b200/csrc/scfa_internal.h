@@ -38,6 +38,7 @@ struct AttnLaunch {
   long long x_nrows;   // rows of the x / out row tables (gather mode)
   long long y_nrows;   // rows of the y row tables
   void* x_out;         // FWD gather mode: stationary Q rows written back in kernel order (BH, T_rows, D)
+  const void* x0_tiled;  // DQ gather mode: Q already in kernel order (BH, T_rows, D): tiled loads, only dO gathered
   const void* o_src;   // DQ: O rows (same addressing as dO) for the fused delta = rowsum(dO * O)
   float* delta_out;    // DQ: delta per query slot (BH, T_rows_pad)
   const uint16_t* list;

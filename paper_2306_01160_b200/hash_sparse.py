@@ -8,6 +8,7 @@ lists and the tcgen05 kernels; the inverse permutation routes outputs back.
 """
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -210,7 +211,11 @@ def _permute3(xs, ranks, T_perm):
 
 _PREP_MAX_T = 16384
 _Q_WRITEOUT = True  # forward gathers Q and writes the bucket-order copy (see _fwd_bwd)
-_DO_WRITEOUT = True  # dQ gathers Q / dO, fuses delta, writes the bucket-order dO copy (two-pass backward)
+_DO_WRITEOUT = True
+# dQ reads Q tiled from the forward's kernel-order copy (only dO through the row table);
+# SCFA_DQ_Q_SORTED=0 gathers both (A/B)
+_DQ_Q_SORTED = os.environ.get("SCFA_DQ_Q_SORTED", "1") != "0"
+  # dQ gathers Q / dO, fuses delta, writes the bucket-order dO copy (two-pass backward)
 
 
 def _event_ptr(ev):
@@ -511,7 +516,7 @@ def _hash_backward_stage(st, d_out):
         # bucket order for dK/dV: no separate delta / dO pass
         xdo = torch.empty_like(st.xq)
         dq, delta = dq_backward_gathered(prob, st.q, st.xk, st.xv, st.outputs, d_out, st.q_only, st.scale, st.T_Q,
-                                         xdo)
+                                         xdo, q_sorted=st.xq if _DQ_Q_SORTED else None)
         dk, dv = dkdv_backward_sorted(prob, st.xq, st.xk, st.xv, xdo, st.outputs._lse2, delta, st.scale, st.T_KV)
         return dq, dk, dv
     shared = sb.q_rank is not None and sb.k_rank is sb.q_rank

@@ -428,8 +428,10 @@ def _qk_backward_stage(st, d_out):
         raise ShapeError(f"dO shape {tuple(d_b.shape)} != Q shape {tuple(st.q.shape)}")
     if st.q_only is not None:
         xdo = torch.empty_like(st.xq)
+        from .hash_sparse import _DQ_Q_SORTED
+
         dq, delta = dq_backward_gathered(prob, st.q, prep.k_c, prep.v_c, st.outputs, d_b, st.q_only, st.scale,
-                                         st.T_Q, xdo)
+                                         st.T_Q, xdo, q_sorted=st.xq if _DQ_Q_SORTED else None)
         dk, dv = dkdv_backward_sorted(prob, st.xq, prep.k_c, prep.v_c, xdo, st.outputs._lse2, delta, st.scale,
                                       st.T_KV, out_rows=prob.rows.k_rows if st.static else None)
     else:
