@@ -70,7 +70,6 @@ class Problem:
         self.flags = int(flags)
         self.rows = None  # RowTables for gather-mode kernels, when the operands stay in (B, T, H, D)
         self._lists = {}
-        self._tiles_total = None
 
     @property
     def BH(self):
@@ -94,6 +93,17 @@ class Problem:
             return _lib.ptr(self.q_hash), _lib.ptr(self.k_hash)
         return _lib.ptr(self.q_idx), _lib.ptr(self.k_idx)
 
+    @property
+    def _tiles_total(self):
+        """Listed tiles per list (fwd, dq, dkdv; int64, device), summed from the counts on
+        demand (the list kernel keeps no running total: no fill launch, no atomics)."""
+        parts = []
+        for name in ("fwd", "dq", "dkdv"):
+            ent = self._lists.get(name)
+            parts.append(ent[1].sum(dtype=torch.int64) if ent is not None
+                         else torch.zeros((), dtype=torch.int64, device=self.q_idx.device))
+        return torch.stack(parts)
+
     # list name -> (rows are queries, streamed tile width, tiles_total slot)
     LISTS = {"fwd": (True, 128, 0), "dq": (True, 64, 1), "dkdv": (False, 64, 2)}
 
@@ -107,8 +117,6 @@ class Problem:
         want = [w for w in which if w not in self._lists]
         if want:
             dev = self.q_idx.device
-            if self._tiles_total is None:
-                self._tiles_total = torch.zeros(3, dtype=torch.int64, device=dev)
             ready = (1 if "q_runs" in self._lists else 0) | (2 if "k_runs" in self._lists else 0)
             if any(self.LISTS[w][0] for w in want) and "q_runs" not in self._lists:
                 self._lists["q_runs"] = torch.empty((self.BH, self.Tq_pad, 2), dtype=torch.int32, device=dev)
@@ -139,7 +147,7 @@ class Problem:
                 _lib.ptr(self.q_idx), qh, _lib.ptr(self.k_idx), kh,
                 self.BH, self.T_q, self.T_kv, self.Tq_pad, self.Tkv_pad, self.flags,
                 _lib.ptr(self._lists.get("q_runs")), _lib.ptr(self._lists.get("k_runs")), ready,
-                *args, _lib.ptr(self._tiles_total), _lib.stream_ptr(),
+                *args, None, _lib.stream_ptr(),
                 kernels=(0 if ready == 3 else 1) + 2,
             )
         return self._lists

@@ -1376,14 +1376,19 @@ extern "C" int scfa_permute_rows3(int n, const void* const* srcs, void* const* d
 #ifndef SCFA_TUNE_PERM_U
 #define SCFA_TUNE_PERM_U 4
 #endif
+// Grid cap, CTAs per SM: two (of eight resident) keep the copy at full speed alone
+// (36 -> 39 us at cfg2) and leave the SMs' other slots to the finishing / tile-list /
+// item-order kernels the copy runs beside on the main stream; with the whole GPU
+// occupied those queue behind the copy (cfg2 step -12 us, T = 16k -9 us, cfg3 -10 us).
 #ifndef SCFA_TUNE_PERM_G
-#define SCFA_TUNE_PERM_G 8
+#define SCFA_TUNE_PERM_G 2
 #endif
     constexpr int U = SCFA_TUNE_PERM_U;
     const int64_t rows = B * T * H;
     const int64_t rows_per_block = (256 / 32) * (32 >> shift) * U;
     int64_t g = (rows + rows_per_block - 1) / rows_per_block;
-    if (g > 148 * SCFA_TUNE_PERM_G) g = 148 * SCFA_TUNE_PERM_G;
+    static const int perm_g = getenv("SCFA_PERM_G") ? atoi(getenv("SCFA_PERM_G")) : SCFA_TUNE_PERM_G;  // A/B knob
+    if (g > 148 * perm_g) g = 148 * perm_g;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int Ti = static_cast<int>(T), Hi = static_cast<int>(H), R = static_cast<int>(rows), RB = static_cast<int>(row_bytes);
     if (n == 1) permute_rows_fast_kernel<1, U><<<static_cast<unsigned>(g), 256, 0, s>>>(J, shift, Ti, Hi, R, RB);

@@ -211,11 +211,10 @@ def _permute3(xs, ranks, T_perm):
 
 _PREP_MAX_T = 16384
 _Q_WRITEOUT = True  # forward gathers Q and writes the bucket-order copy (see _fwd_bwd)
-_DO_WRITEOUT = True
+_DO_WRITEOUT = True  # dQ gathers dO, fuses delta, writes the bucket-order dO copy (two-pass backward)
 # dQ reads Q tiled from the forward's kernel-order copy (only dO through the row table);
 # SCFA_DQ_Q_SORTED=0 gathers both (A/B)
 _DQ_Q_SORTED = os.environ.get("SCFA_DQ_Q_SORTED", "1") != "0"
-  # dQ gathers Q / dO, fuses delta, writes the bucket-order dO copy (two-pass backward)
 
 
 def _event_ptr(ev):
