@@ -112,7 +112,7 @@ struct ListJob {
   uint16_t* list;    // (BH, n_rb, stride)
   int32_t* count;    // (BH, n_rb)
   int64_t stride;
-  int T_rows, T_rows_pad, n_rb, n_cb, col_block;
+  int T_rows, T_rows_pad, n_rb, n_cb, col_block, col_shift;  // col_block = 1 << col_shift
 };
 
 struct ListJobs {
@@ -132,16 +132,18 @@ struct ListJobs {
 // tile_list_kernel's.
 __global__ void __launch_bounds__(128) tile_list_warp_kernel(const __grid_constant__ ListJobs jobs, int n_rb_max) {
   const int lane = threadIdx.x & 31;
-  const int64_t w = static_cast<int64_t>(blockIdx.x) * 4 + (threadIdx.x >> 5);
-  const int64_t per_z = static_cast<int64_t>(jobs.BH) * n_rb_max;
-  const int z = static_cast<int>(w / per_z);
+  // 32-bit index math (3 * BH * n_rb < 2^31, checked by the launcher); column blocks are
+  // powers of two, so the block of a column is a shift
+  const int w = static_cast<int>(blockIdx.x) * 4 + (threadIdx.x >> 5);
+  const int per_z = jobs.BH * n_rb_max;
+  const int z = w / per_z;
   if (z >= 3) return;
-  const int64_t rem = w - z * per_z;
-  const int bh = static_cast<int>(rem / n_rb_max), rb = static_cast<int>(rem - static_cast<int64_t>(bh) * n_rb_max);
+  const int rem = w - z * per_z;
+  const int bh = rem / n_rb_max, rb = rem - bh * n_rb_max;
   const ListJob& J = jobs.job[z];
   if (J.list == nullptr || rb >= J.n_rb) return;
   if (rb == 0 && bh == 0 && lane < 2) J.count[static_cast<int64_t>(jobs.BH) * J.n_rb + lane] = 0;
-  const int B = J.col_block, n_cb = J.n_cb;
+  const int B = J.col_block, sh = J.col_shift, n_cb = J.n_cb;
   // rows 4 * lane .. 4 * lane + 3 of the block, in order
   int lo[4], hi[4];
   bool ne[4];
@@ -151,10 +153,10 @@ __global__ void __launch_bounds__(128) tile_list_warp_kernel(const __grid_consta
     const int row = rb * kRowBlock + 4 * lane + i;
     const int2 r = (row < J.T_rows_pad) ? J.runs[static_cast<int64_t>(bh) * J.T_rows_pad + row] : make_int2(0, 0);
     ne[i] = r.y > r.x;
-    lo[i] = ne[i] ? r.x / B : 0;
-    hi[i] = ne[i] ? (r.y - 1) / B + 1 : 0;
-    my_full_lo = max(my_full_lo, ne[i] ? (r.x + B - 1) / B : 0);
-    my_full_hi = min(my_full_hi, ne[i] ? r.y / B : 0);
+    lo[i] = ne[i] ? r.x >> sh : 0;
+    hi[i] = ne[i] ? ((r.y - 1) >> sh) + 1 : 0;
+    my_full_lo = max(my_full_lo, ne[i] ? (r.x + B - 1) >> sh : 0);
+    my_full_hi = min(my_full_hi, ne[i] ? r.y >> sh : 0);
   }
   const int flo = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(my_full_lo)));
   const int fhi = static_cast<int>(__reduce_min_sync(0xffffffffu, static_cast<unsigned>(my_full_hi)));
@@ -451,6 +453,7 @@ extern "C" int scfa_build_schedule(const int32_t* q_idx, const int32_t* q_hash, 
     J.n_rb = static_cast<int>((T_rows + 127) / 128);
     J.n_cb = static_cast<int>(n_cb);
     J.col_block = B;
+    J.col_shift = (B == 128) ? 7 : 6;
     return SCFA_OK;
   };
   int rc = set(0, q_runs, list_fwd, count_fwd, stride_fwd, T_q, Tq_pad, n_cb128_k, 128);
@@ -477,6 +480,10 @@ extern "C" int scfa_build_schedule(const int32_t* q_idx, const int32_t* q_hash, 
       tile_list_kernel<<<grid, 128, 0, s>>>(jobs);
     } else {
       const int64_t warps = 3 * BH * n_rb;
+      if (warps >= (1LL << 31) - 4) {
+        set_error("schedule: too many (slice, row block) items for the list kernel");
+        return SCFA_ERR_SHAPE;
+      }
       tile_list_warp_kernel<<<static_cast<unsigned>((warps + 3) / 4), 128, 0, s>>>(jobs, n_rb);
     }
     // the longest items first (count buffers hold the order after the work-counter pair)
