@@ -494,6 +494,7 @@ SCFA_DEVICE void radix_pass(PrepSmem& S, const int32_t* key, int T, int shift, c
 struct OrderJobs {
   OrderJob job[3];
   int BH;
+  int cap;  // items per shared-memory array (the largest sorted list)
 };
 
 __global__ void __launch_bounds__(kSortThreads) item_order_kernel(const __grid_constant__ OrderJobs J) {
@@ -508,7 +509,7 @@ __global__ void __launch_bounds__(kSortThreads) item_order_kernel(const __grid_c
     const int rb = o.n_rb - 1 - w / J.BH, bh = w - (w / J.BH) * J.BH;
     return bh * o.n_rb + rb;
   };
-  if (n > kPrepMaxT || !o.lpt) {
+  if (n > J.cap || !o.lpt) {
     for (int w = threadIdx.x; w < n; w += blockDim.x) {
       const int it = item_of(w);
       order[2 * w] = it;
@@ -516,7 +517,7 @@ __global__ void __launch_bounds__(kSortThreads) item_order_kernel(const __grid_c
     }
     return;
   }
-  int32_t* sorted = key + kPrepMaxT;
+  int32_t* sorted = key + J.cap;
   for (int w = threadIdx.x; w < n; w += blockDim.x) key[w] = 255 - min(o.count[item_of(w)], 255);
   __syncthreads();
   radix_pass(S, key, n, 0, nullptr, sorted, nullptr, nullptr);  // stable: equal counts keep their order
@@ -529,13 +530,19 @@ __global__ void __launch_bounds__(kSortThreads) item_order_kernel(const __grid_c
 
 int launch_item_order(const OrderJob* jobs, int n_jobs, int BH, cudaStream_t stream) {
   OrderJobs J{};
-  for (int i = 0; i < n_jobs && i < 3; ++i) J.job[i] = jobs[i];
+  int cap = 0;  // shared memory sized for the lists actually sorted (at most kPrepMaxT items)
+  for (int i = 0; i < n_jobs && i < 3; ++i) {
+    J.job[i] = jobs[i];
+    const int n = BH * jobs[i].n_rb;
+    if (jobs[i].count && jobs[i].lpt && n <= kPrepMaxT && n > cap) cap = n;
+  }
   J.BH = BH;
-  const size_t smem = sizeof(PrepSmem) + 2 * kPrepMaxT * sizeof(int32_t);
+  J.cap = (cap + 31) & ~31;
+  const size_t smem = sizeof(PrepSmem) + 2 * static_cast<size_t>(J.cap) * sizeof(int32_t);
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(item_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
-        cudaSuccess)
+    if (cudaFuncSetAttribute(item_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(sizeof(PrepSmem) + 2 * kPrepMaxT * sizeof(int32_t))) != cudaSuccess)
       return SCFA_ERR_CUDA;
     attr = true;
   }
