@@ -424,7 +424,7 @@ class _HashState:
 
 
 def _hash_forward_stage(q, k, v, q_hash, k_hash, scale=None, exclude_self=True, row_tables=False,
-                        single_pass=False):
+                        single_pass=False, q_ready=None):
     """Preparation + forward of the boundary-layout hash path; returns a _HashState.
 
     Default (shared ids): Q / K / V are put in bucket order without copy passes for Q:
@@ -437,7 +437,12 @@ def _hash_forward_stage(q, k, v, q_hash, k_hash, scale=None, exclude_self=True, 
     Nothing here synchronises with the host: bad bucket ids (sort kernels) and non-finite
     outputs (forward) are flagged in the device word st.err, which the caller reads once
     its launches are queued (check_status).
+    q_ready: an event after which Q's data is on the device (the host-streaming call uploads Q
+    after the ids, K and V; the preparation needs only Q's shape, so only the forward waits).
     """
+    if q_ready is not None and (q.dtype != torch.bfloat16 or not q.is_contiguous()):
+        torch.cuda.current_stream(q.device).wait_event(q_ready)  # as_operand converts: it reads Q
+        q_ready = None
     q, k, v = as_operand(q), as_operand(k), as_operand(v)
     sorted_ev = torch.cuda.Event() if not row_tables else None
     err = torch.zeros(1, dtype=torch.int32, device=q.device)
@@ -452,6 +457,8 @@ def _hash_forward_stage(q, k, v, q_hash, k_hash, scale=None, exclude_self=True, 
     if row_tables:
         st.xq, st.xk, st.xv = q, k, v
         prob.schedule("fwd", "dq", "dkdv")  # runs + all three tile lists in one pass
+        if q_ready is not None:
+            torch.cuda.current_stream(q.device).wait_event(q_ready)
         st.outputs = attention_forward(prob, q, k, v, scale, boundary=(st.T_Q, False), rows=st.rows, err=err)
         return st
     main = torch.cuda.current_stream(q.device)
@@ -462,6 +469,8 @@ def _hash_forward_stage(q, k, v, q_hash, k_hash, scale=None, exclude_self=True, 
     else:
         side.wait_stream(main)
     q_writeout = prob.rows is not None and shared and st.T_Q == st.T_KV and _Q_WRITEOUT
+    if q_ready is not None and not q_writeout:
+        side.wait_event(q_ready)  # the side stream copies Q too
     with torch.cuda.stream(side):
         if q_writeout:
             xk, xv = _permute3([k, v], [sb.k_rank, sb.k_rank], st.T_KV)
@@ -474,6 +483,8 @@ def _hash_forward_stage(q, k, v, q_hash, k_hash, scale=None, exclude_self=True, 
     st.single_pass = bool(single_pass and q_writeout and q.shape[3] == 64)
     prob.schedule(*(("fwd", "dkdv") if st.single_pass else ("fwd", "dq", "dkdv")))
     main.wait_stream(side)
+    if q_ready is not None:
+        main.wait_event(q_ready)
     for t in (xq, xk, xv):
         if t is not None:
             t.record_stream(main)
@@ -622,19 +633,26 @@ def _fwd_bwd_host(q, k, v, q_hash, k_hash, d_out, scale, exclude_self, out, chec
         sl = slice(b, b + 1)
         with torch.cuda.stream(h2d):
             _mark(f"h2d{b}", h2d)
-            xs = [t[sl].to(dev, non_blocking=True) for t in (q, k, v, q_hash)]
-            kh = xs[3] if same else k_hash[sl].to(dev, non_blocking=True)
+            # ids, K, V first: the sort, the K / V permute and the tile lists run while Q
+            # is still on its way (the forward alone waits for it)
+            ids, xk, xv = (t[sl].to(dev, non_blocking=True) for t in (q_hash, k, v))
+            kh = ids if same else k_hash[sl].to(dev, non_blocking=True)
+            ready_p = torch.cuda.Event()
+            ready_p.record(h2d)
+            xq = q[sl].to(dev, non_blocking=True)
+            xs = [xq, xk, xv, ids]
             ready_f = torch.cuda.Event()
             ready_f.record(h2d)
             do_b = d_out[sl].to(dev, non_blocking=True)
             ready_b = torch.cuda.Event()
             ready_b.record(h2d)
             _mark(f"h2d{b}-end", h2d)
-        comp.wait_event(ready_f)
+        comp.wait_event(ready_p)
         for t in xs + [kh, do_b]:
             t.record_stream(comp)
         _mark(f"fwd{b}", comp)
-        st = _hash_forward_stage(xs[0], xs[1], xs[2], xs[3], kh, scale, exclude_self, single_pass=single_pass)
+        st = _hash_forward_stage(xs[0], xs[1], xs[2], xs[3], kh, scale, exclude_self, single_pass=single_pass,
+                                 q_ready=ready_f)
         fwd_done = torch.cuda.Event()
         fwd_done.record(comp)
         with torch.cuda.stream(d2h):
