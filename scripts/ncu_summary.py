@@ -98,7 +98,8 @@ def main():
                     f = float(v.replace(",", ""))
                     unit = units[col[m]] if m in col else ""
                     if m == "gpu__time_duration.sum":  # to microseconds whatever ncu chose
-                        f *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(unit, 1.0)
+                        f *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6,
+                              "s": 1e6}.get(unit, 1.0)
                     elif m.startswith("dram__bytes"):  # to MB
                         f *= {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(unit, 1.0)
                     vals.append(f"{f:.1f}")
