@@ -135,6 +135,30 @@ def test_hash_host_streaming_out_buffers(D, pinned):
         assert torch.equal(a, b.cpu())
 
 
+@pytest.mark.parametrize("fp32,distinct", [(True, False), (False, True), (True, True)])
+def test_hash_host_streaming_q_uploaded_last(fp32, distinct):
+    """The host-buffer call uploads Q after the ids, K and V and lets the preparation run
+    under Q's upload: the paths that read Q before the forward (fp32 inputs converted by
+    as_operand; separate query / key ids, where Q is copied into bucket order on the side
+    stream) must wait for it.  Sized so Q's upload outlasts the preparation."""
+    B, H, T, D, nb = 2, 12, 4096, 64, 16
+    rng = np.random.default_rng(23)
+    dt = torch.float32 if fp32 else torch.bfloat16
+    x = [torch.from_numpy(rng.standard_normal((B, T, H, D)).astype(np.float32)).to(torch.bfloat16).to(dt)
+         for _ in range(4)]
+    hq = torch.from_numpy(scfa.random_buckets(B, T, H, nb, 5))
+    hk = torch.from_numpy(scfa.random_buckets(B, T, H, nb, 6)) if distinct else hq
+    dev = [t.cuda() for t in x]
+    want = scfa.hash_sparse_attention_fwd_bwd(dev[0], dev[1], dev[2], hq.cuda(), hk.cuda() if distinct else hq.cuda(),
+                                              dev[3])
+    host = [t.pin_memory() for t in x]
+    got = scfa.hash_sparse_attention_fwd_bwd(host[0], host[1], host[2], hq, hk, host[3])
+    torch.cuda.synchronize()
+    for a, b in zip(got, want):
+        assert not a.is_cuda
+        assert torch.equal(a, b.cpu())
+
+
 @pytest.mark.parametrize("mode", ["hash", "qk"])
 def test_autograd_matches_fused_fwd_bwd(mode):
     """dynamic_sparse_attention under autograd: same O and gradients as the *_fwd_bwd calls."""
