@@ -81,6 +81,9 @@ enum Mode : int { MODE_FWD = 0, MODE_DQ = 1, MODE_DKDV = 2, MODE_BWD = 3 };
 #ifndef SCFA_TUNE_QE
 #define SCFA_TUNE_QE 3
 #endif
+#ifndef SCFA_TUNE_DQ_SPLIT_SDP
+#define SCFA_TUNE_DQ_SPLIT_SDP 1
+#endif
 
 template <int kMode, int kD>
 struct Cfg {
@@ -101,6 +104,9 @@ struct Cfg {
   static constexpr bool KEYS = (kMode == MODE_DKDV || kMode == MODE_BWD);  // key-stationary
   static constexpr bool ALT = KEYS || (kMode == MODE_DQ && kD == 128);
   static constexpr int NSTREAM = ALT ? 1 : ((kD == 64) ? 2 : 1);
+  // dQ (two streams): S and dP committed separately (s_full, then s_full + 1), so the rows
+  // compute a tile's first P chunk from S while the dP MMAs still run
+  static constexpr bool SDP_SPLIT = SCFA_TUNE_DQ_SPLIT_SDP && kMode == MODE_DQ && !ALT;
   static constexpr int THREADS = 512;
   static constexpr int BM = 128;                             // stationary rows per work item
   static constexpr int BN = (kMode == MODE_FWD) ? 128 : 64;  // streamed rows per tile
@@ -1000,7 +1006,7 @@ __global__ void __launch_bounds__(512, 1)
               } else {
                 umma_ss(tmem + j * C::TM_BUF + C::TM_S, make_sdesc_sw128(a, 16, 1024), make_sdesc_sw128(b, 16, 1024),
                         idesc_s, k > 0);
-                if (kMode != MODE_FWD) {
+                if (kMode != MODE_FWD && !C::SDP_SPLIT) {
                   const uint32_t a1 = x1_addr + (k >> 2) * (C::BM * 128) + koff;
                   const uint32_t b1 = y1_addr + (k >> 2) * (C::BN * 128) + koff;
                   umma_ss(tmem + j * C::TM_BUF + C::TM_DP, make_sdesc_sw128(a1, 16, 1024),
@@ -1008,7 +1014,19 @@ __global__ void __launch_bounds__(512, 1)
                 }
               }
             }
-          umma_commit(bar_s_full + j);
+          if constexpr (C::SDP_SPLIT) {
+            umma_commit(bar_s_full);  // S complete: the rows start on P
+#pragma unroll
+            for (int k = 0; k < kD / 16; ++k) {
+              const uint32_t koff = (k & 3) * 32;
+              const uint32_t a1 = x1_addr + (k >> 2) * (C::BM * 128) + koff;
+              const uint32_t b1 = y1_addr + (k >> 2) * (C::BN * 128) + koff;
+              umma_ss(tmem + C::TM_DP, make_sdesc_sw128(a1, 16, 1024), make_sdesc_sw128(b1, 16, 1024), idesc_s, k > 0);
+            }
+            umma_commit(bar_s_full + 1);  // dP complete
+          } else {
+            umma_commit(bar_s_full + j);
+          }
           if (C::Y0_EARLY) umma_commit(bar_y0_empty + s0);
           if (C::Y1_EARLY) umma_commit(bar_y1_empty + s1);
           }
@@ -1395,6 +1413,8 @@ __global__ void __launch_bounds__(512, 1)
           } else {
             run_mask<NW>(run.x - col0, run.y - col0, vis);
           }
+          bool dp_ok = false;  // SDP_SPLIT: this tile's dP commit waited for
+          (void)dp_ok;
           // 32-column chunks: read S and dP, compute P (and dS), store them over the
           // columns already read (chunk k's P / dS land in columns [16k, 16k+16) of S / dP)
 #pragma unroll
@@ -1412,6 +1432,53 @@ __global__ void __launch_bounds__(512, 1)
                 pk_p[i] = 0u;
                 pk_ds[i] = 0u;
               }
+            } else if constexpr (C::SDP_SPLIT) {
+            // dQ: P from S first; dP (its own commit) is waited for once per tile, after the
+            // first loaded chunk's exponentials
+            float sv[32], dv[32];
+            auto p_in_place = [&]() {
+#pragma unroll
+              for (int c = 0; c < 32; c += 2) {
+                float p0, p1;
+                fma2(p0, p1, sv[c], sv[c + 1], sl, sl, my_nlse, my_nlse);
+                p0 = ex2(p0);
+                p1 = ex2(p1);
+                const uint32_t wv = vis[(cc + c) >> 5];
+                sv[c] = ((wv >> ((cc + c) & 31)) & 1u) ? p0 : 0.f;
+                sv[c + 1] = ((wv >> ((cc + c + 1) & 31)) & 1u) ? p1 : 0.f;
+              }
+            };
+            if (cc == 0) {
+              tmem_ld32(t_sb + cc, *reinterpret_cast<uint32_t(*)[32]>(sv));
+              tmem_wait_ld();
+              p_in_place();
+              mbar_wait(bar_s_full + 1, tg & 1);
+              tc_fence_after();
+              dp_ok = true;
+              tmem_ld32(t_dpb + cc, *reinterpret_cast<uint32_t(*)[32]>(dv));
+              tmem_wait_ld();
+            } else {
+              if (!dp_ok) {
+                mbar_wait(bar_s_full + 1, tg & 1);
+                tc_fence_after();
+                dp_ok = true;
+              }
+              tmem_ld32(t_sb + cc, *reinterpret_cast<uint32_t(*)[32]>(sv));
+              tmem_ld32(t_dpb + cc, *reinterpret_cast<uint32_t(*)[32]>(dv));
+              tmem_wait_ld();
+              p_in_place();
+            }
+            if (C::OVERLAP && cc + 32 == C::BN) {
+              tc_fence_before();
+              mbar_arrive(bar_s_free);
+            }
+#pragma unroll
+            for (int c = 0; c < 32; c += 2) {
+              float d0, d1;
+              add2(d0, d1, dv[c], dv[c + 1], my_ndelta, my_ndelta);
+              mul2(d0, d1, d0, d1, sv[c], sv[c + 1]);
+              pk_ds[c >> 1] = pack_bf16(d0, d1);
+            }
             } else {
             float sv[32], dv[32];
             tmem_ld32(t_sb + cc, *reinterpret_cast<uint32_t(*)[32]>(sv));
