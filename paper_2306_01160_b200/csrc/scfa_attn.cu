@@ -84,6 +84,9 @@ enum Mode : int { MODE_FWD = 0, MODE_DQ = 1, MODE_DKDV = 2, MODE_BWD = 3 };
 #ifndef SCFA_TUNE_DQ_SPLIT_SDP
 #define SCFA_TUNE_DQ_SPLIT_SDP 1
 #endif
+#ifndef SCFA_TUNE_DKDV_SPLIT_SDP
+#define SCFA_TUNE_DKDV_SPLIT_SDP 0
+#endif
 
 template <int kMode, int kD>
 struct Cfg {
@@ -104,9 +107,6 @@ struct Cfg {
   static constexpr bool KEYS = (kMode == MODE_DKDV || kMode == MODE_BWD);  // key-stationary
   static constexpr bool ALT = KEYS || (kMode == MODE_DQ && kD == 128);
   static constexpr int NSTREAM = ALT ? 1 : ((kD == 64) ? 2 : 1);
-  // dQ (two streams): S and dP committed separately (s_full, then s_full + 1), so the rows
-  // compute a tile's first P chunk from S while the dP MMAs still run
-  static constexpr bool SDP_SPLIT = SCFA_TUNE_DQ_SPLIT_SDP && kMode == MODE_DQ && !ALT;
   static constexpr int THREADS = 512;
   static constexpr int BM = 128;                             // stationary rows per work item
   static constexpr int BN = (kMode == MODE_FWD) ? 128 : 64;  // streamed rows per tile
@@ -143,6 +143,12 @@ struct Cfg {
   // 32 instead of 48 clk per N = 64 MMA, scripts/mma_issue.cu) — which leaves room for
   // two S / dP buffers, not three
   static constexpr bool KV_TMEM = SCFA_TUNE_KV_TMEM && (kMode == MODE_DKDV && kD == 64);
+  // S and dP committed separately, so the rows compute a tile's first P chunk from S while
+  // the dP MMAs still run: dQ (two streams; dP completes on s_full + 1) and dK/dV at D = 64
+  // (Sᵀ / dPᵀ from TMEM-resident K / V; dPᵀ of buffer j completes on dq_full + j, a barrier
+  // the dK/dV pass does not otherwise use)
+  static constexpr bool SDP_SPLIT = (SCFA_TUNE_DQ_SPLIT_SDP && kMode == MODE_DQ && !ALT) ||
+                                    (SCFA_TUNE_DKDV_SPLIT_SDP && kMode == MODE_DKDV && KV_TMEM);
   static constexpr int NBUF = (KV_TMEM || FUSED) ? 2 : ((ALT && 3 * TM_BUF + (KEYS ? 2 * kD : kD) <= 512) ? 3 : 2);
   static constexpr int TM_S = 0;
   static constexpr int TM_DP = (kMode == MODE_FWD) ? 0 : BN;
@@ -1000,9 +1006,11 @@ __global__ void __launch_bounds__(512, 1)
               if (C::KV_TMEM) {  // A = K / V rows in TMEM (16 bf16 = 8 columns per K step)
                 const uint32_t kv = tmem + C::TM_KV + (ia & 1) * kD;
                 umma_ts(tmem + j * C::TM_BUF + C::TM_S, kv + k * 8, make_sdesc_sw128(b, 16, 1024), idesc_s, k > 0);
-                const uint32_t b1 = y1_addr + (k >> 2) * (C::BN * 128) + koff;
-                umma_ts(tmem + j * C::TM_BUF + C::TM_DP, kv + kD / 2 + k * 8, make_sdesc_sw128(b1, 16, 1024), idesc_s,
-                        k > 0);
+                if (!C::SDP_SPLIT) {
+                  const uint32_t b1 = y1_addr + (k >> 2) * (C::BN * 128) + koff;
+                  umma_ts(tmem + j * C::TM_BUF + C::TM_DP, kv + kD / 2 + k * 8, make_sdesc_sw128(b1, 16, 1024),
+                          idesc_s, k > 0);
+                }
               } else {
                 umma_ss(tmem + j * C::TM_BUF + C::TM_S, make_sdesc_sw128(a, 16, 1024), make_sdesc_sw128(b, 16, 1024),
                         idesc_s, k > 0);
@@ -1015,15 +1023,22 @@ __global__ void __launch_bounds__(512, 1)
               }
             }
           if constexpr (C::SDP_SPLIT) {
-            umma_commit(bar_s_full);  // S complete: the rows start on P
+            umma_commit(bar_s_full + j);  // S complete: the rows start on P
 #pragma unroll
             for (int k = 0; k < kD / 16; ++k) {
               const uint32_t koff = (k & 3) * 32;
-              const uint32_t a1 = x1_addr + (k >> 2) * (C::BM * 128) + koff;
               const uint32_t b1 = y1_addr + (k >> 2) * (C::BN * 128) + koff;
-              umma_ss(tmem + C::TM_DP, make_sdesc_sw128(a1, 16, 1024), make_sdesc_sw128(b1, 16, 1024), idesc_s, k > 0);
+              if (C::KV_TMEM) {
+                const uint32_t kv = tmem + C::TM_KV + (ia & 1) * kD;
+                umma_ts(tmem + j * C::TM_BUF + C::TM_DP, kv + kD / 2 + k * 8, make_sdesc_sw128(b1, 16, 1024),
+                        idesc_s, k > 0);
+              } else {
+                const uint32_t a1 = x1_addr + (k >> 2) * (C::BM * 128) + koff;
+                umma_ss(tmem + C::TM_DP, make_sdesc_sw128(a1, 16, 1024), make_sdesc_sw128(b1, 16, 1024), idesc_s,
+                        k > 0);
+              }
             }
-            umma_commit(bar_s_full + 1);  // dP complete
+            umma_commit(C::KEYS ? B.dq_full + j : bar_s_full + 1);  // dP complete
           } else {
             umma_commit(bar_s_full + j);
           }
@@ -1433,14 +1448,20 @@ __global__ void __launch_bounds__(512, 1)
                 pk_ds[i] = 0u;
               }
             } else if constexpr (C::SDP_SPLIT) {
-            // dQ: P from S first; dP (its own commit) is waited for once per tile, after the
-            // first loaded chunk's exponentials
+            // P from S first; dP (its own commit) is waited for once per tile, after the first
+            // loaded chunk's exponentials
             float sv[32], dv[32];
+            const MBar dp_full = C::KEYS ? B.dq_full + jb : bar_s_full + 1;
+            const uint32_t dp_par = C::ALT ? ((tg / C::NBUF) & 1) : (tg & 1);
             auto p_in_place = [&]() {
 #pragma unroll
               for (int c = 0; c < 32; c += 2) {
-                float p0, p1;
-                fma2(p0, p1, sv[c], sv[c + 1], sl, sl, my_nlse, my_nlse);
+                float p0, p1, n0 = my_nlse, n1 = my_nlse;
+                if (C::KEYS) {
+                  n0 = -clse[cc + c];
+                  n1 = -clse[cc + c + 1];
+                }
+                fma2(p0, p1, sv[c], sv[c + 1], sl, sl, n0, n1);
                 p0 = ex2(p0);
                 p1 = ex2(p1);
                 const uint32_t wv = vis[(cc + c) >> 5];
@@ -1452,14 +1473,14 @@ __global__ void __launch_bounds__(512, 1)
               tmem_ld32(t_sb + cc, *reinterpret_cast<uint32_t(*)[32]>(sv));
               tmem_wait_ld();
               p_in_place();
-              mbar_wait(bar_s_full + 1, tg & 1);
+              mbar_wait(dp_full, dp_par);
               tc_fence_after();
               dp_ok = true;
               tmem_ld32(t_dpb + cc, *reinterpret_cast<uint32_t(*)[32]>(dv));
               tmem_wait_ld();
             } else {
               if (!dp_ok) {
-                mbar_wait(bar_s_full + 1, tg & 1);
+                mbar_wait(dp_full, dp_par);
                 tc_fence_after();
                 dp_ok = true;
               }
@@ -1468,16 +1489,21 @@ __global__ void __launch_bounds__(512, 1)
               tmem_wait_ld();
               p_in_place();
             }
-            if (C::OVERLAP && cc + 32 == C::BN) {
+            if (!C::ALT && C::OVERLAP && cc + 32 == C::BN) {
               tc_fence_before();
               mbar_arrive(bar_s_free);
             }
 #pragma unroll
             for (int c = 0; c < 32; c += 2) {
-              float d0, d1;
-              add2(d0, d1, dv[c], dv[c + 1], my_ndelta, my_ndelta);
+              float d0, d1, n0 = my_ndelta, n1 = my_ndelta;
+              if (C::KEYS) {
+                n0 = -cdelta[cc + c];
+                n1 = -cdelta[cc + c + 1];
+              }
+              add2(d0, d1, dv[c], dv[c + 1], n0, n1);
               mul2(d0, d1, d0, d1, sv[c], sv[c + 1]);
               pk_ds[c >> 1] = pack_bf16(d0, d1);
+              if (C::KEYS) pk_p[c >> 1] = pack_bf16(sv[c], sv[c + 1]);
             }
             } else {
             float sv[32], dv[32];
