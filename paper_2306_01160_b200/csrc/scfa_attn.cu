@@ -300,7 +300,11 @@ SCFA_DEVICE void red_add_v4(float* p, float a, float b, float c, float d) {
 // Which element pairs of a 32-column chunk take the polynomial exp2 (FMA pipe) instead of
 // MUFU.  Measured: none — the loops are issue / latency bound rather than MUFU bound, and
 // the polynomial's extra instructions cost more than the MUFU time they free.
-SCFA_DEVICE constexpr bool kPolyPair(int pair) { return false && (pair & 3) == 3; }
+#ifndef SCFA_TUNE_POLY
+#define SCFA_TUNE_POLY 0
+#endif
+// every SCFA_TUNE_POLY-th exponential pair on the FMA pipe (0: none)
+SCFA_DEVICE constexpr bool kPolyPair(int pair) { return SCFA_TUNE_POLY > 0 && (pair % (SCFA_TUNE_POLY > 0 ? SCFA_TUNE_POLY : 1)) == SCFA_TUNE_POLY - 1; }
 
 SCFA_DEVICE uint32_t bits_below(int n) { return n <= 0 ? 0u : (n >= 32 ? 0xffffffffu : ((1u << n) - 1u)); }
 
