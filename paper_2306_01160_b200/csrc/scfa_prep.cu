@@ -669,6 +669,30 @@ __global__ void __cluster_dims__(kSortCluster, 1, 1) __launch_bounds__(kSortThre
   for (int i = threadIdx.x; i < 256 * 33; i += blockDim.x) (&S.cnt[0][0])[i] = 0;
   __syncthreads();
   atomicMax(&C.mx, static_cast<unsigned long long>(mh));
+  // ---- one counting pass (ids < 256, the common case): per-warp counts over contiguous warp
+  // segments of this quarter.  Counted before the cluster knows the ids' maximum (digits
+  // clamped, so larger ids stay in bounds): the maximum travels with the counts through one
+  // cluster barrier, and a multi-pass slice discards them.
+  const int wseg = (((nloc + 31) / 32) + 31) & ~31;
+  const int w0 = min(nloc, warp * wseg), w1 = min(nloc, w0 + wseg);
+  for (int base = w0; base < w1; base += 32) {
+    const int i = base + lane;
+    const bool act = i < w1;
+    const int d = act ? min(key[i], 255) : 256 + lane;
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    if (act && (peers & lanemask_lt()) == 0) S.cnt[d][warp] += __popc(peers);
+  }
+  __syncthreads();
+  if (threadIdx.x < 256) {  // within-digit warp prefix, this CTA's total per digit
+    const int d = threadIdx.x;
+    int acc = 0;
+    for (int w = 0; w < 32; ++w) {
+      const int c = S.cnt[d][w];
+      S.cnt[d][w] = acc;
+      acc += c;
+    }
+    C.ctot[d] = acc;
+  }
   cluster.sync();
   unsigned long long gmx = 0;
   for (int c = 0; c < kSortCluster; ++c) gmx = max(gmx, cluster.map_shared_rank(&C.mx, c)[0]);
@@ -692,28 +716,6 @@ __global__ void __cluster_dims__(kSortCluster, 1, 1) __launch_bounds__(kSortThre
     if (threadIdx.x == 0) bounds[256] = T;
     return;
   }
-  // ---- one counting pass: per-warp counts over contiguous warp segments of this quarter
-  const int wseg = (((nloc + 31) / 32) + 31) & ~31;
-  const int w0 = min(nloc, warp * wseg), w1 = min(nloc, w0 + wseg);
-  for (int base = w0; base < w1; base += 32) {
-    const int i = base + lane;
-    const bool act = i < w1;
-    const int d = act ? key[i] : 256 + lane;
-    const uint32_t peers = __match_any_sync(0xffffffffu, d);
-    if (act && (peers & lanemask_lt()) == 0) S.cnt[d][warp] += __popc(peers);
-  }
-  __syncthreads();
-  if (threadIdx.x < 256) {  // within-digit warp prefix, this CTA's total per digit
-    const int d = threadIdx.x;
-    int acc = 0;
-    for (int w = 0; w < 32; ++w) {
-      const int c = S.cnt[d][w];
-      S.cnt[d][w] = acc;
-      acc += c;
-    }
-    C.ctot[d] = acc;
-  }
-  cluster.sync();
   int gsum = 0;
   if (threadIdx.x < 256) {
     const int d = threadIdx.x;
