@@ -81,6 +81,9 @@ enum Mode : int { MODE_FWD = 0, MODE_DQ = 1, MODE_DKDV = 2, MODE_BWD = 3 };
 #ifndef SCFA_TUNE_QE
 #define SCFA_TUNE_QE 3
 #endif
+#ifndef SCFA_TUNE_DKDV_PFREE
+#define SCFA_TUNE_DKDV_PFREE 1
+#endif
 #ifndef SCFA_TUNE_DQ_SPLIT_SDP
 #define SCFA_TUNE_DQ_SPLIT_SDP 1
 #endif
@@ -987,7 +990,10 @@ __global__ void __launch_bounds__(512, 1)
           if (kMode != MODE_FWD) mbar_wait_lazy(bar_y1_full + s1, (tg / C::NS1) & 1);
           const int j = C::ALT ? (tg % C::NBUF) : 0;  // TMEM buffer of this tile
           if (C::ALT) {
-            if (tg >= C::NBUF) mbar_wait(bar_p_free + j, ((tg / C::NBUF) - 1) & 1);  // tile tg-NBUF accumulated
+            // tile tg-NBUF accumulated (SCFA_TUNE_DKDV_PFREE=0, dK/dV: not waited for — the
+            // accumulate MMAs were issued earlier by this thread, tcgen05.mma runs in issue order)
+            if (tg >= C::NBUF && (kMode != MODE_DKDV || SCFA_TUNE_DKDV_PFREE))
+              mbar_wait(bar_p_free + j, ((tg / C::NBUF) - 1) & 1);
           } else if (C::OVERLAP) {
             if (tg > 0) mbar_wait_lazy(bar_s_free, (tg - 1) & 1);
           } else if (p_tg >= 0) {
