@@ -108,7 +108,10 @@ struct Cfg {
   // O = (2^(m0-m) O0 + 2^(m1-m) O1) / (2^(m0-m) l0 + 2^(m1-m) l1).
   static constexpr bool SPLIT = (kMode == MODE_FWD && kD == 128);
   static constexpr bool KEYS = (kMode == MODE_DKDV || kMode == MODE_BWD);  // key-stationary
-  static constexpr bool ALT = KEYS || (kMode == MODE_DQ && kD == 128);
+#ifndef SCFA_TUNE_DQ_ALT64
+#define SCFA_TUNE_DQ_ALT64 0
+#endif
+  static constexpr bool ALT = KEYS || (kMode == MODE_DQ && (kD == 128 || SCFA_TUNE_DQ_ALT64));
   static constexpr int NSTREAM = ALT ? 1 : ((kD == 64) ? 2 : 1);
   static constexpr int THREADS = 512;
   static constexpr int BM = 128;                             // stationary rows per work item
