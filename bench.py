@@ -428,10 +428,18 @@ def run_ours(args, cfg):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # diagnostics: SCFA_BENCH_SHARED_GPU=1 runs every rank on cuda:0 over gloo (the N > 1
+    # plumbing exercised on a one-GPU box; the timing then means nothing)
+    shared = world > 1 and os.environ.get("SCFA_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     _lib.require_cuda()
     ctx = Ctx(world, rank, local, dev)
     placement = gpu_local_cpus(local)
@@ -740,7 +748,8 @@ def verify_gather(ctx, res, blocks, qkvd, buckets, cfg):
 
     B, H = cfg["B"], cfg["H"]
     full = gather_units([(blk, rr) for blk, (rr, _) in zip(blocks, res)], B, H)
-    result = {"gathered": "NCCL all_gather of device tensors (O bf16, dQ/dK/dV fp32)", "world": ctx.world}
+    result = {"gathered": f"{dist.get_backend().upper()} all_gather of device tensors (O bf16, dQ/dK/dV fp32)",
+              "world": ctx.world}
     if ctx.rank == 0:
         x = [torch.from_numpy(a).to(ctx.dev, torch.bfloat16) for a in qkvd]
         h = torch.from_numpy(buckets).to(ctx.dev)
