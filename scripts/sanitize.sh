@@ -1,0 +1,12 @@
+#!/bin/bash
+# compute-sanitizer over the smoke call (memcheck, racecheck, synccheck) and memcheck over the
+# golden / reference-API parity / QK preparation GPU tests (needs a GPU).
+mkdir -p gpurun_out
+for tool in memcheck racecheck synccheck; do
+  timeout 900 compute-sanitizer --tool $tool --print-limit 20 \
+    python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/san_smoke_$tool.txt 2>&1
+  echo "smoke $tool rc=$?: $(tail -1 gpurun_out/san_smoke_$tool.txt)"
+done
+timeout 1500 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_gpu_golden.py \
+  tests/test_gpu_api_parity.py tests/test_gpu_qk_prepare.py -q -x -p no:cacheprovider > gpurun_out/san_tests.txt 2>&1
+echo "tests memcheck rc=$?: $(grep -E 'passed|failed' gpurun_out/san_tests.txt | tail -1); $(tail -1 gpurun_out/san_tests.txt)"
