@@ -7,6 +7,8 @@ for tool in memcheck racecheck synccheck; do
     python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/san_smoke_$tool.txt 2>&1
   echo "smoke $tool rc=$?: $(tail -1 gpurun_out/san_smoke_$tool.txt)"
 done
-timeout 1500 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_gpu_golden.py \
-  tests/test_gpu_api_parity.py tests/test_gpu_qk_prepare.py -q -x -p no:cacheprovider > gpurun_out/san_tests.txt 2>&1
+timeout 2000 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_gpu_golden.py \
+  tests/test_gpu_api_parity.py tests/test_gpu_qk_prepare.py tests/test_gpu_api.py tests/test_gpu_attention.py \
+  tests/test_gpu_errors.py tests/test_gpu_schedule.py tests/test_gpu_sharding.py tests/test_lm.py tests/test_lsh.py \
+  -m gpu -q -x -p no:cacheprovider > gpurun_out/san_tests.txt 2>&1
 echo "tests memcheck rc=$?: $(grep -E 'passed|failed' gpurun_out/san_tests.txt | tail -1); $(tail -1 gpurun_out/san_tests.txt)"
