@@ -949,8 +949,15 @@ __global__ void __launch_bounds__(512, 1)
           p_tg = -1;
         }
         mbar_wait_lazy(bar_q_full + qs, (k / C::NQ) & 1);
-        const int2 item = ring[qs];
-        if (lane == 0) mbar_arrive(bar_q_empty + qs);  // one arrival for the MMA warp
+        // lane 0 reads the slot and releases it to the producer (one arrival for the MMA warp);
+        // the other lanes take the item from it, so no lane reads a slot already released
+        int2 item = make_int2(0, 0);
+        if (lane == 0) {
+          item = ring[qs];
+          mbar_arrive(bar_q_empty + qs);
+        }
+        item.x = __shfl_sync(0xffffffffu, item.x, 0);
+        item.y = __shfl_sync(0xffffffffu, item.y, 0);
         if (item.x < 0) break;
         const int n = item.y;
         if (n == 0) continue;

@@ -432,6 +432,7 @@ SCFA_DEVICE void radix_pass(PrepSmem& S, const int32_t* key, int T, int shift, c
     const int d = act ? ((key[src ? src[s] : s] >> shift) & 255) : 256 + lane;
     const uint32_t peers = __match_any_sync(0xffffffffu, d);
     if (act && (peers & lanemask_lt()) == 0) S.cnt[d][warp] += __popc(peers);
+    __syncwarp();  // the next group leader of digit d (another lane) reads this count
   }
   __syncthreads();
   {  // exclusive scan of cnt in (digit, warp) order: 8 entries per thread
@@ -681,6 +682,7 @@ __global__ void __cluster_dims__(kSortCluster, 1, 1) __launch_bounds__(kSortThre
     const int d = act ? min(key[i], 255) : 256 + lane;
     const uint32_t peers = __match_any_sync(0xffffffffu, d);
     if (act && (peers & lanemask_lt()) == 0) S.cnt[d][warp] += __popc(peers);
+    __syncwarp();  // the next group leader of digit d (another lane) reads this count
   }
   __syncthreads();
   if (threadIdx.x < 256) {  // within-digit warp prefix, this CTA's total per digit
