@@ -1135,7 +1135,7 @@ __global__ void __launch_bounds__(512, 1)
       if (nx_item.x < 0) return;
       const int fbh = nx_item.x / args.n_row_blocks, frb = nx_item.x - fbh * args.n_row_blocks;
       const size_t foff = static_cast<size_t>(fbh) * args.T_rows_pad + frb * C::BM + r;
-      nx_e0 = args.list[static_cast<size_t>(nx_item.x) * args.list_stride];
+      nx_e0 = args.list[static_cast<size_t>(nx_item.x) * args.list_stride];  // (an empty item's entry is 0)
       nx_idx = args.x_rows ? args.x_rows[foff] : args.row_idx[foff];
       nx_run = args.row_runs[foff];
     };

@@ -398,8 +398,11 @@ SCFA_DEVICE void ex2_poly2(float& y0, float& y1, float x0, float x1) {
   y1 = __uint_as_float(__float_as_uint(p1) + (__float_as_uint(t1) << 23));
 }
 
+// Named barrier for warps that reach it at different instructions (e.g. the two row
+// warpgroups of the D = 128 forward): the non-.aligned form (bar.sync is barrier.sync.aligned,
+// which requires every participating thread to execute the same instruction).
 SCFA_DEVICE void named_bar_sync(uint32_t id, uint32_t nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 }  // namespace scfa

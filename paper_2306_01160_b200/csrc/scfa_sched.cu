@@ -235,6 +235,7 @@ __global__ void __launch_bounds__(128) tile_list_warp_kernel(const __grid_consta
   }
   if (lane == 0) {
     J.count[static_cast<int64_t>(bh) * J.n_rb + rb] = total;
+    if (total == 0) out[0] = 0;  // the attention kernels prefetch an item's first entry unconditionally
     if (jobs.tiles) atomicAdd(jobs.tiles + z, static_cast<unsigned long long>(total));
   }
 }
@@ -328,6 +329,7 @@ __global__ void __launch_bounds__(128) tile_list_kernel(const __grid_constant__ 
     }
   }
   if (threadIdx.x == blockDim.x - 1) {
+    if (pos == 0) out[0] = 0;  // the attention kernels prefetch an item's first entry unconditionally
     J.count[bh * J.n_rb + rb] = pos;
     if (jobs.tiles) atomicAdd(jobs.tiles + z, static_cast<unsigned long long>(pos));
   }

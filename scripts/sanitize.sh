@@ -15,3 +15,9 @@ timeout 2000 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest
   tests/test_gpu_errors.py tests/test_gpu_schedule.py tests/test_gpu_sharding.py tests/test_lm.py tests/test_lsh.py \
   -m gpu -q -x -p no:cacheprovider > gpurun_out/san_tests.txt 2>&1
 echo "tests memcheck rc=$?: $(grep -E 'passed|failed' gpurun_out/san_tests.txt | tail -1); $(tail -1 gpurun_out/san_tests.txt)"
+timeout 1200 compute-sanitizer --tool synccheck --print-limit 20 python -m pytest tests/test_gpu_golden.py \
+  tests/test_gpu_api_parity.py tests/test_gpu_schedule.py -q -p no:cacheprovider > gpurun_out/san_sync.txt 2>&1
+echo "tests synccheck rc=$?: $(grep -E 'passed|failed' gpurun_out/san_sync.txt | tail -1); $(tail -1 gpurun_out/san_sync.txt)"
+timeout 1200 compute-sanitizer --tool initcheck --print-limit 20 python -m pytest tests/test_gpu_golden.py \
+  tests/test_gpu_api_parity.py -q -p no:cacheprovider > gpurun_out/san_init.txt 2>&1
+echo "tests initcheck rc=$?: $(grep -E 'passed|failed' gpurun_out/san_init.txt | tail -1); $(tail -1 gpurun_out/san_init.txt)"
