@@ -61,7 +61,7 @@ enum Mode : int { MODE_FWD = 0, MODE_DQ = 1, MODE_DKDV = 2, MODE_BWD = 3 };
 #define SCFA_TUNE_NS1_FWD 3
 #endif
 #ifndef SCFA_TUNE_NS0_DQ
-#define SCFA_TUNE_NS0_DQ 3
+#define SCFA_TUNE_NS0_DQ 4
 #endif
 #ifndef SCFA_TUNE_NS1_DQ
 #define SCFA_TUNE_NS1_DQ 2
